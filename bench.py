@@ -1,0 +1,334 @@
+"""bench.py — Paraexp-EBK solve on B200 (driver contract).
+
+One step = one pexp_solve_linear call over config C2 (BASELINE.json configs[1]: Dirichlet
+advection-diffusion, n=4096, P=64 subintervals, s=64 samples, tol=1e-8, fp64): 64 EBK
+evaluations (truncated two-pass SVD, SaI block Arnoldi, projected Pade-13 expm) + 63 batched
+homogeneous legs + superposition.  value = EBK evaluations/s over all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C1|C3|C4|C5]
+
+N>1 (torchrun): "replicas only" — the north star keeps the path on one GPU, so each rank
+solves an independent replica (weak scaling, no data-path collective; the timing max is
+taken over ranks with one all_reduce after the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name):
+    import synth
+    if name == "C2":
+        p = synth.config2()
+        return p, dict(kind="linear", s=p.s, k_max=384)
+    if name == "C1":
+        p = synth.config1()
+        return p, dict(kind="linear", s=p.s, k_max=256)
+    if name == "C4":
+        p = synth.config4()
+        return p, dict(kind="linear", s=p.s, k_max=96)
+    if name == "C3":
+        p = synth.config3()
+        return p, dict(kind="burgers", s=p.s, k_max=256)
+    if name == "C5":
+        p = synth.config5()
+        return p, dict(kind="burgers", s=p.s, k_max=384)
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
+                          and "Not" not in r[4 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(p, cfg, budget_s=20.0):
+    """The oracle as it stands (test infrastructure, never tuned) on a bounded sample of the
+    same workload, on this host's cores."""
+    import oracle
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    t0 = time.perf_counter()
+    if cfg["kind"] == "linear":
+        if p.batch > 1:       # C4: whole problems from the batch
+            k = 0
+            while time.perf_counter() - t0 < budget_s and k < p.batch:
+                oracle.solve_linear(p.n, p.bc, p.nu[k:k + 1], p.a[k:k + 1], p.u0[k:k + 1], p.src[k:k + 1], p.T,
+                                    p.P, p.s, p.tol)
+                k += 1
+            evals, sample = k * p.P, f"{k} of {p.batch} problems, full solves (P={p.P} EBK evals each)"
+        else:
+            k = 1
+            while True:
+                oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol, i_max=k)
+                if time.perf_counter() - t0 > budget_s / 3 or k >= p.P:
+                    break
+                k *= 2
+            t0 = time.perf_counter()
+            oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol, i_max=k)
+            evals, sample = k, f"first {k} of {p.P} subintervals (nonhomogeneous EBK + homogeneous legs, i_max={k})"
+    else:
+        from oracle.wr import wr_map
+        U = np.broadcast_to(p.u0, (p.P, p.s, p.n)).copy()
+        wr_map(U, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol)
+        evals, sample = p.P, "one WR iteration (iteration 1) of the workload"
+    dt = time.perf_counter() - t0
+    return {"value": evals / dt, "unit": "EBK evals/s", "cores": int(cores), "kind": "oracle", "sample": sample,
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p, cfg = workload(args.config)
+    import oracle
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if cfg["kind"] == "linear":
+            oracle.solve_linear(p.n, p.bc, p.nu[:1], p.a[:1], p.u0[:1], p.src[:1], p.T, p.P, p.s, p.tol, i_max=1)
+            evals = 1
+        else:
+            from oracle.wr import wr_map
+            U = np.broadcast_to(p.u0, (min(p.P, 2), p.s, p.n)).copy()
+            wr_map(U, p.u0, p.nu, p.n, p.T * min(p.P, 2) / p.P, min(p.P, 2), p.s, p.tol)
+            evals = min(p.P, 2)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step = float(np.mean(times))
+    val = evals / step
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    sample = ("first subinterval of C2 (1 EBK eval, oracle SaI Krylov at eta=1e-12) per step"
+              if cfg["kind"] == "linear" else "2 subintervals of one WR iteration per step")
+    line = {"impl": "reference", "metric": "EBK evaluations/s (Paraexp-EBK solve)", "value": val,
+            "unit": "EBK evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d).2)",
+            "config": {"workload": args.config, "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "EBK evals/s", "cores": int(cores), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "EBK evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1509_04567_b200 import build
+    build.build()
+    from paper_1509_04567_b200 import pexp
+
+    p, cfg = workload(args.config)
+    linear = cfg["kind"] == "linear"
+    if linear:
+        ctx = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=cfg["s"], k_max=cfg["k_max"])
+        ctx.ensure_workspace(p.P, dev, kind=0)
+        u0_h = torch.tensor(p.u0).pin_memory()
+        src_h = torch.tensor(p.src).pin_memory()
+        out = torch.empty((p.batch, p.P, p.n), dtype=torch.float64, device=dev)
+    else:
+        ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"])
+        ctx.ensure_workspace(p.P, dev, kind=1)
+        u0_h = torch.tensor(p.u0).pin_memory()
+        src_h = None
+        out = torch.empty((p.P, p.n), dtype=torch.float64, device=dev)
+    u0 = u0_h.to(dev)
+    src = src_h.to(dev) if src_h is not None else None
+    out_h = torch.empty(out.shape, dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
+
+    def step():
+        if linear:
+            return ctx.solve_linear(u0, src, p.T, p.P, p.tol, out=out)[1]
+        return ctx.solve_burgers(u0, p.nu, p.T, p.P, p.tol, p.max_wr_iters, out=out)[1]
+
+    for _ in range(args.warmup):
+        st = step()
+    torch.cuda.synchronize()
+    evals_per_step = st["evals"]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    launches = 0
+    pexp.profile_enable(True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = step()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            launches += st["kernel_launches"]
+    prof = pexp.profile_read()
+    pexp.profile_enable(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = float(np.mean(times))
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * evals_per_step / (ms_max / 1e3)
+
+    # ---- end to end through the public API with host buffers (H2D + solve + D2H timed)
+    e2e = None
+    if not args.no_e2e:
+        et = []
+        for _ in range(max(2, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            u0.copy_(u0_h, non_blocking=True)
+            if src is not None:
+                src.copy_(src_h, non_blocking=True)
+            step()
+            out_h.copy_(out, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            et.append(e0.elapsed_time(e1))
+        tm = torch.tensor([float(np.mean(et))], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        h2d = u0_h.numel() * 8 + (src_h.numel() * 8 if src_h is not None else 0)
+        e2e = {"value": world * evals_per_step / (tm.item() / 1e3), "unit": "EBK evals/s",
+               "ms_per_step": tm.item(), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_h.numel() * 8)}
+
+    # ---- roofline of the dominant kernel class (live CUDA-event timing inside the timed region)
+    peaks = json.load(open(MEASURED)) if os.path.exists(MEASURED) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    if dom in ("small_problem", "small_dense"):
+        ach = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] else 0.0
+        roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "derived fp64 FMA peak 148x64x2x1.965GHz (DESIGN.md §8)"}
+    else:
+        ach = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] else 0.0
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    roof["share_of_step"] = d["ms"] / max(1e-9, sum(times))
+    roof["launches_per_step"] = d["launches"] / args.steps
+    classes = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                   "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None,
+                   "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None}
+               for k, v in prof.items()}
+
+    if rank == 0:
+        line = {
+            "metric": "EBK evaluations/s (Paraexp-EBK solve; solve time = ms_per_step)",
+            "value": value, "unit": "EBK evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded generators, SURVEY §8(d).2)",
+            "config": {"workload": args.config, "n": p.n, "bc": p.bc, "P": p.P, "s": p.s, "tol": p.tol,
+                       "batch": getattr(p, "batch", 1), "evals_per_step": evals_per_step,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "max_m": st["max_m"], "max_k": st["max_k"], "wr_iters": st["wr_iters"]},
+            "roofline": roof, "kernel_classes": classes,
+            "gpu_launches": int(launches / args.steps),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(p, cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

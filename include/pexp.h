@@ -1,0 +1,161 @@
+/*
+ * pexp.h — C ABI of the B200-native Paraexp-EBK hot path (arXiv 1509.04567).
+ *
+ * What it computes (PAPER.md = "P:<line>", readings #k = DESIGN.md §3):
+ *   Linear:  u' = A u + g(t), u(0) = u0, A = nu*D2 - a*D1,
+ *            solved by Paraexp superposition (Fig. 2) with one
+ *            exponential-block-Krylov (EBK) evaluation per subinterval:
+ *            truncated SVD of the sampled shifted source, shift-and-invert block
+ *            Arnoldi, projected exponential, superposition of nonhomogeneous and
+ *            homogeneous parts.
+ *   Burgers: u' = nu*D2 u - u∘(D1 u) (f = 0), solved by waveform relaxation
+ *            with per-subinterval averaged Jacobians (§2.4, Fig. 5 P:428-444;
+ *            Eq.(sourceParallel) read as in reading #2).
+ *
+ * Conventions for every call:
+ *   - All array arguments are CALLER-OWNED, fp64, contiguous, last index fastest.
+ *     Pointers documented "dev" are CUDA device pointers; "host" are host pointers.
+ *     The library never frees caller memory.
+ *   - All device work is enqueued on the stream given in pexp_options.stream
+ *     (a cudaStream_t; NULL = legacy default stream).  A pexp_solve_* call returns
+ *     after its work has completed (it synchronises that stream at the end and at
+ *     a few convergence checks).
+ *   - Device scratch comes from the caller: query pexp_workspace_bytes(), allocate
+ *     (e.g. a torch uint8 CUDA tensor), bind with pexp_set_workspace().  The library
+ *     never calls cudaMalloc for scratch.
+ *   - Errors: every call returns a pexp_status; nothing throws across the ABI.
+ *     On error the output arrays are unspecified and pexp_last_error() returns a
+ *     NUL-terminated message owned by the context (valid until the next call on it).
+ *   - Grids (reading #15): periodic x_i = i/n, dx = 1/n; Dirichlet x_i = (i+1)/(n+1),
+ *     dx = 1/(n+1), zero boundary values.  Sample nodes (reading #9): with dT = T/P,
+ *     t_{j,i} = j*dT + i*(dT/(s-1)), j = 0..P-1, i = 0..s-1 (endpoints included).
+ */
+#ifndef PEXP_H
+#define PEXP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PEXP_API __attribute__((visibility("default")))
+#else
+#define PEXP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pexp_ctx pexp_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  PEXP_OK = 0,
+  PEXP_EINVAL = 1,    /* invalid argument (message says which)                        */
+  PEXP_ENOMEM = 2,    /* workspace missing or too small                              */
+  PEXP_ECUDA = 3,     /* a CUDA runtime error (message carries cudaGetErrorString)    */
+  PEXP_ENOCONV = 4,   /* Krylov column cap k_max reached above tolerance              */
+  PEXP_EDIVERGED = 5, /* WR iterate non-finite or its change grew > 1e3x      */
+  PEXP_EPIVOT = 6     /* shift-and-invert factorisation hit a (relatively) zero pivot   */
+} pexp_status;
+
+typedef enum { PEXP_BC_PERIODIC = 0, PEXP_BC_DIRICHLET = 1 } pexp_bc;
+
+/* Method options.  A zero-initialised struct means "defaults". */
+typedef struct {
+  int32_t s;              /* source samples per subinterval, >= 4 (default 32)           */
+  int32_t node_rule;      /* 0 = uniform incl. endpoints (only value supported)         */
+  double svd_tau_factor;  /* truncation tau_svd = factor*tol relative to sigma_1 (0.01)  */
+  double stop_factor;     /* Krylov stop eta = factor*tol (default 0.01)                 */
+  int32_t restart_blocks; /* paper restarts every 20 blocks    */
+  int32_t k_max;          /* Krylov column capacity per evaluation (default 256)         */
+  void* stream;           /* cudaStream_t; NULL = legacy default stream                  */
+  int32_t stop_rule;      /* 0 = shift-and-invert residual ||(I-gamma A)^{-1} r(t)|| (default),
+                             1 = true residual ||r(t)|| = ||A y + U p - y'|| (DESIGN.md §3 #6) */
+} pexp_options;
+
+/* Per-solve statistics (host memory, caller-owned). */
+typedef struct {
+  int32_t wr_iters;        /* WR iterations performed (Burgers), 0 for linear          */
+  double wr_last_delta;    /* last max-norm change delta_k (Burgers)                  */
+  int32_t max_m;           /* largest block width m_j (retained singular values)      */
+  int32_t max_k;           /* largest Krylov dimension reached                          */
+  int32_t restarts;        /* restart cycles performed                                 */
+  double best_residual;    /* worst relative residual at the last check               */
+  float ms_total;          /* device time of the call (CUDA events), ms                */
+  int32_t evals;           /* nonhomogeneous EBK evaluations performed                 */
+  int32_t kernel_launches; /* kernels this library launched during the call            */
+} pexp_stats;
+
+/* Create a context for one spatial operator A = nu*D2 - a*D1 on n points.
+ * n >= 3; nu >= 0; bc periodic or Dirichlet.  opt may be NULL (defaults).
+ * Host-only: no device work.  *ctx is set to NULL on error. */
+PEXP_API pexp_status pexp_create(pexp_ctx** ctx, int64_t n, pexp_bc bc, double nu, double a,
+                        const pexp_options* opt);
+
+/* Batched variant (config C4): `batch` independent problems sharing n and bc, each
+ * with its own nu_host[b] >= 0 and a_host[b] (host arrays of length batch). */
+PEXP_API pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t batch,
+                                const double* nu_host, const double* a_host,
+                                const pexp_options* opt);
+
+PEXP_API void pexp_destroy(pexp_ctx* ctx);
+PEXP_API const char* pexp_last_error(const pexp_ctx* ctx);
+
+/* Sample times t_{j,i} (header comment) written to t_host[j*s + i], length P*s. */
+PEXP_API pexp_status pexp_sample_times(const pexp_ctx* ctx, double T, int32_t P, double* t_host);
+
+/* Bytes of device scratch needed for solves with P subintervals.
+ * kind: 0 = pexp_solve_linear (and the stage entry points), 1 = pexp_solve_burgers,
+ * 2 = the larger of both.  Returns 0 for invalid arguments. */
+PEXP_API size_t pexp_workspace_bytes(const pexp_ctx* ctx, int32_t P, int32_t kind);
+/* Bind caller-owned device scratch (>= pexp_workspace_bytes, 256-byte aligned). */
+PEXP_API pexp_status pexp_set_workspace(pexp_ctx* ctx, void* dev_ptr, size_t bytes);
+
+/* Linear Paraexp-EBK solve (Fig. 2).
+ *   u0  dev [batch][n]          initial state
+ *   src dev [batch][P][s][n]    g(x, t_{j,i}) at the sample nodes (header comment)
+ *   T > 0, P >= 1, 1e-14 <= tol <= 1e-2
+ *   out dev [batch][P][n]       u(T_1), ..., u(T_P)   (reading #12)
+ *   st  host, nullable */
+PEXP_API pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src, double T,
+                              int32_t P, double tol, double* out, pexp_stats* st);
+
+/* Burgers waveform relaxation (Fig. 5); requires a periodic context with
+ * batch 1; the call's nu is used, the context's nu and a are ignored (reading #18).
+ *   u0  dev [n];  out dev [P][n] = u_K(T_1..T_P) after K iterations, K the first k with
+ *   delta_k = max|u_{k+1}-u_k| < 1e-6 (reading #13) or K = max_wr_iters. */
+PEXP_API pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, double T, int32_t P,
+                               double tol, int32_t max_wr_iters, double* out, pexp_stats* st);
+
+/* ---- Stage entry points (same kernels as the solves; used by stage-parity tests) ---- */
+
+/* One batch of shift-and-invert solves (subsystem 1): x = (I - gamma*A_b)^{-1} rhs for
+ * problem b of the context, every column c of rhs dev [ncols][n] -> x dev [ncols][n]. */
+PEXP_API pexp_status pexp_sai_solve(pexp_ctx* ctx, int32_t b, double gamma, const double* rhs,
+                           int32_t ncols, double* x);
+
+/* Truncated SVD stage (subsystem 3) of E sample matrices G dev [E][s][n] (rows = time
+ * samples).  Writes m_host[E] (retained rank), sigma dev [E][s] (singular values,
+ * descending) and the projection P dev [E][s][n] = U U^T G (rank-m part). */
+PEXP_API pexp_status pexp_source_svd(pexp_ctx* ctx, const double* G, int32_t E, double tol,
+                            int32_t* m_host, double* sigma, double* proj);
+
+/* Batched Pade-13 scaling-and-squaring exponential (subsystem 4) of E dense N x N
+ * matrices A dev [E][N][N] (column-major per matrix) -> X dev [E][N][N]. */
+PEXP_API pexp_status pexp_expm_batched(pexp_ctx* ctx, const double* A, int32_t E, int32_t N, double* X);
+
+/* ---- Live per-kernel-class profiler (diagnostics; used by bench.py's roofline) ----
+ * Classes: 0 SaI solve, 1 X^T Y projections/Grams (incl. reduce), 2 tall-skinny combine,
+ * 3 projected problem (Pade-13 expm + chaining + residual), 4 small dense (eig, Cholesky,
+ * one-sided SVD, spline), 5 stencil / assembly / superposition, 6 factorisation.
+ * pexp_profile_enable(1) clears and starts recording CUDA events around every launch
+ * (on the launch stream), with the launch's ALGORITHMIC bytes and flops;
+ * pexp_profile_read() synchronises the device, fills per-class sums (ms, bytes, flops,
+ * launches; arrays of length ncat, host) and clears; returns the number of classes. */
+PEXP_API void pexp_profile_enable(int32_t on);
+PEXP_API int32_t pexp_profile_read(int32_t ncat, double* ms, double* bytes, double* flops, int32_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PEXP_H */

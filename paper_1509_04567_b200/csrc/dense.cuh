@@ -1,0 +1,290 @@
+// dense.cuh — CTA-level dense fp64 linear algebra on small matrices (N <= ~600) held in
+// global memory (L2-resident per-evaluation workspace).  Every routine is called by ALL
+// threads of the CTA and contains the needed __syncthreads().  Column-major storage.
+#pragma once
+#include "common.cuh"
+
+namespace pexp {
+
+// C = alpha*A*B + beta*C ; A: M x K (lda), B: K x N (ldb), C: M x N (ldc); C must not alias.
+// 64x64 output tiles, K-steps of 16 staged in shared memory, 4x4 register tile per thread.
+__device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda,
+                                const double* B, int ldb, double beta, double* C, int ldc) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int t = threadIdx.x, tr = t % 16, tc = t / 16;  // 16 x 16 threads, 4x4 each
+  for (int i0 = 0; i0 < M; i0 += 64)
+    for (int j0 = 0; j0 < N; j0 += 64) {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += 16) {
+        __syncthreads();
+        for (int idx = t; idx < 16 * 64; idx += blockDim.x) {
+          int r = idx % 64, kk = idx / 64;  // A tile: rows i0+r, col k0+kk (coalesced in r)
+          int gi = i0 + r, gk = k0 + kk;
+          As[kk][r] = (gi < M && gk < K) ? A[gi + size_t(gk) * lda] : 0.0;
+          int kb = idx % 16, c = idx / 16;  // B tile: row k0+kb, col j0+c
+          int gkb = k0 + kb, gj = j0 + c;
+          Bs[kb][c] = (gkb < K && gj < N) ? B[gkb + size_t(gj) * ldb] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          double av[4], bv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) av[a] = As[kk][tr + 16 * a];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tc + 16 * b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          int gi = i0 + tr + 16 * a, gj = j0 + tc + 16 * b;
+          if (gi < M && gj < N) {
+            double* c = C + gi + size_t(gj) * ldc;
+            double v = alpha * acc[a][b];
+            if (beta != 0.0) v = fma(beta, *c, v);
+            *c = v;
+          }
+        }
+    }
+  __syncthreads();
+}
+
+// Y = alpha*X + beta*Y (+ gamma*I) on N x N
+__device__ inline void cta_axpby(int N, double alpha, const double* X, int ldx, double beta,
+                                 double* Y, int ldy, double diag_add = 0.0) {
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int i = idx % N, j = idx / N;
+    double v = alpha * X[i + size_t(j) * ldx] + (beta != 0.0 ? beta * Y[i + size_t(j) * ldy] : 0.0);
+    if (i == j) v += diag_add;
+    Y[i + size_t(j) * ldy] = v;
+  }
+  __syncthreads();
+}
+
+__device__ inline void cta_copy(int M, int N, const double* X, int ldx, double* Y, int ldy) {
+  for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) {
+    int i = idx % M, j = idx / M;
+    Y[i + size_t(j) * ldy] = X[i + size_t(j) * ldx];
+  }
+  __syncthreads();
+}
+
+__device__ inline void cta_identity(int N, double* Y, int ldy, double d = 1.0) {
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int i = idx % N, j = idx / N;
+    Y[i + size_t(j) * ldy] = (i == j) ? d : 0.0;
+  }
+  __syncthreads();
+}
+
+// max column abs-sum
+__device__ inline double cta_norm1(int N, const double* A, int lda, double* red) {
+  double mx = 0.0;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < N; ++i) s += fabs(A[i + size_t(j) * lda]);
+    mx = fmax(mx, s);
+  }
+  return block_max(mx, red);
+}
+
+// Blocked right-looking LU with partial pivoting, in place.  piv[k] = row swapped with k.
+// Returns false if a zero pivot was met.
+__device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red) {
+  __shared__ int s_ip;
+  __shared__ double s_pv;
+  __shared__ int s_bad;
+  __shared__ int s_idx[32];
+  if (threadIdx.x == 0) s_bad = 0;
+  constexpr int NBL = 32;
+  for (int k0 = 0; k0 < N; k0 += NBL) {
+    const int kb = min(NBL, N - k0);
+    // --- unblocked panel factorisation of columns k0..k0+kb-1 (rows k0..N-1)
+    for (int k = k0; k < k0 + kb; ++k) {
+      // pivot search
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + threadIdx.x; i < N; i += blockDim.x) {
+        double v = fabs(A[i + size_t(k) * lda]);
+        if (v > best) { best = v; bi = i; }
+      }
+      // reduce (value, index) over block via warps
+      for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = best; s_idx[threadIdx.x >> 5] = bi; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        double b = red[0];
+        int ii = s_idx[0];
+        for (int w = 1; w < nw; ++w) {
+          double ob = red[w];
+          int oi = s_idx[w];
+          if (ob > b || (ob == b && oi < ii)) { b = ob; ii = oi; }
+        }
+        s_ip = ii;
+        piv[k] = ii;
+        if (!(b > 0.0)) s_bad = 1;
+      }
+      __syncthreads();
+      const int ip = s_ip;
+      if (ip != k)
+        for (int j = threadIdx.x; j < N; j += blockDim.x) {
+          double tmp = A[k + size_t(j) * lda];
+          A[k + size_t(j) * lda] = A[ip + size_t(j) * lda];
+          A[ip + size_t(j) * lda] = tmp;
+        }
+      __syncthreads();
+      if (threadIdx.x == 0) s_pv = A[k + size_t(k) * lda];
+      __syncthreads();
+      const double pv = s_pv;
+      const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
+      for (int i = k + 1 + threadIdx.x; i < N; i += blockDim.x) A[i + size_t(k) * lda] *= inv;
+      __syncthreads();
+      // update the rest of the panel
+      const int w = k0 + kb - (k + 1), h = N - (k + 1);
+      for (int idx = threadIdx.x; idx < w * h; idx += blockDim.x) {
+        int i = k + 1 + idx % h, j = k + 1 + idx / h;
+        A[i + size_t(j) * lda] = fma(-A[i + size_t(k) * lda], A[k + size_t(j) * lda], A[i + size_t(j) * lda]);
+      }
+      __syncthreads();
+    }
+    const int rest = N - (k0 + kb);
+    if (rest > 0) {
+      // U12 = L11^{-1} A12 (unit lower), one thread per column
+      for (int j = k0 + kb + threadIdx.x; j < N; j += blockDim.x)
+        for (int i = k0; i < k0 + kb; ++i) {
+          double s = A[i + size_t(j) * lda];
+          for (int p = k0; p < i; ++p) s = fma(-A[i + size_t(p) * lda], A[p + size_t(j) * lda], s);
+          A[i + size_t(j) * lda] = s;
+        }
+      __syncthreads();
+      // A22 -= L21 U12
+      cta_gemm(rest, rest, kb, -1.0, A + (k0 + kb) + size_t(k0) * lda, lda,
+               A + k0 + size_t(k0 + kb) * lda, lda, 1.0, A + (k0 + kb) + size_t(k0 + kb) * lda, lda);
+    }
+  }
+  __syncthreads();
+  return s_bad == 0;
+}
+
+// Solve (LU) X = P B in place on B (N x nrhs), blocked; uses cta_gemm for off-diagonal blocks.
+__device__ inline void cta_lu_solve(int N, const double* LU, int lda, const int* piv, double* B,
+                                    int ldb, int nrhs) {
+  // row interchanges
+  for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
+    for (int k = 0; k < N; ++k) {
+      int ip = piv[k];
+      if (ip != k) {
+        double tmp = B[k + size_t(j) * ldb];
+        B[k + size_t(j) * ldb] = B[ip + size_t(j) * ldb];
+        B[ip + size_t(j) * ldb] = tmp;
+      }
+    }
+  __syncthreads();
+  constexpr int NBL = 32;
+  // forward: unit lower
+  for (int k0 = 0; k0 < N; k0 += NBL) {
+    const int kb = min(NBL, N - k0);
+    for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
+      for (int i = k0; i < k0 + kb; ++i) {
+        double s = B[i + size_t(j) * ldb];
+        for (int p = k0; p < i; ++p) s = fma(-LU[i + size_t(p) * lda], B[p + size_t(j) * ldb], s);
+        B[i + size_t(j) * ldb] = s;
+      }
+    __syncthreads();
+    const int rest = N - (k0 + kb);
+    if (rest > 0)
+      cta_gemm(rest, nrhs, kb, -1.0, LU + (k0 + kb) + size_t(k0) * lda, lda, B + k0, ldb, 1.0,
+               B + k0 + kb, ldb);
+  }
+  // backward: upper
+  for (int k1 = N; k1 > 0; k1 -= NBL) {
+    const int k0 = max(0, k1 - NBL), kb = k1 - k0;
+    for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
+      for (int i = k1 - 1; i >= k0; --i) {
+        double s = B[i + size_t(j) * ldb];
+        for (int p = i + 1; p < k1; ++p) s = fma(-LU[i + size_t(p) * lda], B[p + size_t(j) * ldb], s);
+        B[i + size_t(j) * ldb] = s / LU[i + size_t(i) * lda];
+      }
+    __syncthreads();
+    if (k0 > 0)
+      cta_gemm(k0, nrhs, kb, -1.0, LU + size_t(k0) * lda, lda, B + k0, ldb, 1.0, B, ldb);
+  }
+}
+
+// Pade-13 scaling-and-squaring exponential (Higham 2005), in place on X (N x N, ld = ldx).
+// work: 7 matrices of ld x N.  Returns the number of squarings.
+__device__ inline int cta_expm_pade13(int N, double* X, int ldx, double* work, int ldw, int* piv,
+                                      double* red) {
+  const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                        1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                        670442572800.0,      33522128640.0,       1323241920.0,
+                        40840800.0,          960960.0,            16380.0,
+                        182.0,               1.0};
+  const double theta13 = 5.371920351148152;
+  const size_t W = size_t(ldw) * N;
+  double *A2 = work, *A4 = work + W, *A6 = work + 2 * W, *T1 = work + 3 * W, *T2 = work + 4 * W,
+         *U = work + 5 * W, *V = work + 6 * W;
+  double nrm = cta_norm1(N, X, ldx, red);
+  int s = 0;
+  if (nrm > theta13) s = max(0, (int)ceil(log2(nrm / theta13)));
+  if (s > 0) cta_axpby(N, ldexp(1.0, -s), X, ldx, 0.0, X, ldx);
+  cta_gemm(N, N, N, 1.0, X, ldx, X, ldx, 0.0, A2, ldw);
+  cta_gemm(N, N, N, 1.0, A2, ldw, A2, ldw, 0.0, A4, ldw);
+  cta_gemm(N, N, N, 1.0, A4, ldw, A2, ldw, 0.0, A6, ldw);
+  // U = X [A6 (b13 A6 + b11 A4 + b9 A2) + b7 A6 + b5 A4 + b3 A2 + b1 I]
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int i = idx % N, j = idx / N;
+    size_t o = i + size_t(j) * ldw;
+    T1[o] = b[13] * A6[o] + b[11] * A4[o] + b[9] * A2[o];
+    T2[o] = b[7] * A6[o] + b[5] * A4[o] + b[3] * A2[o] + (i == j ? b[1] : 0.0);
+  }
+  __syncthreads();
+  cta_gemm(N, N, N, 1.0, A6, ldw, T1, ldw, 1.0, T2, ldw);
+  cta_gemm(N, N, N, 1.0, X, ldx, T2, ldw, 0.0, U, ldw);
+  // V = A6 (b12 A6 + b10 A4 + b8 A2) + b6 A6 + b4 A4 + b2 A2 + b0 I
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int i = idx % N, j = idx / N;
+    size_t o = i + size_t(j) * ldw;
+    T1[o] = b[12] * A6[o] + b[10] * A4[o] + b[8] * A2[o];
+    V[o] = b[6] * A6[o] + b[4] * A4[o] + b[2] * A2[o] + (i == j ? b[0] : 0.0);
+  }
+  __syncthreads();
+  cta_gemm(N, N, N, 1.0, A6, ldw, T1, ldw, 1.0, V, ldw);
+  // (V - U) R = (V + U)
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int i = idx % N, j = idx / N;
+    size_t o = i + size_t(j) * ldw;
+    T1[o] = V[o] - U[o];
+    T2[o] = V[o] + U[o];
+  }
+  __syncthreads();
+  cta_lu(N, T1, ldw, piv, red);
+  cta_lu_solve(N, T1, ldw, piv, T2, ldw, N);
+  // squarings, ping-pong T2 <-> T1
+  double *cur = T2, *nxt = T1;
+  for (int q = 0; q < s; ++q) {
+    cta_gemm(N, N, N, 1.0, cur, ldw, cur, ldw, 0.0, nxt, ldw);
+    double* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  cta_copy(N, N, cur, ldw, X, ldx);
+  return s;
+}
+
+}  // namespace pexp

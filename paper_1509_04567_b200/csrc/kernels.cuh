@@ -1,0 +1,127 @@
+// kernels.cuh — data structures and launch wrappers shared by the pexp sources.
+#pragma once
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace pexp {
+
+constexpr int KSMALL_MAX = 1024;  // max Krylov columns (K + m) of one projected problem
+
+// Tridiagonal rows of the operators A (not M = I - gamma*A): [nops][n] each.
+struct Ops {
+  int n = 0, nops = 0;
+  double *sub = nullptr, *diag = nullptr, *sup = nullptr;
+};
+
+// Factorisations of M_f = I - gamma_f A_{op_f}: [nf][n] each.
+struct Factors {
+  int n = 0, nf = 0, periodic = 0;
+  double *l = nullptr, *dinv = nullptr, *sup = nullptr, *z = nullptr, *w = nullptr;
+};
+
+// Arguments of the projected-problem kernel (one CTA per evaluation, grid-strided).
+struct SPArgs {
+  int E, kcap, m, K, kind;       // kind 0: cubic-forced, 1: homogeneous (initial value)
+  const double* H;               // [E] ldh x ldh block Hessenberg
+  long long hs_e;
+  int ldh;
+  const int* live;               // [E][ls_e] live flags of basis columns
+  long long ls_e;
+  const double* gam;             // [E] shift gamma
+  double h;                      // piece width
+  const int* npieces;            // [E] or nullptr
+  int npieces_const;
+  int out_stride, nout;          // store z at nodes q*out_stride, q < nout
+  const double* coef;            // forced: [E][s-1][4][m]
+  int s;
+  const double* beta;            // homogeneous: [E] start-vector norms
+  const double* crit;            // [E] residual targets
+  const double* Gt;              // [E] m x m Gram of (I - gamma A) V_tail
+  long long gts_e;
+  double* Z;                     // [E][nout][kcap]
+  long long zs_e;
+  double* res;                   // [E]
+  int* conv;                     // [E]
+  int* kfin;                     // [E] columns used by the converged z (written on convergence)
+  const int* active;             // [E]
+  double* work;                  // per-slot workspace (10 Nmax^2)
+  long long work_slot;
+  int* iwork;
+  long long iwork_slot;
+  int Nmax;
+  int stop_rule;                 // 0: SaI residual ||t||/gamma ; 1: true residual sqrt(t^T Gt t)/gamma
+};
+
+// tridiag.cu
+void launch_ade_rows(cudaStream_t st, int nops, int n, bool dirichlet, const double* nu, const double* a,
+                     double* sub, double* diag, double* sup);
+void launch_burgers_rows(cudaStream_t st, int nops, int n, double nu, const double* ubar, double* sub,
+                         double* diag, double* sup);
+void launch_factor(cudaStream_t st, const Factors& F, int nf, const int* opidx, const double* gam,
+                   const Ops& O, int* err);
+void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E, int ncols,
+                      const double* rhs, long long rs_e, int cin0, double* out, long long os_e, int cout0,
+                      const int* active);
+
+// tsmm.cu
+int xty_chunks(int n, int E);
+void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
+                const double* Y, long long ys_e, int y0, int ny, double* part, size_t part_cap, double* D,
+                long long ds_e, int ldd, int row0, int col0, bool accumulate, const int* active);
+void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
+                    const double* M, long long ms_e, int ldm, double* O, long long os_e, int o0, int ny,
+                    double alpha, double beta, const int* active, const int* nxe = nullptr);
+void tsmm_init();
+
+// small.cu
+void launch_sym_eig_select(cudaStream_t st, int E, int s, const double* G, double* lam, double* Msel, int* off,
+                           double* sigma1, int pass, double tau, double theta, const int* active);
+void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long gs_e, int ldg,
+                       const double* norm0, long long ns_e, int ldn, double defl, double* Rinv, const double* Rprev,
+                       long long rps_e, int ldrp, double* Rout, long long rs_e, int ldr, int* live,
+                       long long ls_e, const int* active);
+void launch_onesided_svd(cudaStream_t st, int E, int s, const double* C, const int* kk, double tau, double* Qs,
+                         double* sig, double* Cs, int* m_out, const int* active);
+void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, const double* Qs,
+                        const double* sig, const double* Cs, const int* m, double* Msel, double* Cfin, int* fill);
+void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, const double* Cfin, double h,
+                   double eta, double* coef, double* crit);
+void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots);
+void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
+                         long long work_slot, int* iwork, int nslots);
+void small_init();
+
+// stencil.cu
+void launch_apply_A(cudaStream_t st, const Ops& O, const int* opidx, int E, int ncols, const double* X,
+                    long long xs_e, int x0, double* Y, long long ys_e, int y0, bool periodic);
+void launch_apply_M(cudaStream_t st, const Ops& O, const int* opidx, const double* gam, int E, int ncols,
+                    const double* X, long long xs_e, int x0, double* Y, long long ys_e, int y0, bool periodic,
+                    const int* active);
+void launch_lin_source(cudaStream_t st, int batch, int P, int s, int n, const double* Au0, const double* src,
+                       double* G);
+void launch_fill_random(cudaStream_t st, int E, int n, int mmax, const int* fill, double* V, long long vs_e,
+                        unsigned seed);
+void launch_broadcast_waveform(cudaStream_t st, int P, int s, int n, const double* u0, double* U);
+void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, double dT, double* ubar,
+                       double* gam);
+void launch_burgers_source(cudaStream_t st, int P, int s, int n, double nu, const double* u0, const double* U,
+                           const double* ubar, double* G);
+void launch_wr_step(cudaStream_t st, int s, int n, const double* u0, const double* Wh, const double* Y,
+                    const double* Uold, double* Unew, double* uhat_end, double* delta);
+void launch_superpose(cudaStream_t st, int batch, int P, int n, const double* u0, const double* Yend,
+                      const double* Yh, long long yh_e, long long yh_node, double* out);
+void launch_copy_end(cudaStream_t st, int P, int s, int n, const double* U, double* out);
+void launch_norms(cudaStream_t st, int E, int n, const double* X, long long xs_e, double* nrm);
+void launch_scale_cols(cudaStream_t st, int E, int n, const double* X, long long xs_e, const double* nrm,
+                       double* Y, long long ys_e);
+void launch_add_block(cudaStream_t st, int E, int rows, int cols, const double* S, long long ss_e, int lds,
+                      double* D, long long ds_e, int ldd, const int* active);
+void launch_hupdate(cudaStream_t st, int E, int rows, int m, const double* T, long long ts_e, int ldt, const double* R,
+                    long long rs_e, int ldr, double* H, long long hs_e, int ldh, const int* active);
+void launch_hom_setup(cudaStream_t st, int E, int mode, int P, int s, double h, double eta, const double* beta,
+                      double* crit, int* npieces, int* active);
+void launch_update_active(cudaStream_t st, int E, const int* conv, int* active, int* count);
+void launch_fill_i32(cudaStream_t st, int* p, int count, int v);
+void launch_fill_f64(cudaStream_t st, double* p, size_t count, double v);
+
+}  // namespace pexp

@@ -1,0 +1,916 @@
+// pexp_api.cu — host orchestration (EBK batch engine, linear Paraexp driver, Burgers WR
+// driver) and the C ABI declared in include/pexp.h.  Every arithmetic step runs in the
+// CUDA kernels of tridiag.cu / tsmm.cu / small.cu / stencil.cu; this file only sequences
+// launches on the caller's stream and carves the caller's workspace.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "pexp.h"
+
+namespace pexp {
+thread_local long g_launches = 0;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+
+// ---------------------------------------------------------------- helper kernels
+__global__ void k_set_live0(int E, int kcap, int m, int* live) {
+  const int e = blockIdx.x;
+  for (int c = threadIdx.x; c < kcap; c += blockDim.x) live[size_t(e) * kcap + c] = c < m ? 1 : 0;
+}
+
+__global__ void k_active_from_m(int E, const int* m, int* active) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) active[e] = m[e] > 0;
+}
+
+// Start vectors of the homogeneous legs: eval eh = b*(P-1)+j takes Y[b*P+j] (v_j(T_{j+1})),
+// beta = ||.||, Vh block 0 = Y/beta.
+__global__ void k_hom_start(int P, int n, const double* Y, long long ys_e, double* beta, double* Vh,
+                            long long vs_e) {
+  const int eh = blockIdx.x;
+  __shared__ double red[32];
+  const int b = eh / (P - 1), j = eh % (P - 1);
+  const double* y = Y + (long long)(b * P + j) * ys_e;
+  double a = 0.0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) a = fma(y[r], y[r], a);
+  a = sqrt(block_sum(a, red));
+  if (threadIdx.x == 0) beta[eh] = a;
+  const double sc = a > 0.0 ? 1.0 / a : 0.0;
+  double* v = Vh + eh * vs_e;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) v[r] = y[r] * sc;
+}
+
+static void check_err(cudaStream_t st) { PEXP_CUDA_TRY(cudaGetLastError()); (void)st; }
+
+template <class T>
+static void h2d(cudaStream_t st, T* dst, const std::vector<T>& v) {
+  if (v.empty()) return;
+  PEXP_CUDA_TRY(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  PEXP_CUDA_TRY(cudaStreamSynchronize(st));  // pageable source: keep it alive until copied
+}
+
+// ---------------------------------------------------------------- options
+struct Opts {
+  int s;
+  double tau_f, eta_f;
+  int restart_blocks, kcap, stop_rule;
+  cudaStream_t st;
+};
+
+static Opts norm_opts(const pexp_options& o) {
+  Opts r;
+  r.s = o.s > 0 ? o.s : 32;
+  r.tau_f = o.svd_tau_factor > 0 ? o.svd_tau_factor : 0.01;
+  r.eta_f = o.stop_factor > 0 ? o.stop_factor : 0.01;
+  r.restart_blocks = o.restart_blocks > 0 ? o.restart_blocks : 20;
+  r.kcap = o.k_max > 0 ? o.k_max : 256;
+  r.st = (cudaStream_t)o.stream;
+  r.stop_rule = o.stop_rule;
+  return r;
+}
+
+// ---------------------------------------------------------------- EBK buffers
+struct EbkBufs {
+  int E = 0, n = 0, kcap = 0, mcap = 0, nout = 0, s = 0;
+  long long vs_e = 0, hs_e = 0, zs_e = 0;
+  double *V, *H, *Z, *Gt, *Wt, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef;
+  int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx;
+  double* part;
+  size_t part_cap;
+  double* work;
+  int* iwork;
+  int nslots, Nmax;
+  long long work_slot, iwork_slot;
+};
+
+static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, int nout, int s, bool forced,
+                      double* Wt_shared) {
+  B.E = E; B.n = n; B.kcap = kcap; B.mcap = mcap; B.nout = nout; B.s = s;
+  B.vs_e = (long long)kcap * n;
+  B.hs_e = (long long)kcap * kcap;
+  B.zs_e = (long long)nout * kcap;
+  B.V = ar.take<double>(size_t(E) * kcap * n);
+  B.H = ar.take<double>(size_t(E) * kcap * kcap);
+  B.Z = ar.take<double>(size_t(E) * nout * kcap);
+  B.Gt = ar.take<double>(size_t(E) * mcap * mcap);
+  B.Wt = Wt_shared ? Wt_shared : ar.take<double>(size_t(E) * mcap * n);
+  B.T = ar.take<double>(size_t(E) * kcap * mcap);
+  B.G0 = ar.take<double>(size_t(E) * mcap * mcap);
+  B.G1 = ar.take<double>(size_t(E) * mcap * mcap);
+  B.Rinv = ar.take<double>(size_t(E) * mcap * mcap);
+  B.Rtmp = ar.take<double>(size_t(E) * mcap * mcap);
+  B.res = ar.take<double>(E);
+  B.gam = ar.take<double>(E);
+  B.crit = ar.take<double>(E);
+  B.beta = ar.take<double>(E);
+  B.coef = forced ? ar.take<double>(size_t(E) * (s - 1) * 4 * mcap) : nullptr;
+  B.live = ar.take<int>(size_t(E) * kcap);
+  B.active = ar.take<int>(E);
+  B.conv = ar.take<int>(E);
+  B.kfin = ar.take<int>(E);
+  B.npieces = ar.take<int>(E);
+  B.count = ar.take<int>(4);
+  B.fidx = ar.take<int>(E);
+  B.opidx = ar.take<int>(E);
+  // bound on E'*nch(E') for every E' <= E (xty_chunks stops at <= 1184 CTAs or one chunk)
+  size_t ech = std::max<size_t>(size_t(E) * cdiv(n, xty_chunks(n, E)), 2 * 148 * 8 + size_t(E));
+  ech = std::min<size_t>(ech, size_t(E) * cdiv(n, 512));
+  B.part_cap = ech * std::max(kcap, s) * (forced ? std::max(mcap, s) : mcap);
+  B.part = ar.take<double>(B.part_cap);
+  B.nslots = std::min(E, 512);
+  B.Nmax = kcap + (forced ? 4 * mcap : 0);
+  B.work_slot = 10LL * B.Nmax * B.Nmax;
+  B.iwork_slot = B.Nmax;
+  B.work = ar.take<double>(size_t(B.nslots) * B.work_slot);
+  B.iwork = ar.take<int>(size_t(B.nslots) * B.iwork_slot);
+}
+
+struct RunInfo {
+  int max_k = 0;
+  int unconverged = 0;
+  double worst_res_ratio = 0.0;
+};
+
+// SaI block Arnoldi with BCGS2 + deflating CholQR2, projected problem checks on a geometric
+// schedule.  Preconditions: V block 0 (m columns) orthonormal; active, gam, fidx, opidx set;
+// forced: coef and crit set; homogeneous: beta, crit, npieces set.
+static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops& O, bool periodic, int m,
+                       int kind, double h, int npieces_const, int out_stride, int nout, int stop_rule) {
+  RunInfo info;
+  const int E = B.E, n = B.n, kcap = B.kcap;
+  if (E == 0) return info;
+  if (m > B.mcap) fail(1, "block width exceeds capacity");
+  k_set_live0<<<E, 128, 0, st>>>(E, kcap, m, B.live);
+  count_launch();
+  launch_fill_f64(st, B.H, size_t(E) * kcap * kcap, 0.0);
+  launch_fill_f64(st, B.Z, size_t(E) * nout * kcap, 0.0);
+  launch_fill_i32(st, B.kfin, E, 0);
+  launch_fill_i32(st, B.conv, E, 0);
+  PEXP_LAUNCH_CHECK();
+  int steps = 0, last_check = -1;
+  int next_check = std::max(4, 2 * m);
+  const double defl = 1e-12;
+  SPArgs a{};
+  a.E = E; a.kcap = kcap; a.m = m; a.kind = kind;
+  a.H = B.H; a.hs_e = B.hs_e; a.ldh = kcap;
+  a.live = B.live; a.ls_e = kcap;
+  a.gam = B.gam; a.h = h;
+  a.npieces = kind == 1 ? B.npieces : nullptr;
+  a.npieces_const = npieces_const;
+  a.out_stride = out_stride; a.nout = nout;
+  a.coef = B.coef; a.s = B.s;
+  a.beta = B.beta; a.crit = B.crit;
+  a.Gt = B.Gt; a.gts_e = (long long)m * m;
+  a.Z = B.Z; a.zs_e = B.zs_e;
+  a.res = B.res; a.conv = B.conv; a.kfin = B.kfin; a.active = B.active;
+  a.work = B.work; a.work_slot = B.work_slot; a.iwork = B.iwork; a.iwork_slot = B.iwork_slot; a.Nmax = B.Nmax;
+  a.stop_rule = stop_rule;
+  int remaining = E;
+  auto do_check = [&](int K) {
+    if (stop_rule == 1) {  // true residual: tail Gram of Wt = (I - gamma A) V[:, K:K+m]
+      launch_apply_M(st, O, B.opidx, B.gam, E, m, B.V, B.vs_e, K, B.Wt, (long long)m * n, 0, periodic, B.active);
+      launch_xty(st, E, n, B.Wt, (long long)m * n, 0, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.Gt,
+                 (long long)m * m, m, 0, 0, false, B.active);
+    }
+    a.K = K;
+    if (K + m > a.Nmax - (kind == 0 ? 4 * m : 0) + m) fail(1, "small problem exceeds workspace");
+    launch_small_problem(st, a, B.nslots);
+    PEXP_CUDA_TRY(cudaMemsetAsync(B.count, 0, sizeof(int), st));
+    launch_update_active(st, E, B.conv, B.active, B.count);
+    int h_count = 0;
+    PEXP_CUDA_TRY(cudaMemcpyAsync(&h_count, B.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    remaining = h_count;
+    last_check = K;
+    info.max_k = std::max(info.max_k, K);
+    static const bool dbg = getenv("PEXP_DEBUG") != nullptr;
+    if (dbg) {  // developer trace: residual/target distribution at this check
+      std::vector<double> r(E), c(E);
+      std::vector<int> lv(size_t(E) * kcap), cv(E);
+      cudaMemcpy(r.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost);
+      cudaMemcpy(c.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost);
+      cudaMemcpy(cv.data(), B.conv, E * sizeof(int), cudaMemcpyDeviceToHost);
+      cudaMemcpy(lv.data(), B.live, size_t(E) * kcap * sizeof(int), cudaMemcpyDeviceToHost);
+      std::vector<double> q;
+      int tail_live = 0, dead_total = 0;
+      for (int e = 0; e < E; ++e) {
+        q.push_back(c[e] > 0 ? r[e] / c[e] : -1);
+        for (int j = K; j < K + m; ++j) tail_live += lv[size_t(e) * kcap + j];
+        for (int j = 0; j < K; ++j) dead_total += !lv[size_t(e) * kcap + j];
+      }
+      std::sort(q.begin(), q.end());
+      fprintf(stderr, "[pexp] kind=%d E=%d m=%d K=%d remaining=%d ratio min=%.3g med=%.3g max=%.3g tail_live=%d dead=%d\n",
+              kind, E, m, K, remaining, q.front(), q[q.size() / 2], q.back(), tail_live, dead_total);
+    }
+  };
+  // initial active count (some evals may start inactive: zero source / zero start vector)
+  {
+    PEXP_CUDA_TRY(cudaMemsetAsync(B.count, 0, sizeof(int), st));
+    launch_update_active(st, E, B.conv, B.active, B.count);
+    int h_count = 0;
+    PEXP_CUDA_TRY(cudaMemcpyAsync(&h_count, B.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    remaining = h_count;
+  }
+  while (remaining > 0) {
+    if ((steps + 2) * m > kcap) {
+      if (steps >= 1 && last_check != steps * m) do_check(steps * m);
+      break;
+    }
+    const int b = steps, nv = (b + 1) * m;
+    const long long ws_e = B.vs_e;
+    // W = (I - gamma A)^{-1} V_b  -> columns [nv, nv+m)
+    launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
+    // W^T W before orthogonalisation (deflation reference)
+    launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G0, (long long)m * m, m, 0, 0,
+               false, B.active);
+    // BCGS2 with intra-block Cholesky-QR in each pass (pass 2 restores orthogonality of
+    // nearly deflated columns):  W = V H1 + Q1 R1,  Q1 = V H2 + Q2 R2
+    //   => H[:, block b] = H1 + H2 R1,  H[nv:nv+m, block b] = R2 R1.
+    // pass 1: H1 -> H ; W -= V H1 ; [Q1, R1] = deflating CholQR(W)  (R1 -> Rtmp)
+    launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.H, B.hs_e, kcap, 0, b * m,
+               false, B.active);
+    launch_combine(st, E, n, B.V, ws_e, 0, nv, B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.V, ws_e, nv, m, -1.0, 1.0,
+                   B.active);
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) {
+        // pass 2: T = V^T Q1 ; W -= V T ; H[:, block b] += T R1
+        launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.T, (long long)kcap * B.mcap,
+                   nv, 0, 0, false, B.active);
+        launch_combine(st, E, n, B.V, ws_e, 0, nv, B.T, (long long)kcap * B.mcap, nv, B.V, ws_e, nv, m, -1.0, 1.0,
+                       B.active);
+        launch_hupdate(st, E, nv, m, B.T, (long long)kcap * B.mcap, nv, B.Rtmp, (long long)m * m, m,
+                       B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.active);
+      }
+      launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0,
+                 false, B.active);
+      if (pass == 0) {
+        launch_block_chol(st, E, m, B.G1, (long long)m * m, m, B.G0, (long long)m * m, m, defl, B.Rinv, nullptr, 0,
+                          0, B.Rtmp, (long long)m * m, m, B.live + nv, kcap, B.active);
+      } else {
+        launch_block_chol(st, E, m, B.G1, (long long)m * m, m, nullptr, 0, 0, defl, B.Rinv, B.Rtmp,
+                          (long long)m * m, m, B.H + size_t(nv) + size_t(b) * m * kcap, B.hs_e, kcap, B.live + nv,
+                          kcap, B.active);
+      }
+      if (m <= 32) {
+        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.V, ws_e, nv, m, 1.0, 0.0,
+                       B.active);
+      } else {
+        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.Wt, (long long)m * n, 0, m, 1.0,
+                       0.0, B.active);
+        PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.V + size_t(nv) * n, ws_e * sizeof(double), B.Wt, size_t(m) * n * sizeof(double),
+                                        size_t(m) * n * sizeof(double), E, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    ++steps;
+    const int K = steps * m;
+    if (K >= next_check || (steps + 2) * m > kcap) {
+      do_check(K);
+      next_check = std::max(K + m, (int)std::ceil(K * 1.25));
+    }
+  }
+  info.unconverged = remaining;
+  {  // worst residual / target over the evaluations at their last check (diagnostic)
+    std::vector<double> r(E), c(E);
+    PEXP_CUDA_TRY(cudaMemcpyAsync(r.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaMemcpyAsync(c.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int e = 0; e < E; ++e)
+      if (c[e] > 0 && last_check >= 0) info.worst_res_ratio = std::max(info.worst_res_ratio, r[e] / c[e]);
+  }
+  return info;
+}
+
+// ---------------------------------------------------------------- source SVD stage
+struct SvdBufs {
+  double *U, *R, *Gs, *lam, *Msel, *sigma1, *Cb, *Qs, *Cs, *sig, *Cfin, *Rinv, *Kinv;
+  int *off, *me, *fill;
+};
+
+static void alloc_svd(Arena& ar, SvdBufs& S, int E, int n, int s) {
+  S.U = ar.take<double>(size_t(E) * s * n);
+  S.R = ar.take<double>(size_t(E) * s * n);
+  S.Gs = ar.take<double>(size_t(E) * s * s);
+  S.lam = ar.take<double>(size_t(E) * s);
+  S.Msel = ar.take<double>(size_t(E) * s * s);
+  S.sigma1 = ar.take<double>(E);
+  S.Cb = ar.take<double>(size_t(E) * s * s);
+  S.Qs = ar.take<double>(size_t(E) * s * s);
+  S.Cs = ar.take<double>(size_t(E) * s * s);
+  S.sig = ar.take<double>(size_t(E) * s);
+  S.Cfin = ar.take<double>(size_t(E) * s * s);
+  S.Rinv = ar.take<double>(size_t(E) * s * s);
+  S.Kinv = ar.take<double>(size_t(s) * s);
+  S.off = ar.take<int>(E);
+  S.me = ar.take<int>(E);
+  S.fill = ar.take<int>(size_t(E) * s);
+}
+
+// Not-a-knot system matrix (rows: M0-2M1+M2 = 0; M_{i-1}+4M_i+M_{i+1} = r_i; last analogous),
+// inverted on the host once per solve (depends on s only).
+static std::vector<double> notaknot_inverse(int s) {
+  std::vector<double> K(size_t(s) * s, 0.0), I(size_t(s) * s, 0.0);
+  auto at = [&](std::vector<double>& M, int i, int j) -> double& { return M[i + size_t(j) * s]; };
+  at(K, 0, 0) = 1; at(K, 0, 1) = -2; at(K, 0, 2) = 1;
+  at(K, s - 1, s - 3) = 1; at(K, s - 1, s - 2) = -2; at(K, s - 1, s - 1) = 1;
+  for (int i = 1; i < s - 1; ++i) { at(K, i, i - 1) = 1; at(K, i, i) = 4; at(K, i, i + 1) = 1; }
+  for (int i = 0; i < s; ++i) at(I, i, i) = 1;
+  // Gauss-Jordan with partial pivoting
+  for (int c = 0; c < s; ++c) {
+    int p = c;
+    for (int r = c + 1; r < s; ++r) if (std::fabs(at(K, r, c)) > std::fabs(at(K, p, c))) p = r;
+    if (p != c) for (int j = 0; j < s; ++j) { std::swap(at(K, c, j), at(K, p, j)); std::swap(at(I, c, j), at(I, p, j)); }
+    double d = at(K, c, c);
+    for (int j = 0; j < s; ++j) { at(K, c, j) /= d; at(I, c, j) /= d; }
+    for (int r = 0; r < s; ++r)
+      if (r != c) {
+        double f = at(K, r, c);
+        if (f != 0.0) for (int j = 0; j < s; ++j) { at(K, r, j) -= f * at(K, c, j); at(I, r, j) -= f * at(I, c, j); }
+      }
+  }
+  return I;
+}
+
+// Two-pass Gram SVD (subsystem 3) of E sample matrices G [E][s][n]; writes V block 0
+// (mmax columns, orthonormal), coef, crit into B and returns mmax (host).
+static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int s, const double* G, double tau,
+                     double eta, double h, int* me_host) {
+  const long long gs_e = (long long)s * n;
+  const double theta = 1e-6;
+  int npass = std::max(1, (int)std::ceil(std::log(0.5 * tau) / std::log(theta)));
+  npass = std::min(npass, 4);
+  double* part = B->part;
+  size_t part_cap = B->part_cap;
+  PEXP_CUDA_TRY(cudaMemsetAsync(S.U, 0, size_t(E) * s * n * sizeof(double), st));
+  launch_fill_i32(st, S.off, E, 0);
+  double* U = S.U;   // current orthonormal basis (zero columns beyond off[e])
+  double* Fr = S.R;  // free buffer
+  for (int p = 0; p < npass; ++p) {
+    const double* X = G;
+    if (p > 0) {
+      // residual R = G - U (U^T G), explicit (pass p resolves what pass p-1 could not)
+      launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr);
+      PEXP_CUDA_TRY(cudaMemcpyAsync(Fr, G, size_t(E) * s * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      launch_combine(st, E, n, U, gs_e, 0, s, S.Cb, (long long)s * s, s, Fr, gs_e, 0, s, -1.0, 1.0, nullptr);
+      X = Fr;
+    }
+    launch_xty(st, E, n, X, gs_e, 0, s, X, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false, nullptr);
+    launch_sym_eig_select(st, E, s, S.Gs, S.lam, S.Msel, S.off, S.sigma1, p, tau, theta, nullptr);
+    launch_combine(st, E, n, X, gs_e, 0, s, S.Msel, (long long)s * s, s, U, gs_e, 0, s, 1.0, 1.0, nullptr);
+    // CholQR2 of U (masked: zero columns stay zero); ping-pong U <-> Fr
+    for (int q = 0; q < 2; ++q) {
+      launch_xty(st, E, n, U, gs_e, 0, s, U, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false,
+                 nullptr);
+      launch_block_chol(st, E, s, S.Gs, (long long)s * s, s, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0, 0,
+                        nullptr, 0, nullptr);
+      launch_combine(st, E, n, U, gs_e, 0, s, S.Rinv, (long long)s * s, s, Fr, gs_e, 0, s, 1.0, 0.0, nullptr);
+      std::swap(U, Fr);
+    }
+  }
+  // C = U^T G, one-sided Jacobi SVD, truncation
+  launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr);
+  launch_onesided_svd(st, E, s, S.Cb, S.off, tau, S.Qs, S.sig, S.Cs, S.me, nullptr);
+  std::vector<int> mh(E);
+  PEXP_CUDA_TRY(cudaMemcpyAsync(mh.data(), S.me, E * sizeof(int), cudaMemcpyDeviceToHost, st));
+  PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+  int mmax = 0;
+  for (int e = 0; e < E; ++e) mmax = std::max(mmax, mh[e]);
+  if (me_host) std::copy(mh.begin(), mh.end(), me_host);
+  if (!B) return mmax;
+  const int mb = std::max(mmax, 1);
+  if (mb > B->mcap) fail(1, "retained rank exceeds capacity");
+  launch_build_final(st, E, s, mb, S.off, S.Qs, S.sig, S.Cs, S.me, S.Msel, S.Cfin, S.fill);
+  launch_combine(st, E, n, U, gs_e, 0, s, S.Msel, (long long)s * mb, s, B->V, B->vs_e, 0, mb, 1.0, 0.0, nullptr);
+  launch_fill_random(st, E, n, mb, S.fill, B->V, B->vs_e, 12345u);
+  for (int q = 0; q < 2; ++q) {
+    launch_xty(st, E, n, B->V, B->vs_e, 0, mb, B->V, B->vs_e, 0, mb, part, part_cap, S.Gs, (long long)mb * mb, mb, 0, 0,
+               false, nullptr);
+    launch_block_chol(st, E, mb, S.Gs, (long long)mb * mb, mb, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0,
+                      0, nullptr, 0, nullptr);
+    if (mb <= 32) {
+      launch_combine(st, E, n, B->V, B->vs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, B->V, B->vs_e, 0, mb, 1.0, 0.0,
+                     nullptr);
+    } else {
+      launch_combine(st, E, n, B->V, B->vs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, Fr, gs_e, 0, mb, 1.0, 0.0, nullptr);
+      PEXP_CUDA_TRY(cudaMemcpy2DAsync(B->V, B->vs_e * sizeof(double), Fr, gs_e * sizeof(double),
+                                      size_t(mb) * n * sizeof(double), E, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  std::vector<double> Ki = notaknot_inverse(s);
+  h2d(st, S.Kinv, Ki);
+  launch_spline(st, E, s, mb, S.Kinv, S.Cfin, h, eta, B->coef, B->crit);
+  k_active_from_m<<<cdiv(E, 256), 256, 0, st>>>(E, S.me, B->active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+  return mmax;
+}
+
+}  // namespace pexp
+
+using namespace pexp;
+
+// ---------------------------------------------------------------- context
+struct pexp_ctx {
+  int64_t n = 0;
+  int bc = 0;
+  int batch = 1;
+  std::vector<double> nu, a;
+  pexp_options opt{};
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  std::string err;
+};
+
+static pexp_status set_err(pexp_ctx* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return (pexp_status)code;
+}
+
+template <class F>
+static pexp_status guarded(pexp_ctx* c, F&& f) {
+  try {
+    f();
+    if (c) c->err.clear();
+    return PEXP_OK;
+  } catch (const Error& e) {
+    return set_err(c, e.code, e.msg);
+  } catch (const std::exception& e) {
+    return set_err(c, PEXP_EINVAL, e.what());
+  }
+}
+
+// ---------------------------------------------------------------- workspace plans
+struct LinPlan {
+  Ops O;
+  Factors F;
+  double *nu_d, *a_d, *gam_f, *Au0, *G, *Yend, *Yh;
+  int *opidx_f, *err, *iota;
+  SvdBufs S;
+  EbkBufs B, Bh;
+};
+
+static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
+  Opts o = norm_opts(c->opt);
+  const int n = (int)c->n, Bt = c->batch, s = o.s, E = Bt * P, Eh = Bt * (P - 1);
+  L.O.n = n; L.O.nops = Bt;
+  L.O.sub = ar.take<double>(size_t(Bt) * n);
+  L.O.diag = ar.take<double>(size_t(Bt) * n);
+  L.O.sup = ar.take<double>(size_t(Bt) * n);
+  L.F.n = n; L.F.nf = 2 * Bt; L.F.periodic = c->bc == PEXP_BC_PERIODIC;
+  L.F.l = ar.take<double>(size_t(2 * Bt) * n);
+  L.F.dinv = ar.take<double>(size_t(2 * Bt) * n);
+  L.F.sup = ar.take<double>(size_t(2 * Bt) * n);
+  L.F.z = ar.take<double>(size_t(2 * Bt) * n);
+  L.F.w = ar.take<double>(size_t(2 * Bt) * n);
+  L.nu_d = ar.take<double>(Bt);
+  L.a_d = ar.take<double>(Bt);
+  L.gam_f = ar.take<double>(2 * Bt);
+  L.opidx_f = ar.take<int>(2 * Bt);
+  L.err = ar.take<int>(4);
+  L.iota = ar.take<int>(std::max(Bt, 1));
+  L.Au0 = ar.take<double>(size_t(Bt) * n);
+  L.G = ar.take<double>(size_t(E) * s * n);
+  L.Yend = ar.take<double>(size_t(E) * n);
+  alloc_svd(ar, L.S, E, n, s);
+  alloc_ebk(ar, L.B, E, n, o.kcap, s, 2, s, true, L.S.R);
+  if (Eh > 0) {
+    alloc_ebk(ar, L.Bh, Eh, n, o.kcap, 1, P, s, false, nullptr);
+    L.Yh = ar.take<double>(size_t(Eh) * P * n);
+  } else {
+    L.Yh = nullptr;
+  }
+}
+
+struct BurPlan {
+  Ops O;
+  Factors F;
+  double *Uk, *Un, *ubar, *G, *Y, *Wh, *uhat, *delta;
+  int *iota, *err;
+  SvdBufs S;
+  EbkBufs B, B1;
+};
+
+static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
+  Opts o = norm_opts(c->opt);
+  const int n = (int)c->n, s = o.s, E = P;
+  L.O.n = n; L.O.nops = P;
+  L.O.sub = ar.take<double>(size_t(P) * n);
+  L.O.diag = ar.take<double>(size_t(P) * n);
+  L.O.sup = ar.take<double>(size_t(P) * n);
+  L.F.n = n; L.F.nf = P; L.F.periodic = 1;
+  L.F.l = ar.take<double>(size_t(P) * n);
+  L.F.dinv = ar.take<double>(size_t(P) * n);
+  L.F.sup = ar.take<double>(size_t(P) * n);
+  L.F.z = ar.take<double>(size_t(P) * n);
+  L.F.w = ar.take<double>(size_t(P) * n);
+  L.Uk = ar.take<double>(size_t(P) * s * n);
+  L.Un = ar.take<double>(size_t(P) * s * n);
+  L.ubar = ar.take<double>(size_t(P) * n);
+  L.G = ar.take<double>(size_t(P) * s * n);
+  L.Y = ar.take<double>(size_t(P) * s * n);
+  L.Wh = ar.take<double>(size_t(s) * n);
+  L.uhat = ar.take<double>(n);
+  L.delta = ar.take<double>(4);
+  L.iota = ar.take<int>(P);
+  L.err = ar.take<int>(4);
+  alloc_svd(ar, L.S, E, n, s);
+  alloc_ebk(ar, L.B, E, n, o.kcap, s, s, s, true, L.S.R);
+  alloc_ebk(ar, L.B1, 1, n, std::min(o.kcap, 512), 1, s, s, false, nullptr);
+}
+
+static size_t lin_bytes(const pexp_ctx* c, int P) {
+  Arena ar;
+  LinPlan L;
+  plan_linear(ar, L, c, P);
+  return ar.off;
+}
+static size_t bur_bytes(const pexp_ctx* c, int P) {
+  if (c->bc != PEXP_BC_PERIODIC || c->batch != 1) return 0;
+  Arena ar;
+  BurPlan L;
+  plan_burgers(ar, L, c, P);
+  return ar.off;
+}
+
+static void init_once() {
+  static bool done = false;
+  if (!done) {
+    tsmm_init();
+    small_init();
+    done = true;
+  }
+}
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+pexp_status pexp_create(pexp_ctx** ctx, int64_t n, pexp_bc bc, double nu, double a, const pexp_options* opt) {
+  return pexp_create_batched(ctx, n, bc, 1, &nu, &a, opt);
+}
+
+pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t batch, const double* nu_host,
+                                const double* a_host, const pexp_options* opt) {
+  if (!ctx) return PEXP_EINVAL;
+  *ctx = nullptr;
+  if (n < 3 || n > (1LL << 30)) return PEXP_EINVAL;
+  if (bc != PEXP_BC_PERIODIC && bc != PEXP_BC_DIRICHLET) return PEXP_EINVAL;
+  if (batch < 1 || !nu_host || !a_host) return PEXP_EINVAL;
+  for (int b = 0; b < batch; ++b)
+    if (!(nu_host[b] >= 0.0) || !std::isfinite(nu_host[b]) || !std::isfinite(a_host[b])) return PEXP_EINVAL;
+  pexp_options o{};
+  if (opt) o = *opt;
+  if (o.s != 0 && (o.s < 4 || o.s > 64)) return PEXP_EINVAL;
+  if (o.node_rule != 0) return PEXP_EINVAL;
+  if (o.k_max < 0 || o.k_max > KSMALL_MAX - 64) return PEXP_EINVAL;
+  if (o.stop_rule < 0 || o.stop_rule > 1) return PEXP_EINVAL;
+  pexp_ctx* c = new pexp_ctx;
+  c->n = n;
+  c->bc = bc;
+  c->batch = batch;
+  c->nu.assign(nu_host, nu_host + batch);
+  c->a.assign(a_host, a_host + batch);
+  c->opt = o;
+  *ctx = c;
+  return PEXP_OK;
+}
+
+void pexp_destroy(pexp_ctx* ctx) { delete ctx; }
+
+const char* pexp_last_error(const pexp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+pexp_status pexp_sample_times(const pexp_ctx* ctx, double T, int32_t P, double* t_host) {
+  if (!ctx || !t_host || !(T > 0) || P < 1) return PEXP_EINVAL;
+  Opts o = norm_opts(ctx->opt);
+  const double dT = T / P;
+  for (int j = 0; j < P; ++j)
+    for (int i = 0; i < o.s; ++i) t_host[size_t(j) * o.s + i] = j * dT + i * (dT / (o.s - 1));
+  return PEXP_OK;
+}
+
+size_t pexp_workspace_bytes(const pexp_ctx* ctx, int32_t P, int32_t kind) {
+  if (!ctx || P < 1 || kind < 0 || kind > 2) return 0;
+  if (kind == 0) return lin_bytes(ctx, P) + 256;
+  if (kind == 1) return bur_bytes(ctx, P) + 256;
+  return std::max(lin_bytes(ctx, P), bur_bytes(ctx, P)) + 256;
+}
+
+pexp_status pexp_set_workspace(pexp_ctx* ctx, void* dev_ptr, size_t bytes) {
+  if (!ctx) return PEXP_EINVAL;
+  if (dev_ptr && (reinterpret_cast<uintptr_t>(dev_ptr) & 255)) return set_err(ctx, PEXP_EINVAL, "workspace must be 256-byte aligned");
+  ctx->ws = (char*)dev_ptr;
+  ctx->ws_bytes = bytes;
+  return PEXP_OK;
+}
+
+pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src, double T, int32_t P, double tol,
+                              double* out, pexp_stats* st_out) {
+  if (!ctx) return PEXP_EINVAL;
+  if (!u0 || !src || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
+  if (!(T > 0) || !std::isfinite(T)) return set_err(ctx, PEXP_EINVAL, "T must be > 0");
+  if (P < 1) return set_err(ctx, PEXP_EINVAL, "P must be >= 1");
+  if (!(tol >= 1e-14 && tol <= 1e-2)) return set_err(ctx, PEXP_EINVAL, "tol must be in [1e-14, 1e-2]");
+  if (!ctx->ws) return set_err(ctx, PEXP_ENOMEM, "workspace not set (pexp_set_workspace)");
+  if (ctx->ws_bytes < lin_bytes(ctx, P)) return set_err(ctx, PEXP_ENOMEM, "workspace too small for this P");
+  return guarded(ctx, [&] {
+    init_once();
+    g_launches = 0;
+    Opts o = norm_opts(ctx->opt);
+    cudaStream_t st = o.st;
+    const int n = (int)ctx->n, Bt = ctx->batch, s = o.s, E = Bt * P, Eh = Bt * (P - 1);
+    const bool periodic = ctx->bc == PEXP_BC_PERIODIC;
+    const double dT = T / P, h = dT / (s - 1), tau = o.tau_f * tol, eta = o.eta_f * tol;
+    Arena ar{ctx->ws, ctx->ws_bytes, 0};
+    LinPlan L;
+    plan_linear(ar, L, ctx, P);
+    cudaEvent_t e0, e1;
+    PEXP_CUDA_TRY(cudaEventCreate(&e0));
+    PEXP_CUDA_TRY(cudaEventCreate(&e1));
+    PEXP_CUDA_TRY(cudaEventRecord(e0, st));
+    // operators and factorisations: f < Bt: gamma = dT/10 (nonhomogeneous); f >= Bt: gamma = T/10 (legs)
+    h2d(st, L.nu_d, ctx->nu);
+    h2d(st, L.a_d, ctx->a);
+    launch_ade_rows(st, Bt, n, !periodic, L.nu_d, L.a_d, L.O.sub, L.O.diag, L.O.sup);
+    std::vector<double> gf(2 * Bt);
+    std::vector<int> of(2 * Bt), iota(Bt);
+    for (int b = 0; b < Bt; ++b) { gf[b] = dT / 10; gf[Bt + b] = T / 10; of[b] = b; of[Bt + b] = b; iota[b] = b; }
+    h2d(st, L.gam_f, gf);
+    h2d(st, L.opidx_f, of);
+    h2d(st, L.iota, iota);
+    PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
+    launch_factor(st, L.F, 2 * Bt, L.opidx_f, L.gam_f, L.O, L.err);
+    // shifted source G = A u0 + g at the nodes
+    launch_apply_A(st, L.O, L.iota, Bt, 1, u0, n, 0, L.Au0, n, 0, periodic);
+    launch_lin_source(st, Bt, P, s, n, L.Au0, src, L.G);
+    // per-eval maps for the nonhomogeneous batch
+    std::vector<int> fe(E);
+    std::vector<double> ge(E, dT / 10);
+    for (int e = 0; e < E; ++e) fe[e] = e / P;
+    h2d(st, L.B.fidx, fe);
+    h2d(st, L.B.opidx, fe);
+    h2d(st, L.B.gam, ge);
+    int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, nullptr);
+    int herr = 0;
+    PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
+    RunInfo ri{}, rh{};
+    if (mmax > 0) {
+      ri = ebk_run(st, L.B, L.F, L.O, periodic, mmax, 0, h, s - 1, s - 1, 2, o.stop_rule);
+      launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, ri.max_k, L.B.Z + L.B.kcap, L.B.zs_e, L.B.kcap, L.Yend, n, 0, 1,
+                     1.0, 0.0, nullptr, L.B.kfin);
+    } else {
+      PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
+    }
+    if (Eh > 0) {
+      std::vector<int> fh(Eh), oh(Eh);
+      std::vector<double> gh(Eh, T / 10);
+      for (int e = 0; e < Eh; ++e) { fh[e] = Bt + e / (P - 1); oh[e] = e / (P - 1); }
+      h2d(st, L.Bh.fidx, fh);
+      h2d(st, L.Bh.opidx, oh);
+      h2d(st, L.Bh.gam, gh);
+      k_hom_start<<<Eh, PEXP_THREADS, 0, st>>>(P, n, L.Yend, n, L.Bh.beta, L.Bh.V, L.Bh.vs_e);
+      count_launch();
+      PEXP_LAUNCH_CHECK();
+      launch_hom_setup(st, Eh, 0, P, s, h, eta, L.Bh.beta, L.Bh.crit, L.Bh.npieces, L.Bh.active);
+      rh = ebk_run(st, L.Bh, L.F, L.O, periodic, 1, 1, h, 0, s - 1, P, o.stop_rule);
+      launch_combine(st, Eh, n, L.Bh.V, L.Bh.vs_e, 0, std::max(rh.max_k, 1), L.Bh.Z, L.Bh.zs_e, L.Bh.kcap, L.Yh,
+                     (long long)P * n, 0, P, 1.0, 0.0, nullptr, L.Bh.kfin);
+    }
+    launch_superpose(st, Bt, P, n, u0, L.Yend, L.Yh, (long long)P * n, n, out);
+    PEXP_CUDA_TRY(cudaEventRecord(e1, st));
+    PEXP_CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    check_err(st);
+    if (st_out) {
+      std::memset(st_out, 0, sizeof(*st_out));
+      st_out->max_m = mmax;
+      st_out->max_k = std::max(ri.max_k, rh.max_k);
+      st_out->best_residual = std::max(ri.worst_res_ratio, rh.worst_res_ratio);
+      st_out->ms_total = ms;
+      st_out->evals = E;
+      st_out->kernel_launches = (int)g_launches;
+    }
+    if (ri.unconverged || rh.unconverged)
+      fail(PEXP_ENOCONV, "Krylov capacity k_max reached before the residual target (" +
+                             std::to_string(ri.unconverged) + " nonhomogeneous, " + std::to_string(rh.unconverged) +
+                             " homogeneous evaluations; worst residual/target " +
+                             std::to_string(std::max(ri.worst_res_ratio, rh.worst_res_ratio)) + ", max_k " +
+                             std::to_string(std::max(ri.max_k, rh.max_k)) + ", m " + std::to_string(mmax) + ")");
+  });
+}
+
+pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, double T, int32_t P, double tol,
+                               int32_t max_wr_iters, double* out, pexp_stats* st_out) {
+  if (!ctx) return PEXP_EINVAL;
+  if (!u0 || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
+  if (ctx->bc != PEXP_BC_PERIODIC || ctx->batch != 1)
+    return set_err(ctx, PEXP_EINVAL, "Burgers requires a periodic context with batch 1");
+  if (!(nu > 0) || !std::isfinite(nu)) return set_err(ctx, PEXP_EINVAL, "nu must be > 0");
+  if (!(T > 0)) return set_err(ctx, PEXP_EINVAL, "T must be > 0");
+  if (P < 1) return set_err(ctx, PEXP_EINVAL, "P must be >= 1");
+  if (!(tol >= 1e-14 && tol <= 1e-2)) return set_err(ctx, PEXP_EINVAL, "tol must be in [1e-14, 1e-2]");
+  if (max_wr_iters < 1) return set_err(ctx, PEXP_EINVAL, "max_wr_iters must be >= 1");
+  if (!ctx->ws) return set_err(ctx, PEXP_ENOMEM, "workspace not set (pexp_set_workspace)");
+  if (ctx->ws_bytes < bur_bytes(ctx, P)) return set_err(ctx, PEXP_ENOMEM, "workspace too small for this P");
+  return guarded(ctx, [&] {
+    init_once();
+    g_launches = 0;
+    Opts o = norm_opts(ctx->opt);
+    cudaStream_t st = o.st;
+    const int n = (int)ctx->n, s = o.s, E = P;
+    const double dT = T / P, h = dT / (s - 1), tau = o.tau_f * tol, eta = o.eta_f * tol;
+    const double wr_tol = 1e-6;
+    Arena ar{ctx->ws, ctx->ws_bytes, 0};
+    BurPlan L;
+    plan_burgers(ar, L, ctx, P);
+    cudaEvent_t e0, e1;
+    PEXP_CUDA_TRY(cudaEventCreate(&e0));
+    PEXP_CUDA_TRY(cudaEventCreate(&e1));
+    PEXP_CUDA_TRY(cudaEventRecord(e0, st));
+    std::vector<int> iota(P);
+    for (int j = 0; j < P; ++j) iota[j] = j;
+    h2d(st, L.iota, iota);
+    h2d(st, L.B.fidx, iota);
+    h2d(st, L.B.opidx, iota);
+    launch_broadcast_waveform(st, P, s, n, u0, L.Uk);
+    int iters = 0, max_m = 0, max_k = 0;
+    double delta = 0.0, delta0 = -1.0;
+    for (int k = 0; k < max_wr_iters; ++k) {
+      launch_ubar_gamma(st, P, s, n, L.Uk, dT, L.ubar, L.B.gam);
+      launch_burgers_rows(st, P, n, nu, L.ubar, L.O.sub, L.O.diag, L.O.sup);
+      PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
+      launch_factor(st, L.F, P, L.iota, L.B.gam, L.O, L.err);
+      launch_burgers_source(st, P, s, n, nu, u0, L.Uk, L.ubar, L.G);
+      int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, nullptr);
+      int herr = 0;
+      PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+      if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
+      max_m = std::max(max_m, mmax);
+      if (mmax > 0) {
+        RunInfo ri = ebk_run(st, L.B, L.F, L.O, true, mmax, 0, h, s - 1, 1, s, o.stop_rule);
+        if (ri.unconverged) fail(PEXP_ENOCONV, "Krylov capacity reached (nonhomogeneous, WR iteration " + std::to_string(k + 1) + ")");
+        max_k = std::max(max_k, ri.max_k);
+        launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, ri.max_k, L.B.Z, L.B.zs_e, L.B.kcap, L.Y, (long long)s * n, 0, s,
+                       1.0, 0.0, nullptr, L.B.kfin);
+      } else {
+        PEXP_CUDA_TRY(cudaMemsetAsync(L.Y, 0, size_t(P) * s * n * sizeof(double), st));
+      }
+      PEXP_CUDA_TRY(cudaMemsetAsync(L.delta, 0, sizeof(double), st));
+      for (int i = 0; i < P; ++i) {
+        const size_t off = size_t(i) * s * n;
+        if (i == 0) {
+          launch_wr_step(st, s, n, u0, nullptr, L.Y + off, L.Uk + off, L.Un + off, L.uhat, L.delta);
+          continue;
+        }
+        // homogeneous scan step: exp((t - T_{i-1}) A_i) uhat(T_{i-1}) at the s nodes
+        EbkBufs& B1 = L.B1;
+        k_hom_start<<<1, PEXP_THREADS, 0, st>>>(2, n, L.uhat, n, B1.beta, B1.V, B1.vs_e);
+        count_launch();
+        PEXP_CUDA_TRY(cudaMemcpyAsync(B1.fidx, L.iota + i, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        PEXP_CUDA_TRY(cudaMemcpyAsync(B1.opidx, L.iota + i, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        PEXP_CUDA_TRY(cudaMemcpyAsync(B1.gam, L.B.gam + i, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        launch_hom_setup(st, 1, 1, P, s, h, eta, B1.beta, B1.crit, B1.npieces, B1.active);
+        RunInfo rh = ebk_run(st, B1, L.F, L.O, true, 1, 1, h, 0, 1, s, o.stop_rule);
+        if (rh.unconverged) fail(PEXP_ENOCONV, "Krylov capacity reached (homogeneous scan)");
+        max_k = std::max(max_k, rh.max_k);
+        launch_combine(st, 1, n, B1.V, B1.vs_e, 0, std::max(rh.max_k, 1), B1.Z, B1.zs_e, B1.kcap, L.Wh, (long long)s * n, 0, s,
+                       1.0, 0.0, nullptr, B1.kfin);
+        launch_wr_step(st, s, n, u0, L.Wh, L.Y + off, L.Uk + off, L.Un + off, L.uhat, L.delta);
+      }
+      PEXP_CUDA_TRY(cudaMemcpyAsync(&delta, L.delta, sizeof(double), cudaMemcpyDeviceToHost, st));
+      PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+      std::swap(L.Uk, L.Un);
+      ++iters;
+      if (delta0 < 0) delta0 = delta;
+      if (!std::isfinite(delta) || delta > 1e3 * delta0)
+        fail(PEXP_EDIVERGED, "waveform relaxation diverged at iteration " + std::to_string(iters));
+      if (delta < wr_tol) break;
+    }
+    launch_copy_end(st, P, s, n, L.Uk, out);
+    PEXP_CUDA_TRY(cudaEventRecord(e1, st));
+    PEXP_CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    check_err(st);
+    if (st_out) {
+      std::memset(st_out, 0, sizeof(*st_out));
+      st_out->wr_iters = iters;
+      st_out->wr_last_delta = delta;
+      st_out->max_m = max_m;
+      st_out->max_k = max_k;
+      st_out->ms_total = ms;
+      st_out->evals = P * iters;
+      st_out->kernel_launches = (int)g_launches;
+    }
+  });
+}
+
+pexp_status pexp_sai_solve(pexp_ctx* ctx, int32_t b, double gamma, const double* rhs, int32_t ncols, double* x) {
+  if (!ctx) return PEXP_EINVAL;
+  if (b < 0 || b >= ctx->batch || !(gamma > 0) || ncols < 0 || !rhs || !x) return set_err(ctx, PEXP_EINVAL, "bad argument");
+  if (!ctx->ws || ctx->ws_bytes < lin_bytes(ctx, 1)) return set_err(ctx, PEXP_ENOMEM, "workspace not set or too small");
+  return guarded(ctx, [&] {
+    init_once();
+    Opts o = norm_opts(ctx->opt);
+    cudaStream_t st = o.st;
+    const int n = (int)ctx->n;
+    Arena ar{ctx->ws, ctx->ws_bytes, 0};
+    LinPlan L;
+    plan_linear(ar, L, ctx, 1);
+    std::vector<double> nu1{ctx->nu[b]}, a1{ctx->a[b]}, g1{gamma};
+    std::vector<int> z1{0};
+    h2d(st, L.nu_d, nu1);
+    h2d(st, L.a_d, a1);
+    h2d(st, L.gam_f, g1);
+    h2d(st, L.opidx_f, z1);
+    Ops O1 = L.O;
+    O1.nops = 1;
+    launch_ade_rows(st, 1, n, ctx->bc == PEXP_BC_DIRICHLET, L.nu_d, L.a_d, O1.sub, O1.diag, O1.sup);
+    PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
+    launch_factor(st, L.F, 1, L.opidx_f, L.gam_f, O1, L.err);
+    launch_sai_solve(st, L.F, nullptr, 1, ncols, rhs, 0, 0, x, 0, 0, nullptr);
+    int herr = 0;
+    PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
+  });
+}
+
+pexp_status pexp_source_svd(pexp_ctx* ctx, const double* G, int32_t E, double tol, int32_t* m_host, double* sigma,
+                            double* proj) {
+  if (!ctx) return PEXP_EINVAL;
+  if (!G || !m_host || !sigma || !proj || E < 1) return set_err(ctx, PEXP_EINVAL, "bad argument");
+  if (!(tol >= 1e-14 && tol <= 1e-2)) return set_err(ctx, PEXP_EINVAL, "tol must be in [1e-14, 1e-2]");
+  Opts o0 = norm_opts(ctx->opt);
+  int Pneed = (E + ctx->batch - 1) / ctx->batch;
+  if (!ctx->ws || ctx->ws_bytes < lin_bytes(ctx, Pneed)) return set_err(ctx, PEXP_ENOMEM, "workspace too small");
+  (void)o0;
+  return guarded(ctx, [&] {
+    init_once();
+    Opts o = norm_opts(ctx->opt);
+    cudaStream_t st = o.st;
+    const int n = (int)ctx->n, s = o.s;
+    Arena ar{ctx->ws, ctx->ws_bytes, 0};
+    LinPlan L;
+    plan_linear(ar, L, ctx, Pneed);
+    L.B.E = E;
+    const double tau = o.tau_f * tol;
+    int mmax = svd_stage(st, L.S, &L.B, E, n, s, G, tau, o.eta_f * tol, 1.0, m_host);
+    PEXP_CUDA_TRY(cudaMemcpyAsync(sigma, L.S.sig, size_t(E) * s * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int mb = std::max(mmax, 1);
+    launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, mb, L.S.Cfin, (long long)mb * s, mb, proj, (long long)s * n, 0, s, 1.0,
+                   0.0, nullptr);
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+  });
+}
+
+pexp_status pexp_expm_batched(pexp_ctx* ctx, const double* A, int32_t E, int32_t N, double* X) {
+  if (!ctx) return PEXP_EINVAL;
+  if (!A || !X || E < 1 || N < 1 || N > 1024) return set_err(ctx, PEXP_EINVAL, "bad argument");
+  const int nslots = std::min(E, 148);
+  const size_t need = size_t(nslots) * (7ull * N * N * sizeof(double) + N * sizeof(int)) + 1024;
+  if (!ctx->ws || ctx->ws_bytes < need) return set_err(ctx, PEXP_ENOMEM, "workspace too small for expm");
+  return guarded(ctx, [&] {
+    init_once();
+    Opts o = norm_opts(ctx->opt);
+    Arena ar{ctx->ws, ctx->ws_bytes, 0};
+    double* work = ar.take<double>(size_t(nslots) * 7 * N * N);
+    int* iwork = ar.take<int>(size_t(nslots) * N);
+    launch_expm_batched(o.st, E, N, A, X, work, 7LL * N * N, iwork, nslots);
+    PEXP_CUDA_TRY(cudaStreamSynchronize(o.st));
+  });
+}
+
+void pexp_profile_enable(int32_t on) {
+  for (auto& r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  g_prof.clear();
+  g_prof_on = on != 0;
+}
+
+int32_t pexp_profile_read(int32_t ncat, double* ms, double* bytes, double* flops, int32_t* launches) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  for (int c = 0; c < ncat; ++c) { ms[c] = 0; bytes[c] = 0; flops[c] = 0; launches[c] = 0; }
+  for (auto& r : g_prof) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.cat < ncat) { ms[r.cat] += t; bytes[r.cat] += r.bytes; flops[r.cat] += r.flops; launches[r.cat] += 1; }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  return PC_NCAT;
+}
+
+}  // extern "C"

@@ -1,0 +1,643 @@
+// small.cu — one-CTA-per-evaluation dense kernels on the small projected quantities:
+//   * k_sym_eig_select  : cyclic parallel Jacobi eigensolver of an s x s source Gram matrix
+//                         (subsystem 3, "Gram matrix plus small Jacobi eigensolve") and the
+//                         pass selection of the two-pass rank-revealing source SVD
+//   * k_block_chol      : scaled, deflating Cholesky of a block Gram matrix -> R, R^{-1}
+//                         (Cholesky-QR of Arnoldi blocks and of the source basis)
+//   * k_onesided_svd    : one-sided (Hestenes) Jacobi SVD of the projected coefficient matrix
+//                         C = U^T G, final truncation m_j = #{sigma > tau*sigma_1}
+//   * k_build_final     : selection matrices for U_final = U Q[:, :m] and coefficient rows
+//   * k_spline          : not-a-knot cubic p(t) per coefficient row
+//   * k_small_problem   : projected SaI problem: H^{-1}, A_hat = (I - H^{-1})/gamma, Pade-13
+//                         exponential of the augmented matrix, exact chaining over the cubic
+//                         pieces, residual norms at every node (subsystem 4)
+#include "common.cuh"
+#include "dense.cuh"
+#include "kernels.cuh"
+
+namespace pexp {
+
+constexpr int MAXS = 64;
+constexpr size_t SM2 = 2 * MAXS * (MAXS + 1) * sizeof(double);  // two padded 64x64 tiles
+
+__device__ inline void jacobi_pair(int Ne, int r, int k, int& p, int& q) {
+  if (k == 0) {
+    p = r;
+    q = Ne - 1;
+  } else {
+    p = (r + k) % (Ne - 1);
+    q = (r - k + (Ne - 1)) % (Ne - 1);
+  }
+  if (p > q) { int t = p; p = q; q = t; }
+}
+
+__device__ inline void sym_schur2(double app, double aqq, double apq, double& c, double& s) {
+  if (fabs(apq) < 1e-300) { c = 1.0; s = 0.0; return; }
+  double tau = (aqq - app) / (2.0 * apq);
+  double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
+  c = 1.0 / sqrt(1.0 + t * t);
+  s = t * c;
+}
+
+// ---------------------------------------------------------------- Jacobi eig + selection
+// G: [E][s][s] (col-major s x s).  Pass `pass` of the two-pass SVD: keep eigenpairs with
+// sigma_i = sqrt(lambda_i) > theta*sigma_max(pass) and > 0.5*tau*sigma1 (sigma1 from pass 0),
+// write Msel[:, off + c] = q_i / sigma_i (all other columns 0), off += kept.
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off, double* sigma1,
+                 int pass, double tau, double theta, const int* active) {
+  const int e = blockIdx.x;
+  extern __shared__ double dsm[];
+  double (*A)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm);
+  double (*Q)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm + MAXS * (MAXS + 1));
+  __shared__ double rc[MAXS / 2], rs[MAXS / 2];
+  __shared__ int rp[MAXS / 2], rq[MAXS / 2];
+  __shared__ int perm[MAXS];
+  __shared__ double red[32];
+  double* M = Msel + size_t(e) * s * s;
+  if (active && !active[e]) {
+    for (int i = threadIdx.x; i < s * s; i += blockDim.x) M[i] = 0.0;
+    return;
+  }
+  const int Ne = s + (s & 1);
+  const double* Ge = G + size_t(e) * s * s;
+  for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+    int i = idx % Ne, j = idx / Ne;
+    A[i][j] = (i < s && j < s) ? 0.5 * (Ge[i + j * s] + Ge[j + i * s]) : 0.0;
+    Q[i][j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off2 = 0.0, dg2 = 0.0;
+    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+      int i = idx % Ne, j = idx / Ne;
+      double v = A[i][j] * A[i][j];
+      if (i == j) dg2 += v; else off2 += v;
+    }
+    off2 = block_sum(off2, red);
+    dg2 = block_sum(dg2, red);
+    if (off2 <= 1e-32 * dg2 || off2 == 0.0) break;
+    for (int r = 0; r < Ne - 1; ++r) {
+      if (threadIdx.x < Ne / 2) {
+        int p, q;
+        jacobi_pair(Ne, r, threadIdx.x, p, q);
+        double c, sn;
+        sym_schur2(A[p][p], A[q][q], A[p][q], c, sn);
+        rp[threadIdx.x] = p; rq[threadIdx.x] = q; rc[threadIdx.x] = c; rs[threadIdx.x] = sn;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < (Ne / 2) * Ne; idx += blockDim.x) {  // rows
+        int k = idx / Ne, j = idx % Ne, p = rp[k], q = rq[k];
+        double c = rc[k], sn = rs[k], ap = A[p][j], aq = A[q][j];
+        A[p][j] = c * ap - sn * aq;
+        A[q][j] = sn * ap + c * aq;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < (Ne / 2) * Ne; idx += blockDim.x) {  // columns
+        int k = idx / Ne, j = idx % Ne, p = rp[k], q = rq[k];
+        double c = rc[k], sn = rs[k], ap = A[j][p], aq = A[j][q];
+        A[j][p] = c * ap - sn * aq;
+        A[j][q] = sn * ap + c * aq;
+        double qp = Q[j][p], qq = Q[j][q];
+        Q[j][p] = c * qp - sn * qq;
+        Q[j][q] = sn * qp + c * qq;
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < s; ++i) perm[i] = i;
+    for (int i = 0; i < s; ++i) {
+      int b = i;
+      for (int j = i + 1; j < s; ++j)
+        if (A[perm[j]][perm[j]] > A[perm[b]][perm[b]]) b = j;
+      int t = perm[i]; perm[i] = perm[b]; perm[b] = t;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s; i += blockDim.x) lam_out[size_t(e) * s + i] = fmax(A[perm[i]][perm[i]], 0.0);
+  for (int i = threadIdx.x; i < s * s; i += blockDim.x) M[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double smax = sqrt(fmax(A[perm[0]][perm[0]], 0.0));
+    if (pass == 0) sigma1[e] = smax;
+    const double thr = 0.5 * tau * sigma1[e];
+    int o = off[e], kept = 0;
+    for (int i = 0; i < s && o + kept < s; ++i) {
+      double sg = sqrt(fmax(A[perm[i]][perm[i]], 0.0));
+      if (!(sg > theta * smax) || !(sg > thr)) break;
+      ++kept;
+    }
+    off[e] = o + kept;
+    rq[0] = o;
+    rq[1] = kept;
+  }
+  __syncthreads();
+  const int o = rq[0], kept = rq[1];
+  for (int idx = threadIdx.x; idx < kept * s; idx += blockDim.x) {
+    int c = idx / s, i = idx % s;
+    double sg = sqrt(fmax(A[perm[c]][perm[c]], 0.0));
+    M[i + size_t(o + c) * s] = Q[i][perm[c]] / sg;
+  }
+}
+
+// ---------------------------------------------------------------- deflating Cholesky-QR
+// G: [E] N x N Gram (ld ldg, stride gs_e).  norm0 (nullable): squared norms of the columns
+// before orthogonalisation against the previous basis; a column is deflated (dead) when
+// G_kk <= defl^2 * norm0_k, when G_kk == 0, or when its scaled Cholesky pivot is <= 1e-14
+// (it lies within 1e-7 of the span of the earlier columns of the block).
+// Outputs Rinv (N x N, ld N, stride N*N): Q = W Rinv has orthonormal live columns and zero
+// dead columns; R (= R_this * Rprev if Rprev) written to Rout (ld ldr, stride rs_e);
+// live flags to live (stride ls_e).
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm0, long long ns_e,
+             int ldn, double defl, double* Rinv, const double* Rprev, long long rps_e, int ldrp, double* Rout,
+             long long rs_e, int ldr, int* live, long long ls_e, const int* active) {
+  const int e = blockIdx.x;
+  if (active && !active[e]) return;
+  extern __shared__ double dsm[];
+  double (*L)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm);
+  double (*X)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm + MAXS * (MAXS + 1));
+  __shared__ double d[MAXS];
+  __shared__ int dead[MAXS];
+  const double* Ge = G + e * gs_e;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    double g = Ge[k + size_t(k) * ldg];
+    bool dk = !(g > 0.0);
+    if (norm0 && !(g > defl * defl * norm0[e * ns_e + k + size_t(k) * ldn])) dk = true;
+    dead[k] = dk;
+    d[k] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int i = idx % N, j = idx / N;
+    L[i][j] = d[i] * d[j] * 0.5 * (Ge[i + size_t(j) * ldg] + Ge[j + size_t(i) * ldg]);
+  }
+  __syncthreads();
+  __shared__ double s_piv;
+  for (int k = 0; k < N; ++k) {
+    if (threadIdx.x == 0) {
+      double p = L[k][k];
+      if (dead[k] || !(p > 1e-14)) {
+        dead[k] = 1;
+        s_piv = 0.0;
+      } else {
+        s_piv = sqrt(p);
+      }
+    }
+    __syncthreads();
+    const double pv = s_piv;
+    for (int i = k + threadIdx.x; i < N; i += blockDim.x) L[i][k] = (pv > 0.0) ? (i == k ? pv : L[i][k] / pv) : 0.0;
+    __syncthreads();
+    if (pv > 0.0) {
+      const int h = N - k - 1;
+      for (int idx = threadIdx.x; idx < h * h; idx += blockDim.x) {
+        int i = k + 1 + idx % h, j = k + 1 + idx / h;
+        if (j <= i) L[i][j] -= L[i][k] * L[j][k];
+      }
+    }
+    __syncthreads();
+  }
+  // Rs = L^T (upper): Rs[k][j] = L[j][k] for j >= k.  X = Rs^{-1} on live rows/cols.
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    for (int k = 0; k < N; ++k) X[k][j] = 0.0;
+    if (!dead[j]) {
+      for (int k = j; k >= 0; --k) {
+        if (dead[k]) continue;
+        double sum = (k == j) ? 1.0 : 0.0;
+        for (int p = k + 1; p <= j; ++p) sum -= L[p][k] * X[p][j];
+        X[k][j] = sum / L[k][k];
+      }
+    }
+  }
+  __syncthreads();
+  double* Ri = Rinv + size_t(e) * N * N;
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int k = idx % N, j = idx / N;
+    Ri[idx] = d[k] * X[k][j];
+  }
+  if (live)
+    for (int k = threadIdx.x; k < N; k += blockDim.x) live[e * ls_e + k] = dead[k] ? 0 : 1;
+  // R = Rs D^{-1}: R[k][j] = L[j][k] / d[j]  (j >= k), 0 if d[j] == 0
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int k = idx % N, j = idx / N;
+    X[k][j] = (j >= k && d[j] > 0.0) ? L[j][k] / d[j] : 0.0;
+  }
+  __syncthreads();
+  if (Rout) {
+    double* Ro = Rout + e * rs_e;
+    for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+      int k = idx % N, j = idx / N;
+      double v;
+      if (Rprev) {
+        const double* Rp = Rprev + e * rps_e;
+        v = 0.0;
+        for (int p = k; p <= j; ++p) v += X[k][p] * Rp[p + size_t(j) * ldrp];
+      } else {
+        v = X[k][j];
+      }
+      Ro[k + size_t(j) * ldr] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- one-sided Jacobi SVD
+// C: [E] s x s col-major; rows 0..kk-1 are the coefficients U^T G of the current basis.
+// Produces Qs (s x s, columns = left singular vectors of C, sorted by sigma desc),
+// sig [E][s], Cs (s x s: row c = sigma_c * v_c^T) and m[e] = #{sigma > tau*sigma_1}.
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_onesided_svd(int s, const double* C, const int* kk_arr, double tau, double* Qs, double* sig,
+               double* Cs, int* m_out, const int* active) {
+  const int e = blockIdx.x;
+  extern __shared__ double dsm[];
+  double (*W)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm);  // W[j][i] = row j of C
+  double (*Q)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm + MAXS * (MAXS + 1));
+  __shared__ double nrm[MAXS];
+  __shared__ int perm[MAXS];
+  __shared__ int s_conv;
+  if (active && !active[e]) {
+    if (threadIdx.x == 0) m_out[e] = 0;
+    return;
+  }
+  const int kk = kk_arr[e];
+  const int Ne = kk + (kk & 1);
+  const double* Ce = C + size_t(e) * s * s;
+  for (int idx = threadIdx.x; idx < MAXS * MAXS; idx += blockDim.x) {
+    int j = idx / MAXS, i = idx % MAXS;
+    W[j][i] = (j < kk && i < s) ? Ce[j + size_t(i) * s] : 0.0;
+    Q[j][i] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int g = threadIdx.x / 8, lg = threadIdx.x % 8;  // 32 groups of 8 lanes
+  for (int sweep = 0; sweep < 60 && Ne >= 2; ++sweep) {
+    if (threadIdx.x == 0) s_conv = 1;
+    __syncthreads();
+    for (int r = 0; r < Ne - 1; ++r) {
+      const bool act = g < Ne / 2;
+      int p = 0, q = 0;
+      if (act) jacobi_pair(Ne, r, g, p, q);
+      double al = 0.0, be = 0.0, ga = 0.0;
+      if (act)
+        for (int i = lg; i < s; i += 8) {
+          double wp = W[p][i], wq = W[q][i];
+          al += wp * wp; be += wq * wq; ga += wp * wq;
+        }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {  // reduce within the 8-lane group (all lanes execute)
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      if (act && fabs(ga) > 1e-15 * sqrt(al * be) && fabs(ga) > 1e-300) {
+        if (lg == 0) s_conv = 0;
+        double zeta = (be - al) / (2.0 * ga);
+        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+        double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        for (int i = lg; i < s; i += 8) {
+          double wp = W[p][i], wq = W[q][i];
+          W[p][i] = c * wp - sn * wq;
+          W[q][i] = sn * wp + c * wq;
+        }
+        for (int i = lg; i < kk; i += 8) {
+          double qp = Q[i][p], qq = Q[i][q];
+          Q[i][p] = c * qp - sn * qq;
+          Q[i][q] = sn * qp + c * qq;
+        }
+      }
+      __syncthreads();
+    }
+    if (s_conv) break;
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < MAXS; j += blockDim.x) {
+    double a = 0.0;
+    if (j < kk)
+      for (int i = 0; i < s; ++i) a += W[j][i] * W[j][i];
+    nrm[j] = sqrt(a);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < s; ++i) perm[i] = i;
+    for (int i = 0; i < kk; ++i) {
+      int b = i;
+      for (int j = i + 1; j < kk; ++j)
+        if (nrm[perm[j]] > nrm[perm[b]]) b = j;
+      int t = perm[i]; perm[i] = perm[b]; perm[b] = t;
+    }
+    int m = 0;
+    double s1 = kk > 0 ? nrm[perm[0]] : 0.0;
+    if (s1 > 0.0)
+      for (int i = 0; i < kk; ++i)
+        if (nrm[perm[i]] > tau * s1) ++m;
+    m_out[e] = m;
+  }
+  __syncthreads();
+  double* Qe = Qs + size_t(e) * s * s;
+  double* Ce2 = Cs + size_t(e) * s * s;
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) {
+    int i = idx % s, c = idx / s;  // Qe[i + c*s] = Q[i][perm[c]]
+    Qe[idx] = (c < kk && i < kk) ? Q[i][perm[c]] : 0.0;
+    // Ce2 row c, column i  (col-major s x s: Ce2[c + i*s])
+    int cc = idx % s, ii = idx / s;
+    Ce2[cc + size_t(ii) * s] = (cc < kk) ? W[perm[cc]][ii] : 0.0;
+  }
+  for (int c = threadIdx.x; c < s; c += blockDim.x) sig[size_t(e) * s + c] = c < kk ? nrm[perm[c]] : 0.0;
+}
+
+// Msel_e (s x mmax) = Qs[:, :mmax] restricted to kk columns with nonzero sigma; Cfin_e (mmax x s)
+// = rows c < m_e of Cs, zero otherwise; fill[e*mmax + c] = 1 where U_final column c must be
+// replaced by a (pseudo-random, then orthonormalised) padding vector.
+__global__ void k_build_final(int s, int mmax, const int* kk_arr, const double* Qs, const double* sig,
+                              const double* Cs, const int* m_arr, double* Msel, double* Cfin, int* fill) {
+  const int e = blockIdx.x;
+  const int kk = kk_arr[e], m = m_arr[e];
+  const double* Qe = Qs + size_t(e) * s * s;
+  const double* Ce = Cs + size_t(e) * s * s;
+  double* Me = Msel + size_t(e) * s * mmax;
+  double* Fe = Cfin + size_t(e) * mmax * s;
+  for (int idx = threadIdx.x; idx < s * mmax; idx += blockDim.x) {
+    int i = idx % s, c = idx / s;
+    bool ok = c < kk && sig[size_t(e) * s + c] > 0.0;
+    Me[idx] = ok ? Qe[i + size_t(c) * s] : 0.0;
+    int cr = idx % mmax, ic = idx / mmax;  // Cfin col-major mmax x s
+    Fe[cr + size_t(ic) * mmax] = (cr < m) ? Ce[cr + size_t(ic) * s] : 0.0;
+  }
+  for (int c = threadIdx.x; c < mmax; c += blockDim.x)
+    fill[e * mmax + c] = !(c < kk && sig[size_t(e) * s + c] > 0.0);
+}
+
+// ---------------------------------------------------------------- not-a-knot spline
+// Kinv: inverse of the s x s not-a-knot second-derivative system (host-computed, depends
+// only on s).  Cfin_e: mmax x s samples.  coef_e: [s-1][4][mmax] Taylor coefficients
+// (p, p', p'', p''') at the left node of each piece; crit[e] = eta * max_i ||Cfin[:, i]||.
+__global__ void k_spline(int s, int mmax, const double* Kinv, const double* Cfin, double h, double eta,
+                         double* coef, double* crit, const int* active) {
+  const int e = blockIdx.x;
+  extern __shared__ double sm[];
+  double* Y = sm;              // [mmax][s]
+  double* R = sm + mmax * s;   // [mmax][s]
+  double* Mv = R + mmax * s;   // [mmax][s]
+  __shared__ double red[32];
+  const double* Ce = Cfin + size_t(e) * mmax * s;
+  for (int idx = threadIdx.x; idx < mmax * s; idx += blockDim.x) {
+    int c = idx / s, i = idx % s;
+    Y[idx] = Ce[c + size_t(i) * mmax];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < mmax * s; idx += blockDim.x) {
+    int c = idx / s, i = idx % s;
+    R[idx] = (i == 0 || i == s - 1) ? 0.0 : 6.0 * (Y[c * s + i + 1] - 2.0 * Y[c * s + i] + Y[c * s + i - 1]) / (h * h);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < mmax * s; idx += blockDim.x) {
+    int c = idx / s, i = idx % s;
+    double a = 0.0;
+    for (int k = 0; k < s; ++k) a += Kinv[i + k * s] * R[c * s + k];
+    Mv[idx] = a;
+  }
+  __syncthreads();
+  double* ce = coef + size_t(e) * (s - 1) * 4 * mmax;
+  for (int idx = threadIdx.x; idx < mmax * (s - 1); idx += blockDim.x) {
+    int c = idx % mmax, i = idx / mmax;
+    double y0 = Y[c * s + i], y1 = Y[c * s + i + 1], m0 = Mv[c * s + i], m1 = Mv[c * s + i + 1];
+    double* o = ce + size_t(i) * 4 * mmax;
+    o[0 * mmax + c] = y0;
+    o[1 * mmax + c] = (y1 - y0) / h - h * (2.0 * m0 + m1) / 6.0;
+    o[2 * mmax + c] = m0;
+    o[3 * mmax + c] = (m1 - m0) / h;
+  }
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    double a = 0.0;
+    for (int c = 0; c < mmax; ++c) a += Y[c * s + i] * Y[c * s + i];
+    mx = fmax(mx, sqrt(a));
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) crit[e] = eta * mx;
+  (void)active;
+}
+
+// ---------------------------------------------------------------- projected SaI problem
+__global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
+  __shared__ int idx[KSMALL_MAX];
+  __shared__ int tidx[MAXS], lpos[MAXS];
+  __shared__ int s_K, s_mt, s_ml;
+  __shared__ double red[32];
+  __shared__ double xs[MAXS], ts[MAXS];
+  extern __shared__ double zsm[];  // 2 * KSMALL_MAX doubles
+  double* z = zsm;
+  double* zn = zsm + KSMALL_MAX;
+  const int slot = blockIdx.x;
+  double* S0 = a.work + slot * a.work_slot;
+  const int ld = a.Nmax;
+  const size_t MM = size_t(ld) * ld;
+  double* S1 = S0 + MM;
+  double* S2 = S1 + MM;
+  double* WK = S2 + MM;
+  int* piv = a.iwork + slot * a.iwork_slot;
+  const int K = a.K, m = a.m;
+  for (int e = blockIdx.x; e < a.E; e += gridDim.x) {
+    if (a.active && !a.active[e]) continue;
+    const double* He = a.H + e * a.hs_e;
+    const int* lv = a.live + e * a.ls_e;
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int c = 0; c < K; ++c)
+        if (lv[c]) idx[k++] = c;
+      s_K = k;
+      int mt = 0;
+      for (int c = K; c < K + m; ++c)
+        if (lv[c]) tidx[mt++] = c;
+      s_mt = mt;
+      int ml = 0;
+      for (int r = 0; r < k; ++r)
+        if (idx[r] >= K - m) lpos[ml++] = r;
+      s_ml = ml;
+    }
+    __syncthreads();
+    const int Kp = s_K, mt = s_mt, ml = s_ml;
+    const double gam = a.gam[e];
+    const int forced = a.kind == 0;
+    const int Nn = Kp + (forced ? 4 * m : 0);
+    // Hs -> S0, Hinv -> S1
+    for (int t = threadIdx.x; t < Kp * Kp; t += blockDim.x) {
+      int i = t % Kp, j = t / Kp;
+      S0[i + size_t(j) * ld] = He[idx[i] + size_t(idx[j]) * a.ldh];
+    }
+    __syncthreads();
+    cta_identity(Kp, S1, ld);
+    cta_lu(Kp, S0, ld, piv, red);
+    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp);
+    // augmented matrix in S2
+    for (int t = threadIdx.x; t < Nn * Nn; t += blockDim.x) {
+      int i = t % Nn, j = t / Nn;
+      double v = 0.0;
+      if (i < Kp && j < Kp) v = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
+      else if (forced && i < m && j >= Kp && j < Kp + m && (j - Kp) == i) v = a.h;
+      else if (forced && i >= Kp && j >= Kp && j - i == m && i < Kp + 3 * m) v = 1.0;
+      S2[i + size_t(j) * ld] = v;
+    }
+    __syncthreads();
+    cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red);
+    // chain
+    const int np = a.npieces ? a.npieces[e] : a.npieces_const;
+    for (int r = threadIdx.x; r < Kp; r += blockDim.x) z[r] = (!forced && r == 0) ? a.beta[e] : 0.0;
+    double* Ze = a.Z + e * a.zs_e;
+    for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[idx[r]] = z[r];
+    double maxres = 0.0;
+    const double* cf = forced ? a.coef + size_t(e) * (a.s - 1) * 4 * m : nullptr;
+    for (int i = 0; i < np; ++i) {
+      __syncthreads();
+      for (int r = threadIdx.x; r < Kp; r += blockDim.x) {
+        double v = 0.0;
+        for (int j = 0; j < Kp; ++j) v = fma(S2[r + size_t(j) * ld], z[j], v);
+        if (forced) {
+          const double* ci = cf + size_t(i) * 4 * m;
+          double hq = 1.0;
+          for (int q = 0; q < 4; ++q) {
+            const double* B = S2 + size_t(Kp + q * m) * ld;
+            double acc = 0.0;
+            for (int c = 0; c < m; ++c) acc = fma(B[r + size_t(c) * ld], ci[q * m + c], acc);
+            v = fma(hq, acc, v);
+            hq *= a.h;
+          }
+        }
+        zn[r] = v;
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < Kp; r += blockDim.x) z[r] = zn[r];
+      __syncthreads();
+      const int node = i + 1;
+      if (node % a.out_stride == 0 && node / a.out_stride < a.nout)
+        for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[size_t(node / a.out_stride) * a.kcap + idx[r]] = z[r];
+      // residual ||r(t)|| = (1/gamma) || (I - gamma A) Vtail Htail x ||, x = (H^{-1} z)[last block]
+      if (mt > 0) {
+        for (int c = threadIdx.x; c < ml; c += blockDim.x) {
+          double v = 0.0;
+          const int row = lpos[c];
+          for (int j = 0; j < Kp; ++j) v = fma(S1[row + size_t(j) * ld], z[j], v);
+          xs[c] = v;
+        }
+        __syncthreads();
+        for (int tc = threadIdx.x; tc < mt; tc += blockDim.x) {
+          double v = 0.0;
+          for (int c = 0; c < ml; ++c) v = fma(He[tidx[tc] + size_t(idx[lpos[c]]) * a.ldh], xs[c], v);
+          ts[tc] = v;
+        }
+        __syncthreads();
+        double part = 0.0;
+        if (a.stop_rule == 1) {  // ||(I - gamma A) Vtail t||^2 = t^T Gt t
+          const double* Gt = a.Gt + e * a.gts_e;
+          for (int p = threadIdx.x; p < mt * mt; p += blockDim.x) {
+            int i1 = p % mt, i2 = p / mt;
+            part += ts[i1] * Gt[(tidx[i1] - K) + size_t(tidx[i2] - K) * m] * ts[i2];
+          }
+        } else {                 // ||Vtail t||^2 = ||t||^2 (orthonormal tail)
+          for (int p = threadIdx.x; p < mt; p += blockDim.x) part += ts[p] * ts[p];
+        }
+        double r2 = block_sum(part, red);
+        maxres = fmax(maxres, sqrt(fmax(r2, 0.0)) / gam);
+      }
+    }
+    if (threadIdx.x == 0) {
+      a.res[e] = maxres;
+      int cv = (mt == 0) || (maxres <= a.crit[e]);
+      a.conv[e] = cv;
+      if (cv && a.kfin) a.kfin[e] = K;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- batched expm (stage API)
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_expm_batched(int E, int N, const double* A, double* X, double* work, long long work_slot, int* iwork) {
+  __shared__ double red[32];
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    double* Xe = X + size_t(e) * N * N;
+    const double* Ae = A + size_t(e) * N * N;
+    for (int t = threadIdx.x; t < N * N; t += blockDim.x) Xe[t] = Ae[t];
+    __syncthreads();
+    cta_expm_pade13(N, Xe, N, work + blockIdx.x * work_slot, N, iwork + blockIdx.x * N, red);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- host wrappers
+void launch_sym_eig_select(cudaStream_t st, int E, int s, const double* G, double* lam, double* Msel,
+                           int* off, double* sigma1, int pass, double tau, double theta, const int* active) {
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_sym_eig_select<<<E, PEXP_THREADS, SM2, st>>>(s, G, lam, Msel, off, sigma1, pass, tau, theta, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long gs_e, int ldg,
+                       const double* norm0, long long ns_e, int ldn, double defl, double* Rinv, const double* Rprev,
+                       long long rps_e, int ldrp, double* Rout, long long rs_e, int ldr, int* live,
+                       long long ls_e, const int* active) {
+  if (N > MAXS) fail(1, "block width > 64 not supported");
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_block_chol<<<E, PEXP_THREADS, SM2, st>>>(N, G, gs_e, ldg, norm0, ns_e, ldn, defl, Rinv, Rprev, rps_e, ldrp,
+                                            Rout, rs_e, ldr, live, ls_e, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_onesided_svd(cudaStream_t st, int E, int s, const double* C, const int* kk, double tau,
+                         double* Qs, double* sig, double* Cs, int* m_out, const int* active) {
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_onesided_svd<<<E, PEXP_THREADS, SM2, st>>>(s, C, kk, tau, Qs, sig, Cs, m_out, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, const double* Qs,
+                        const double* sig, const double* Cs, const int* m, double* Msel, double* Cfin,
+                        int* fill) {
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_build_final<<<E, PEXP_THREADS, 0, st>>>(s, mmax, kk, Qs, sig, Cs, m, Msel, Cfin, fill);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, const double* Cfin,
+                   double h, double eta, double* coef, double* crit) {
+  size_t smem = size_t(3) * mmax * s * sizeof(double);
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_spline<<<E, PEXP_THREADS, smem, st>>>(s, mmax, Kinv, Cfin, h, eta, coef, crit, nullptr);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots) {
+  if (a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
+  size_t smem = 2 * KSMALL_MAX * sizeof(double);
+  {
+  const double N = a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
+  ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
+  k_small_problem<<<std::min(a.E, nslots), PEXP_THREADS, smem, st>>>(a);
+  }
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
+                         long long work_slot, int* iwork, int nslots) {
+  k_expm_batched<<<std::min(E, nslots), PEXP_THREADS, 0, st>>>(E, N, A, X, work, work_slot, iwork);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void small_init() {
+  cudaFuncSetAttribute(k_sym_eig_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
+  cudaFuncSetAttribute(k_block_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
+  cudaFuncSetAttribute(k_onesided_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
+  cudaFuncSetAttribute(k_small_problem, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KSMALL_MAX * 8);
+  cudaFuncSetAttribute(k_spline, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * 64 * 8);
+}
+
+}  // namespace pexp

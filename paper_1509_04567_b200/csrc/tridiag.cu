@@ -1,0 +1,297 @@
+// tridiag.cu — subsystem (1): batched shift-and-invert solves x = (I - gamma*A)^{-1} b
+// for tridiagonal (Dirichlet) and periodic-tridiagonal A (PAPER.md:176 shift-and-invert;
+// DESIGN.md §5.1).
+//
+// Design (B200): each (operator, gamma) pair is factored ONCE per solve/WR iteration
+// (Thomas LU of the tridiagonal part T plus the Sherman–Morrison vectors of the periodic
+// corners, M = T + u v^T), and every Krylov right-hand side is then solved by two
+// HBM-streaming passes in one CTA: the first-order recurrences of the L- and U-solves
+// are affine maps y_i = a_i y_{i-1} + b_i, evaluated as a chunked block-wide parallel
+// scan (8 consecutive rows per thread in registers, warp-shuffle + shared-memory scan of
+// the composed maps, carry across 2048-row chunks).  The periodic correction
+// x = T^{-1}b - (w'^T b) z needs only a dot product with a precomputed w' = T^{-T}v/(1+v^T z),
+// accumulated during the forward pass, so no third pass is needed.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pexp {
+
+// ---------------------------------------------------------------- operator rows
+// A = nu*D2 - a*D1: sub = nu/dx^2 + a/(2dx), diag = -2 nu/dx^2, sup = nu/dx^2 - a/(2dx).
+__global__ void k_ade_rows(int nops, int n, int dirichlet, const double* nu, const double* a,
+                           double* sub, double* diag, double* sup) {
+  int op = blockIdx.y;
+  double dx = dirichlet ? 1.0 / (n + 1) : 1.0 / n;
+  double d2 = nu[op] / (dx * dx), d1 = a[op] / (2.0 * dx);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    size_t k = size_t(op) * n + i;
+    sub[k] = d2 + d1;
+    diag[k] = -2.0 * d2;
+    sup[k] = d2 - d1;
+  }
+}
+
+// Burgers operator A_j = nu*D2 + J(ubar_j), J(u) = -diag(D1 u) - diag(u) D1 (PAPER.md:297-301,
+// reading #3): sub = nu/dx^2 + ubar_i/(2dx), diag = -2nu/dx^2 - (ubar_{i+1}-ubar_{i-1})/(2dx),
+// sup = nu/dx^2 - ubar_i/(2dx); periodic.
+__global__ void k_burgers_rows(int nops, int n, double nu, const double* ubar, double* sub,
+                               double* diag, double* sup) {
+  int op = blockIdx.y;
+  double dx = 1.0 / n, d2 = nu / (dx * dx), inv2dx = 1.0 / (2.0 * dx);
+  const double* u = ubar + size_t(op) * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int im = i == 0 ? n - 1 : i - 1, ip = i == n - 1 ? 0 : i + 1;
+    size_t k = size_t(op) * n + i;
+    double ui = u[i];
+    sub[k] = d2 + ui * inv2dx;
+    diag[k] = -2.0 * d2 - (u[ip] - u[im]) * inv2dx;
+    sup[k] = d2 - ui * inv2dx;
+  }
+}
+
+// ---------------------------------------------------------------- factorisation
+// One thread per factor f: M = I - gamma_f A_{op_f}.  Writes l (multipliers), dinv (1/pivot),
+// msup (super-diagonal of M), and for periodic z = T^{-1}u, w' = T^{-T}v/(1+v^T z)
+// with the Numerical-Recipes splitting u = (gs,0..,0,alpha), v = (1,0..,0,beta/gs), gs = -M_00.
+__global__ void k_factor(int nf, int n, int periodic, const int* opidx, const double* gam,
+                         const double* sub, const double* diag, const double* sup, double* fl,
+                         double* fdinv, double* fsup, double* fz, double* fw, int* err) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const double g = gam[f];
+  const size_t o = size_t(opidx ? opidx[f] : f) * n, fo = size_t(f) * n;
+  const double *A = sub + o, *B = diag + o, *C = sup + o;
+  double *l = fl + fo, *di = fdinv + fo, *cs = fsup + fo;
+  const double d0 = 1.0 - g * B[0];
+  double alpha = 0.0, beta = 0.0, gs = 0.0;
+  if (periodic) {
+    beta = -g * A[0];       // M[0][n-1]
+    alpha = -g * C[n - 1];  // M[n-1][0]
+    gs = -d0;
+  }
+  double dprev = periodic ? d0 - gs : d0;
+  // pivots must be finite and not tiny relative to their row (no positivity needed: in the
+  // cell-Peclet > 2 regime the periodic corner legitimately makes the last pivot negative)
+  bool bad = !(fabs(dprev) > 1e-13 * fabs(d0)) || !isfinite(dprev);
+  l[0] = 0.0;
+  di[0] = 1.0 / dprev;
+  for (int i = 0; i < n - 1; ++i) cs[i] = -g * C[i];
+  cs[n - 1] = 0.0;
+  for (int i = 1; i < n; ++i) {
+    double Ti = 1.0 - g * B[i];
+    if (periodic && i == n - 1) Ti -= alpha * beta / gs;
+    double li = (-g * A[i]) / dprev;
+    double d = Ti - li * cs[i - 1];
+    if (!(fabs(d) > 1e-13 * (fabs(Ti) + fabs(li * cs[i - 1]))) || !isfinite(d)) bad = true;
+    l[i] = li;
+    di[i] = 1.0 / d;
+    dprev = d;
+  }
+  if (periodic) {
+    double *z = fz + fo, *w = fw + fo;
+    // z = T^{-1} u
+    z[0] = gs;
+    for (int i = 1; i < n; ++i) z[i] = ((i == n - 1) ? alpha : 0.0) - l[i] * z[i - 1];
+    z[n - 1] = z[n - 1] * di[n - 1];
+    for (int i = n - 2; i >= 0; --i) z[i] = (z[i] - cs[i] * z[i + 1]) * di[i];
+    // w = T^{-T} v :  U^T q = v, then L^T w = q
+    const double vl = beta / gs;
+    w[0] = 1.0 * di[0];
+    for (int i = 1; i < n; ++i) w[i] = (((i == n - 1) ? vl : 0.0) - cs[i - 1] * w[i - 1]) * di[i];
+    for (int i = n - 2; i >= 0; --i) w[i] = w[i] - l[i + 1] * w[i + 1];
+    const double denom = 1.0 + z[0] + vl * z[n - 1];
+    if (!(fabs(denom) > 0.0) || !isfinite(denom)) bad = true;
+    const double inv = 1.0 / denom;
+    for (int i = 0; i < n; ++i) w[i] *= inv;
+  }
+  if (bad) atomicExch(err, 1);
+}
+
+// ---------------------------------------------------------------- affine-map block scan
+// Map f(y) = A*y + B.  compose(first, then) = then ∘ first.
+struct Aff {
+  double A, B;
+};
+__device__ __forceinline__ Aff after(Aff first, Aff then) {
+  return {then.A * first.A, fma(then.A, first.B, then.B)};
+}
+
+// Exclusive scan over the block (ordered by `rank`, 0..255) of the per-thread maps.
+// rank = threadIdx.x (forward) or 255 - threadIdx.x (reverse, REV = true); in the reverse
+// order the lane of rank-predecessor k-o is the PHYSICAL lane +o, hence shfl_down.
+// Returns the composition of all maps of lower rank (identity for rank 0) and, through
+// `total`, the composition of all 256.
+template <bool REV>
+__device__ __forceinline__ Aff block_excl_scan(Aff v, int rank, Aff* wsm, Aff& total) {
+  const int lane = rank & 31, w = rank >> 5;
+  Aff inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double pa = REV ? __shfl_down_sync(0xffffffffu, inc.A, o) : __shfl_up_sync(0xffffffffu, inc.A, o);
+    double pb = REV ? __shfl_down_sync(0xffffffffu, inc.B, o) : __shfl_up_sync(0xffffffffu, inc.B, o);
+    if (lane >= o) inc = after(Aff{pa, pb}, inc);
+  }
+  double ea = REV ? __shfl_down_sync(0xffffffffu, inc.A, 1) : __shfl_up_sync(0xffffffffu, inc.A, 1);
+  double eb = REV ? __shfl_down_sync(0xffffffffu, inc.B, 1) : __shfl_up_sync(0xffffffffu, inc.B, 1);
+  Aff exc = lane == 0 ? Aff{1.0, 0.0} : Aff{ea, eb};
+  __syncthreads();
+  if (lane == 31) wsm[w] = inc;
+  __syncthreads();
+  if (rank == 0) {
+    Aff acc{1.0, 0.0};
+    for (int k = 0; k < PEXP_THREADS / 32; ++k) {
+      Aff t = wsm[k];
+      wsm[k] = acc;  // exclusive prefix of warp k
+      acc = after(acc, t);
+    }
+    wsm[PEXP_THREADS / 32] = acc;
+  }
+  __syncthreads();
+  Aff pre = wsm[w];
+  total = wsm[PEXP_THREADS / 32];
+  return after(pre, exc);
+}
+
+constexpr int EPT = 8;                       // rows per thread per chunk
+constexpr int CHUNK = EPT * PEXP_THREADS;    // 2048 rows
+constexpr int SPAD = EPT + 1;                // smem row padding (bank spread)
+
+// Grid (ncols, E).  Column c of eval e: rhs at rhs + e*rs_e + (cin0+c)*n, result at
+// out + e*os_e + (cout0+c)*n (may alias rhs only if identical).  fidx[e] selects the factor.
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_sai_solve(int n, int periodic, const int* fidx, const double* fl, const double* fdinv,
+            const double* fsup, const double* fz, const double* fw, const double* rhs,
+            long long rs_e, int cin0, double* out, long long os_e, int cout0,
+            const int* active) {
+  const int c = blockIdx.x, e = blockIdx.y;
+  if (active && !active[e]) return;
+  __shared__ double s0[PEXP_THREADS * SPAD];
+  __shared__ double s1[PEXP_THREADS * SPAD];
+  __shared__ Aff wsm[PEXP_THREADS / 32 + 1];
+  __shared__ double red[32];
+  __shared__ double carry_s;
+  const int t = threadIdx.x;
+  const size_t fo = size_t(fidx ? fidx[e] : e) * n;
+  const double *l = fl + fo, *di = fdinv + fo, *cs = fsup + fo;
+  const double* b = rhs + e * rs_e + size_t(cin0 + c) * n;
+  double* x = out + e * os_e + size_t(cout0 + c) * n;
+  const int nchunk = (n + CHUNK - 1) / CHUNK;
+  double carry = 0.0, dot = 0.0;
+  // ---- forward: y_i = b_i - l_i y_{i-1}
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int base = ch * CHUNK;
+    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
+      int g = base + i;
+      int si = (i / EPT) * SPAD + (i % EPT);
+      double bv = g < n ? b[g] : 0.0;
+      s0[si] = bv;
+      s1[si] = g < n ? -l[g] : 1.0;
+      if (periodic && g < n) dot = fma(fw[fo + g], bv, dot);
+    }
+    __syncthreads();
+    Aff m{1.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
+    Aff tot;
+    Aff pre = block_excl_scan<false>(m, t, wsm, tot);
+    double y = fma(pre.A, carry, pre.B);
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      y = fma(s1[t * SPAD + k], y, s0[t * SPAD + k]);
+      s0[t * SPAD + k] = y;
+    }
+    carry = fma(tot.A, carry, tot.B);
+    __syncthreads();
+    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
+      int g = base + i;
+      if (g < n) x[g] = s0[(i / EPT) * SPAD + (i % EPT)];
+    }
+    __syncthreads();
+  }
+  double f = 0.0;
+  if (periodic) f = block_sum(dot, red);
+  // ---- backward: x_i = dinv_i*(y_i - msup_i*x_{i+1}) = (-dinv_i msup_i) x_{i+1} + dinv_i y_i
+  carry = 0.0;
+  const int r = PEXP_THREADS - 1 - t;  // reversed rank: highest rows first
+  for (int ch = nchunk - 1; ch >= 0; --ch) {
+    const int base = ch * CHUNK;
+    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
+      int g = base + i;
+      int si = (i / EPT) * SPAD + (i % EPT);
+      if (g < n) {
+        double dv = di[g];
+        s0[si] = dv * x[g];
+        s1[si] = -dv * cs[g];
+      } else {
+        s0[si] = 0.0;
+        s1[si] = 1.0;
+      }
+    }
+    __syncthreads();
+    Aff m{1.0, 0.0};
+#pragma unroll
+    for (int k = EPT - 1; k >= 0; --k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
+    Aff tot;
+    Aff pre = block_excl_scan<true>(m, r, wsm, tot);
+    double y = fma(pre.A, carry, pre.B);
+#pragma unroll
+    for (int k = EPT - 1; k >= 0; --k) {
+      y = fma(s1[t * SPAD + k], y, s0[t * SPAD + k]);
+      s0[t * SPAD + k] = y;
+    }
+    carry = fma(tot.A, carry, tot.B);
+    __syncthreads();
+    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
+      int g = base + i;
+      if (g < n) {
+        double v = s0[(i / EPT) * SPAD + (i % EPT)];
+        if (periodic) v = fma(-f, fz[fo + g], v);
+        x[g] = v;
+      }
+    }
+    __syncthreads();
+  }
+  (void)carry_s;
+}
+
+// ---------------------------------------------------------------- host wrappers
+void launch_ade_rows(cudaStream_t st, int nops, int n, bool dirichlet, const double* nu,
+                     const double* a, double* sub, double* diag, double* sup) {
+  dim3 grid(std::min(cdiv(n, PEXP_THREADS), 64), nops);
+  k_ade_rows<<<grid, PEXP_THREADS, 0, st>>>(nops, n, dirichlet ? 1 : 0, nu, a, sub, diag, sup);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_burgers_rows(cudaStream_t st, int nops, int n, double nu, const double* ubar,
+                         double* sub, double* diag, double* sup) {
+  dim3 grid(std::min(cdiv(n, PEXP_THREADS), 64), nops);
+  k_burgers_rows<<<grid, PEXP_THREADS, 0, st>>>(nops, n, nu, ubar, sub, diag, sup);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_factor(cudaStream_t st, const Factors& F, int nf, const int* opidx, const double* gam,
+                   const Ops& O, int* err) {
+  ProfScope ps(PC_FACTOR, st, double(nf) * F.n * 8.0 * (3 + 3 + (F.periodic ? 2 : 0)), 0.0);
+  k_factor<<<cdiv(nf, 64), 64, 0, st>>>(nf, F.n, F.periodic, opidx, gam, O.sub, O.diag, O.sup,
+                                         F.l, F.dinv, F.sup, F.z, F.w, err);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E, int ncols,
+                      const double* rhs, long long rs_e, int cin0, double* out, long long os_e,
+                      int cout0, const int* active) {
+  if (E == 0 || ncols == 0) return;
+  // algorithmic: read rhs + write x per column, factors once per distinct factor (<= E)
+  ProfScope ps(PC_SOLVE, st, double(E) * ncols * F.n * 16.0 + double(std::min(E, F.nf)) * F.n * 8.0 * (F.periodic ? 5 : 3),
+               double(E) * ncols * F.n * (F.periodic ? 8.0 : 6.0));
+  dim3 grid(ncols, E);
+  k_sai_solve<<<grid, PEXP_THREADS, 0, st>>>(F.n, F.periodic, fidx, F.l, F.dinv, F.sup, F.z, F.w,
+                                              rhs, rs_e, cin0, out, os_e, cout0, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+}  // namespace pexp

@@ -1,0 +1,212 @@
+// tsmm.cu — tall-skinny fp64 products used by subsystems (2) and (3):
+//   * xty:     T_e = X_e^T Y_e  (X_e: n x nx, Y_e: n x ny column slices of per-eval
+//              column-major panels), split over row chunks; per-chunk partials reduced
+//              deterministically by k_reduce.  Used for the block classical Gram–Schmidt
+//              projections V^T W (BCGS2), block Gram matrices W^T W (CholQR2) and the
+//              source Gram / cross products of the two-pass SVD.
+//   * combine: Out_e = beta*Out_e + alpha * X_e M_e (n x nx times nx x ny), one thread per
+//              row so that Out may alias X (in-place right-multiplication, ny <= 32).
+// Loads are coalesced along rows (each warp reads 32 consecutive rows of a column);
+// per-thread 4x4 register tiles accumulate the small products from shared memory.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pexp {
+
+constexpr int TR = 16;  // rows per shared-memory stage
+constexpr int RA = 4, RB = 4;
+
+template <int NT>
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_xty_partial(int n, int rch, const double* X, long long xs_e, int x0, int nx, const double* Y,
+              long long ys_e, int y0, int ny, double* part, const int* active) {
+  extern __shared__ double sm[];
+  const int e = blockIdx.y, ch = blockIdx.x, nch = gridDim.x;
+  if (active && !active[e]) return;
+  const int nxp = ((nx + RA - 1) / RA) * RA, nyp = ((ny + RB - 1) / RB) * RB;
+  double* Xs = sm;              // [TR][nxp]
+  double* Ys = sm + TR * nxp;   // [TR][nyp]
+  const double* Xe = X + e * xs_e + size_t(x0) * n;
+  const double* Ye = Y + e * ys_e + size_t(y0) * n;
+  const int ntb = nyp / RB, ntiles = (nxp / RA) * ntb;
+  double acc[NT][RA][RB];
+#pragma unroll
+  for (int q = 0; q < NT; ++q)
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+      for (int j = 0; j < RB; ++j) acc[q][i][j] = 0.0;
+  const int r0 = ch * rch, r1 = min(n, r0 + rch);
+  for (int rb = r0; rb < r1; rb += TR) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TR * nxp; idx += PEXP_THREADS) {
+      int a = idx / TR, r = idx % TR, row = rb + r;
+      Xs[r * nxp + a] = (a < nx && row < r1) ? Xe[size_t(a) * n + row] : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < TR * nyp; idx += PEXP_THREADS) {
+      int b = idx / TR, r = idx % TR, row = rb + r;
+      Ys[r * nyp + b] = (b < ny && row < r1) ? Ye[size_t(b) * n + row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      int tile = threadIdx.x + q * PEXP_THREADS;
+      if (tile < ntiles) {
+        int ta = tile / ntb, tb = tile % ntb;
+        for (int r = 0; r < TR; ++r) {
+          double xv[RA], yv[RB];
+#pragma unroll
+          for (int i = 0; i < RA; ++i) xv[i] = Xs[r * nxp + ta * RA + i];
+#pragma unroll
+          for (int j = 0; j < RB; ++j) yv[j] = Ys[r * nyp + tb * RB + j];
+#pragma unroll
+          for (int i = 0; i < RA; ++i)
+#pragma unroll
+            for (int j = 0; j < RB; ++j) acc[q][i][j] = fma(xv[i], yv[j], acc[q][i][j]);
+        }
+      }
+    }
+  }
+  double* P = part + (size_t(e) * nch + ch) * size_t(nx) * ny;
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    int tile = threadIdx.x + q * PEXP_THREADS;
+    if (tile < ntiles) {
+      int ta = tile / ntb, tb = tile % ntb;
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+          int a = ta * RA + i, b = tb * RB + j;
+          if (a < nx && b < ny) P[a + size_t(b) * nx] = acc[q][i][j];
+        }
+    }
+  }
+}
+
+// D_e[row0 + a, col0 + b] (= or +=) sum_ch part[e][ch][a + b*nx]
+__global__ void k_reduce(int nx, int ny, int nch, const double* part, double* D, long long ds_e,
+                         int ldd, int row0, int col0, int accumulate, const int* active) {
+  const int e = blockIdx.y;
+  if (active && !active[e]) return;
+  const size_t sz = size_t(nx) * ny;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nx * ny; idx += gridDim.x * blockDim.x) {
+    const double* p = part + size_t(e) * nch * sz + idx;
+    double s = 0.0;
+    for (int c = 0; c < nch; ++c) s += p[c * sz];
+    int a = idx % nx, b = idx / nx;
+    double* d = D + e * ds_e + (row0 + a) + size_t(col0 + b) * ldd;
+    *d = accumulate ? *d + s : s;
+  }
+}
+
+constexpr int NB = 32;  // max output columns per combine launch
+
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_combine(int n, const double* X, long long xs_e, int x0, int nx, const double* M, long long ms_e,
+          int ldm, double* O, long long os_e, int o0, int ny, double alpha, double beta,
+          const int* active, const int* nxe) {
+  extern __shared__ double Ms[];  // [nx][NB]
+  const int e = blockIdx.y;
+  if (active && !active[e]) return;
+  const double* Me = M + e * ms_e;
+  for (int idx = threadIdx.x; idx < nx * NB; idx += PEXP_THREADS) {
+    int a = idx / NB, b = idx % NB;
+    Ms[idx] = b < ny ? Me[a + size_t(b) * ldm] : 0.0;
+  }
+  __syncthreads();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const double* Xe = X + e * xs_e + size_t(x0) * n + row;
+  const int nxl = nxe ? min(nx, nxe[e]) : nx;
+  double acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = 0.0;
+  for (int a = 0; a < nxl; ++a) {
+    double xv = Xe[size_t(a) * n];
+    const double* mr = Ms + a * NB;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = fma(xv, mr[b], acc[b]);
+  }
+  double* Oe = O + e * os_e + size_t(o0) * n + row;
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+    if (b < ny) {
+      double v = alpha * acc[b];
+      if (beta != 0.0) v = fma(beta, Oe[size_t(b) * n], v);
+      Oe[size_t(b) * n] = v;
+    }
+}
+
+// ---------------------------------------------------------------- host wrappers
+int xty_chunks(int n, int E) {
+  // aim for >= ~4 waves of CTAs over 148 SMs, chunks of >= 512 rows
+  int rch = 512;
+  while (long(cdiv(n, rch)) * E > 148 * 8 && rch < n) rch *= 2;
+  return rch;
+}
+
+void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
+                const double* Y, long long ys_e, int y0, int ny, double* part, size_t part_cap,
+                double* D, long long ds_e, int ldd, int row0, int col0, bool accumulate,
+                const int* active) {
+  if (E == 0 || nx == 0 || ny == 0) return;
+  int rch = xty_chunks(n, E);
+  int nch = cdiv(n, rch);
+  if (size_t(E) * nch * nx * ny > part_cap) fail(2, "xty partial buffer too small");
+  int nxp = cdiv(nx, RA) * RA, nyp = cdiv(ny, RB) * RB;
+  int ntiles = (nxp / RA) * (nyp / RB);
+  size_t smem = size_t(TR) * (nxp + nyp) * sizeof(double);
+  const bool same = (X == Y && xs_e == ys_e && y0 >= x0 && y0 + ny <= x0 + nx);
+  ProfScope ps(PC_XTY, st, double(E) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * E * double(n) * nx * ny);
+  dim3 grid(nch, E);
+  if (ntiles <= PEXP_THREADS) {
+    k_xty_partial<1><<<grid, PEXP_THREADS, smem, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+  } else if (ntiles <= 2 * PEXP_THREADS) {
+    k_xty_partial<2><<<grid, PEXP_THREADS, smem, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+  } else if (ntiles <= 4 * PEXP_THREADS) {
+    k_xty_partial<4><<<grid, PEXP_THREADS, smem, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+  } else if (ntiles <= 8 * PEXP_THREADS) {
+    k_xty_partial<8><<<grid, PEXP_THREADS, smem, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+  } else {
+    fail(1, "xty: product too large (nx*ny > 32768)");
+  }
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+  dim3 g2(std::min(cdiv(nx * ny, PEXP_THREADS), 64), E);
+  k_reduce<<<g2, PEXP_THREADS, 0, st>>>(nx, ny, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
+                    const double* M, long long ms_e, int ldm, double* O, long long os_e, int o0,
+                    int ny, double alpha, double beta, const int* active, const int* nxe) {
+  if (E == 0 || ny == 0) return;
+  for (int b0 = 0; b0 < ny; b0 += NB) {
+    int nb = std::min(NB, ny - b0);
+    if (nx == 0) {
+      if (beta == 1.0) continue;
+    }
+    if (ny > NB && O == X && o0 < x0 + nx && x0 < o0 + ny && xs_e == os_e)
+      fail(1, "combine: in-place product with more than 32 output columns");
+    size_t smem = size_t(std::max(nx, 1)) * NB * sizeof(double);
+    ProfScope ps(PC_COMBINE, st, double(E) * n * 8.0 * (nx + nb * (beta != 0.0 ? 2 : 1)), 2.0 * E * double(n) * nx * nb);
+    dim3 grid(cdiv(n, PEXP_THREADS), E);
+    k_combine<<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, M + size_t(b0) * ldm, ms_e, ldm,
+                                                 O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+  }
+}
+
+void tsmm_init() {
+  // allow > 48 KB dynamic shared memory
+  cudaFuncSetAttribute(k_xty_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_partial<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+}  // namespace pexp

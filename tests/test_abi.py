@@ -1,0 +1,88 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/pexp.h
+declares, and its host-only calls validate arguments (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pexp.h")
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1509_04567_b200 import build
+    build.build()
+    from paper_1509_04567_b200 import pexp
+    return pexp
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"PEXP_API\s+[\w\s\*]+?\b(pexp_\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("pexp_create", "pexp_solve_linear", "pexp_solve_burgers", "pexp_destroy"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(P):
+    lib = C.CDLL(P.LIB_PATH)
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert sorted(P.EXPORTED) == declared_symbols()
+
+
+def test_no_oracle_or_cpu_fallback_in_product(root):
+    """The product package never imports the oracle, and the binding has no fallback path."""
+    pkg = os.path.join(root, "paper_1509_04567_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "numpy.linalg" not in txt and "scipy" not in txt, f
+
+
+def test_create_validation(P):
+    with pytest.raises(P.PexpError):
+        P.Context(2, "periodic", 1e-2, 1.0)              # n < 3
+    with pytest.raises(P.PexpError):
+        P.Context(64, "periodic", -1.0, 1.0)             # nu < 0
+    with pytest.raises(P.PexpError):
+        P.Context(64, "periodic", 1e-2, 1.0, s=3)         # s < 4 (not-a-knot minimum)
+    with pytest.raises(P.PexpError):
+        P.Context(64, "periodic", 1e-2, 1.0, s=65)        # s > 64
+    c = P.Context(64, "dirichlet", [1e-2, 1e-3], [1.0, 0.5])
+    assert c.batch == 2
+
+
+def test_sample_times_match_synth_convention(P):
+    c = P.Context(50, "periodic", 1e-2, 1.0, s=7)
+    t = c.sample_times(0.9, 5).numpy()
+    np.testing.assert_array_equal(t, synth.node_times(0.9, 5, 7))
+
+
+def test_workspace_query_and_solve_without_workspace(P):
+    c = P.Context(128, "periodic", 1e-2, 1.0, s=8)
+    assert c.workspace_bytes(4, 0) > 0
+    assert c.workspace_bytes(4, 1) > 0
+    assert c.workspace_bytes(4, 2) == max(c.workspace_bytes(4, 0), c.workspace_bytes(4, 1))
+    assert c.workspace_bytes(0, 0) == 0
+    d = P.Context(128, "dirichlet", 1e-2, 1.0, s=8)
+    assert d.workspace_bytes(4, 1) == 256          # Burgers plan: none for Dirichlet
+    lib = P._lib
+    # solve calls fail cleanly (ENOMEM: no workspace bound) before touching the device
+    st = lib.pexp_solve_linear(c._h, 1, 1, 1.0, 4, 1e-8, 1, None)
+    assert st == P.PEXP_ENOMEM
+    assert b"workspace" in lib.pexp_last_error(c._h)
+    st = lib.pexp_solve_linear(c._h, 1, 1, 1.0, 4, 1.0, 1, None)   # tol out of range
+    assert st == P.PEXP_EINVAL
+    st = lib.pexp_solve_burgers(d._h, 1, 1e-2, 1.0, 4, 1e-8, 30, 1, None)
+    assert st == P.PEXP_EINVAL and b"periodic" in lib.pexp_last_error(d._h)

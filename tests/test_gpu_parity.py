@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle / library routines on the
+same seeded inputs.  Tolerances: relative 2-norm 1e-8 for solves (BASELINE.json north_star);
+stage tolerances from SURVEY.md §8(c).5 / DESIGN.md §7."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1509_04567_b200 import build  # noqa: E402
+
+build.build()
+from paper_1509_04567_b200 import pexp  # noqa: E402
+import oracle  # noqa: E402
+from oracle.operators import ade_matrix  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def t(x):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device=DEV)
+
+
+# ---------------------------------------------------------------- subsystem 1: SaI solves
+
+@pytest.mark.parametrize("n,bc,nu,a,gamma", [
+    (256, "periodic", 1e-2, 1.0, 1 / 80),
+    (5000, "periodic", 1e-3, 1.0, 1 / 640),      # ragged: 2 full 2048-row chunks + tail
+    (4096, "dirichlet", 1e-3, 1.0, 1 / 640),
+    (1024, "periodic", 1e-4, 2.0, 1 / 160),      # C4 corner: cell Peclet ~20, M not dominant
+    (7, "dirichlet", 0.3, -1.0, 0.5),            # tiny
+])
+def test_sai_solve_vs_dense(n, bc, nu, a, gamma):
+    r = np.random.default_rng(n)
+    c = pexp.Context(n, bc, nu, a)
+    B = r.standard_normal((5, n))
+    X = c.sai_solve(0, gamma, t(B)).cpu().numpy()
+    M = np.eye(n) - gamma * ade_matrix(n, bc, nu, a).toarray()
+    ref = np.linalg.solve(M, B.T).T
+    assert rel(X, ref) < 1e-12
+    assert np.linalg.norm(M @ X.T - B.T) <= 1e-12 * np.linalg.norm(B)
+
+
+# ---------------------------------------------------------------- subsystem 3: source SVD
+
+def _svd_case(G, tol):
+    c = pexp.Context(G.shape[2], "periodic", 1e-2, 1.0, s=G.shape[1])
+    m, sig, proj = c.source_svd(t(G), tol)
+    return m, sig.cpu().numpy(), proj.cpu().numpy()
+
+
+def test_source_svd_config1_exact_rank():
+    p = synth.config1()
+    A = ade_matrix(p.n, p.bc, p.nu[0], p.a[0])
+    G = np.stack([(A @ p.u0[0])[None, :] + p.src[0, j] for j in range(p.P)])  # [P][s][n]
+    m, sig, proj = _svd_case(G, p.tol)
+    for j in range(p.P):
+        U, C, sv = oracle.truncated_svd(G[j].T, 0.01 * p.tol)
+        assert m[j] == U.shape[1] == 4
+        assert rel(proj[j].T, U @ C) < 1e-12
+        np.testing.assert_allclose(sig[j][:4], sv[:4], rtol=1e-10)
+
+
+def test_source_svd_noisy_no_gap():
+    """C2-like spectrum: geometric decay, then a 1e-10 noise floor: the two-pass
+    Gram SVD must find the same m as LAPACK and the same projection."""
+    p = synth.config2(n=1500, P=3, s=64)
+    G = p.src[0] + 0.0
+    m, sig, proj = _svd_case(G, p.tol)
+    for j in range(p.P):
+        U, C, sv = oracle.truncated_svd(G[j].T, 0.01 * p.tol)
+        assert m[j] == U.shape[1]
+        assert np.linalg.norm(proj[j].T - U @ C) <= 1e-12 * sv[0]
+
+
+def test_source_svd_zero_and_rank_one():
+    n, s = 300, 9
+    G = np.zeros((2, s, n))
+    G[1] = np.outer(np.linspace(1, 2, s), np.sin(np.arange(n)))
+    m, sig, proj = _svd_case(G, 1e-8)
+    assert m == [0, 1]
+    assert np.abs(proj[0]).max() == 0.0
+    assert rel(proj[1], G[1]) < 1e-13
+
+
+# ---------------------------------------------------------------- subsystem 4: batched expm
+
+def test_expm_batched_vs_scipy():
+    from scipy.linalg import expm
+    r = np.random.default_rng(0)
+    mats = [r.standard_normal((40, 40)) * s for s in (0.01, 1.0, 8.0)]
+    mats.append(np.diag(-np.linspace(0, 300, 40)) + np.triu(r.standard_normal((40, 40)), 1))
+    A = np.stack(mats)
+    c = pexp.Context(16, "periodic", 1e-2, 1.0)
+    X = c.expm_batched(t(A)).cpu().numpy()
+    for k in range(len(mats)):
+        ref = expm(A[k])
+        assert rel(X[k], ref) < 1e-12, k
+
+
+# ---------------------------------------------------------------- linear Paraexp-EBK solves
+
+def _linear(p, k_max=256, **kw):
+    c = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=p.s, k_max=k_max)
+    out, st = c.solve_linear(t(p.u0), t(p.src), p.T, p.P, p.tol)
+    return out.cpu().numpy(), st
+
+
+def _oracle_linear(p, **kw):
+    return oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol, **kw)
+
+
+def test_linear_config1_full():
+    p = synth.config1()
+    out, st = _linear(p)
+    ref = _oracle_linear(p)
+    assert rel(out, ref) < 1e-8, st
+    assert st["max_m"] == 4
+
+
+@pytest.mark.parametrize("bc,n,nu,a", [("periodic", 777, 5e-3, 1.3), ("dirichlet", 600, 1e-3, 1.0)])
+def test_linear_generic_deep_arnoldi(bc, n, nu, a):
+    """Non-Fourier data: the Krylov space is not invariant; deep Arnoldi, ragged n."""
+    p = synth.generic_linear(n=n, bc=bc, nu=nu, a=a, P=5, s=12, T=0.5, seed=7)
+    out, st = _linear(p)
+    ref = _oracle_linear(p)
+    assert rel(out, ref) < 1e-8, st
+    assert st["max_k"] > 20
+
+
+def test_linear_config2_reduced():
+    p = synth.config2(n=1200, P=16, T=0.25, s=64)     # same subinterval length dT = 1/64 as C2
+    out, st = _linear(p)
+    ref = _oracle_linear(p)
+    assert rel(out, ref) < 1e-8, st
+
+
+def test_linear_config4_subset():
+    p = synth.config4(indices=[0, 1, 511], P=4, s=16)
+    out, st = _linear(p, k_max=128)
+    ref = _oracle_linear(p)
+    for b in range(p.batch):
+        assert rel(out[b], ref[b]) < 1e-8, (b, st)
+
+
+def test_linear_P1_and_unforced_and_zero():
+    n = 300
+    x = synth.grid_x(n, "periodic")
+    u0 = np.exp(-((x - 0.5) / 0.08) ** 2)[None]
+    src = np.zeros((1, 1, 6, n))
+    c = pexp.Context(n, "periodic", 1e-2, 1.0, s=6)
+    out, _ = c.solve_linear(t(u0), t(src), 1.0, 1, 1e-8)
+    ref = oracle.solve_linear(n, "periodic", [1e-2], [1.0], u0, src, 1.0, 1, 6, 1e-8)
+    assert rel(out.cpu().numpy(), ref) < 1e-8
+    z, _ = c.solve_linear(t(np.zeros((1, n))), t(np.zeros((1, 3, 6, n))), 1.0, 3, 1e-8)
+    assert torch.count_nonzero(z).item() == 0
+
+
+def test_linear_config2_full_size_sampled():
+    """C2 at its full size in the bench's launch configuration; the oracle computes the first
+    two outputs u(T_1), u(T_2) (which depend only on subintervals 1-2)."""
+    p = synth.config2()
+    out, st = _linear(p, k_max=384)
+    ref = _oracle_linear(p, i_max=2)
+    assert rel(out[0, :2], ref[0]) < 1e-8, st
+    assert np.all(np.isfinite(out))
+
+
+# ---------------------------------------------------------------- Burgers WR
+
+def _burgers(p, k_max=256):
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=k_max)
+    out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters)
+    return out.cpu().numpy(), st
+
+
+def test_burgers_small():
+    p = synth.config3(n=256, P=4, s=12, T=0.2, nu=0.02)
+    out, st = _burgers(p)
+    ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
+    assert st["wr_iters"] == info["iters"], (st, info["delta"])
+    assert rel(out, ref) < 1e-8, st
+    assert abs(out.sum(axis=1) - p.u0.sum()).max() < 1e-9 * np.abs(p.u0).sum()
+
+
+def test_burgers_config3_full():
+    p = synth.config3()
+    out, st = _burgers(p)
+    ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
+    assert st["wr_iters"] == info["iters"], (st, info["delta"])
+    assert rel(out, ref) < 1e-8, st
