@@ -65,7 +65,7 @@ typedef struct {
   int32_t s;              /* source samples per subinterval, >= 4 (default 32)           */
   int32_t node_rule;      /* 0 = uniform incl. endpoints (only value supported)         */
   double svd_tau_factor;  /* truncation tau_svd = factor*tol relative to sigma_1 (0.01)  */
-  double stop_factor;     /* Krylov stop eta = factor*tol (default 0.01)                 */
+  double stop_factor;     /* Krylov stop eta = factor*tol (default 0.1; DESIGN.md §3 #6)  */
   int32_t restart_blocks; /* paper restarts every 20 blocks    */
   int32_t k_max;          /* Krylov column capacity per evaluation (default 256)         */
   void* stream;           /* cudaStream_t; NULL = legacy default stream                  */

@@ -65,6 +65,7 @@ void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E,
 
 // tsmm.cu
 int xty_chunks(int n, int E);
+void xty_tall_plan(int n, int E, int nx, int ny, int& rsub, int& rch, int& nch);
 void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
                 const double* Y, long long ys_e, int y0, int ny, double* part, size_t part_cap, double* D,
                 long long ds_e, int ldd, int row0, int col0, bool accumulate, const int* active);
@@ -79,7 +80,10 @@ void launch_sym_eig_select(cudaStream_t st, int E, int s, const double* G, doubl
 void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long gs_e, int ldg,
                        const double* norm0, long long ns_e, int ldn, double defl, double* Rinv, const double* Rprev,
                        long long rps_e, int ldrp, double* Rout, long long rs_e, int ldr, int* live,
-                       long long ls_e, const int* active);
+                       long long ls_e, const int* active, bool pivoted, double dtol = 0.0,
+                       double* norm0_out = nullptr);
+void launch_defer_corr(cudaStream_t st, int E, int N, const double* Gb, long long gs_e, const int* cls, long long cs_e,
+                       double* Mc, const int* active);
 void launch_onesided_svd(cudaStream_t st, int E, int s, const double* C, const int* kk, double tau, double* Qs,
                          double* sig, double* Cs, int* m_out, const int* active);
 void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, const double* Qs,

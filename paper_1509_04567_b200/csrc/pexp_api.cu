@@ -67,7 +67,7 @@ static Opts norm_opts(const pexp_options& o) {
   Opts r;
   r.s = o.s > 0 ? o.s : 32;
   r.tau_f = o.svd_tau_factor > 0 ? o.svd_tau_factor : 0.01;
-  r.eta_f = o.stop_factor > 0 ? o.stop_factor : 0.01;
+  r.eta_f = o.stop_factor > 0 ? o.stop_factor : 0.1;
   r.restart_blocks = o.restart_blocks > 0 ? o.restart_blocks : 20;
   r.kcap = o.k_max > 0 ? o.k_max : 256;
   r.st = (cudaStream_t)o.stream;
@@ -79,7 +79,7 @@ static Opts norm_opts(const pexp_options& o) {
 struct EbkBufs {
   int E = 0, n = 0, kcap = 0, mcap = 0, nout = 0, s = 0;
   long long vs_e = 0, hs_e = 0, zs_e = 0;
-  double *V, *H, *Z, *Gt, *Wt, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef;
+  double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p;
   int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx;
   double* part;
   size_t part_cap;
@@ -100,6 +100,8 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, i
   B.Z = ar.take<double>(size_t(E) * nout * kcap);
   B.Gt = ar.take<double>(size_t(E) * mcap * mcap);
   B.Wt = Wt_shared ? Wt_shared : ar.take<double>(size_t(E) * mcap * n);
+  B.Wt2 = ar.take<double>(size_t(E) * mcap * n);
+  B.n0p = ar.take<double>(size_t(E) * mcap);
   B.T = ar.take<double>(size_t(E) * kcap * mcap);
   B.G0 = ar.take<double>(size_t(E) * mcap * mcap);
   B.G1 = ar.take<double>(size_t(E) * mcap * mcap);
@@ -122,6 +124,10 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, i
   size_t ech = std::max<size_t>(size_t(E) * cdiv(n, xty_chunks(n, E)), 2 * 148 * 8 + size_t(E));
   ech = std::min<size_t>(ech, size_t(E) * cdiv(n, 512));
   B.part_cap = ech * std::max(kcap, s) * (forced ? std::max(mcap, s) : mcap);
+  // tall path (ny <= 32): E' * nch(E') <= E' + 2*148*6 chunks for any E' <= E
+  const int nyt = std::min(forced ? std::max(mcap, s) : mcap, 32);
+  size_t tall = (size_t(E) + 2 * 148 * 6) * size_t(std::max(kcap, s)) * nyt;
+  B.part_cap = std::max(B.part_cap, tall);
   B.part = ar.take<double>(B.part_cap);
   B.nslots = std::min(E, 512);
   B.Nmax = kcap + (forced ? 4 * mcap : 0);
@@ -155,7 +161,9 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   PEXP_LAUNCH_CHECK();
   int steps = 0, last_check = -1;
   int next_check = std::max(4, 2 * m);
-  const double defl = 1e-12;
+  // deflation: a new column is dropped when BCGS leaves < 1e-10 of ||(I - gamma A)^{-1} v|| (well
+  // above the shift-and-invert solve rounding (~1e-13..1e-12), below the 1e-8 parity bar)
+  static const double defl = getenv("PEXP_DEFL") ? atof(getenv("PEXP_DEFL")) : 1e-10;  // developer override
   SPArgs a{};
   a.E = E; a.kcap = kcap; a.m = m; a.kind = kind;
   a.H = B.H; a.hs_e = B.hs_e; a.ldh = kcap;
@@ -172,6 +180,11 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   a.work = B.work; a.work_slot = B.work_slot; a.iwork = B.iwork; a.iwork_slot = B.iwork_slot; a.Nmax = B.Nmax;
   a.stop_rule = stop_rule;
   int remaining = E;
+  std::vector<double> prevq(E, -1.0), curq(E, -1.0);
+  std::vector<int> prevK(E, -1);
+  std::vector<double> hres(E), hcrit(E);
+  std::vector<int> hact(E);
+  int predicted_next = -1;
   auto do_check = [&](int K) {
     if (stop_rule == 1) {  // true residual: tail Gram of Wt = (I - gamma A) V[:, K:K+m]
       launch_apply_M(st, O, B.opidx, B.gam, E, m, B.V, B.vs_e, K, B.Wt, (long long)m * n, 0, periodic, B.active);
@@ -189,6 +202,51 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     remaining = h_count;
     last_check = K;
     info.max_k = std::max(info.max_k, K);
+    // predict the K at which the still-active evaluations converge: the residual ratio
+    // q = res/crit decays roughly geometrically in K; extrapolate from the last two checks
+    predicted_next = -1;
+    if (remaining > 0) {
+      PEXP_CUDA_TRY(cudaMemcpyAsync(hres.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
+      PEXP_CUDA_TRY(cudaMemcpyAsync(hcrit.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
+      PEXP_CUDA_TRY(cudaMemcpyAsync(hact.data(), B.active, E * sizeof(int), cudaMemcpyDeviceToHost, st));
+      PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+      std::vector<double> preds;
+      for (int e = 0; e < E; ++e) {
+        if (!hact[e] || !(hcrit[e] > 0)) continue;
+        double q = hres[e] / hcrit[e];
+        if (prevK[e] >= 0 && prevq[e] > 0 && q > 0 && q < prevq[e]) {
+          double slope = (std::log(q) - std::log(prevq[e])) / double(K - prevK[e]);
+          preds.push_back(K + std::log(0.5 / q) / slope);
+        }
+        prevq[e] = q;
+        prevK[e] = K;
+      }
+      if (!preds.empty()) {
+        std::sort(preds.begin(), preds.end());
+        double p80 = preds[std::min(preds.size() - 1, size_t(0.8 * preds.size()))];
+        predicted_next = (int)std::ceil(p80);
+      }
+    }
+    static const char* dump = getenv("PEXP_DUMP");
+    if (dump && E == 1) {  // developer dump of the Arnoldi state of a single evaluation
+      std::vector<double> hv(size_t(kcap) * n), hh(size_t(kcap) * kcap), hz(size_t(B.nout) * kcap);
+      std::vector<int> hl(kcap);
+      cudaMemcpy(hv.data(), B.V, hv.size() * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(hh.data(), B.H, hh.size() * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(hz.data(), B.Z, hz.size() * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(hl.data(), B.live, hl.size() * 4, cudaMemcpyDeviceToHost);
+      std::string base = std::string(dump) + "_K" + std::to_string(K);
+      FILE* fp = fopen((base + ".bin").c_str(), "wb");
+      if (fp) {
+        int hdr[5] = {n, kcap, K, m, B.nout};
+        fwrite(hdr, 4, 5, fp);
+        fwrite(hl.data(), 4, hl.size(), fp);
+        fwrite(hv.data(), 8, hv.size(), fp);
+        fwrite(hh.data(), 8, hh.size(), fp);
+        fwrite(hz.data(), 8, hz.size(), fp);
+        fclose(fp);
+      }
+    }
     static const bool dbg = getenv("PEXP_DEBUG") != nullptr;
     if (dbg) {  // developer trace: residual/target distribution at this check
       std::vector<double> r(E), c(E);
@@ -227,52 +285,68 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     const long long ws_e = B.vs_e;
     // W = (I - gamma A)^{-1} V_b  -> columns [nv, nv+m)
     launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
-    // W^T W before orthogonalisation (deflation reference)
+    // keep the raw image W0 = (I - gamma A)^{-1} V_b: the subdiagonal block of H is computed
+    // directly as Q^T W0 at the end (exact to eps, independent of the in-block QR route)
+    PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.Wt, size_t(m) * n * sizeof(double), B.V + size_t(nv) * n,
+                                    ws_e * sizeof(double), size_t(m) * n * sizeof(double), E,
+                                    cudaMemcpyDeviceToDevice, st));
+    // norms of W0 (deflation reference)
     launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G0, (long long)m * m, m, 0, 0,
                false, B.active);
-    // BCGS2 with intra-block Cholesky-QR in each pass (pass 2 restores orthogonality of
-    // nearly deflated columns):  W = V H1 + Q1 R1,  Q1 = V H2 + Q2 R2
-    //   => H[:, block b] = H1 + H2 R1,  H[nv:nv+m, block b] = R2 R1.
-    // pass 1: H1 -> H ; W -= V H1 ; [Q1, R1] = deflating CholQR(W)  (R1 -> Rtmp)
+    // BCGS pass 1: H[0:nv, block b] = V^T W0 ; W = W0 - V H
     launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.H, B.hs_e, kcap, 0, b * m,
                false, B.active);
     launch_combine(st, E, n, B.V, ws_e, 0, nv, B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.V, ws_e, nv, m, -1.0, 1.0,
                    B.active);
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {
-        // pass 2: T = V^T Q1 ; W -= V T ; H[:, block b] += T R1
-        launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.T, (long long)kcap * B.mcap,
-                   nv, 0, 0, false, B.active);
-        launch_combine(st, E, n, B.V, ws_e, 0, nv, B.T, (long long)kcap * B.mcap, nv, B.V, ws_e, nv, m, -1.0, 1.0,
-                       B.active);
-        launch_hupdate(st, E, nv, m, B.T, (long long)kcap * B.mcap, nv, B.Rtmp, (long long)m * m, m,
-                       B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.active);
-      }
+    // in-block QR, stage A: pivoted CholQR accepting only well-separated columns (scaled pivot
+    // > 1e-8, i.e. kappa <= 1e4); nearly dependent columns are DEFERRED (passed through raw,
+    // class 2), columns below defl * |W0| are dead.  norm0 is re-ordered to the new positions.
+    auto chol_combine = [&](const double* n0, long long n0s, int n0ld, double dtol, double* n0out) {
       launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0,
                  false, B.active);
-      if (pass == 0) {
-        launch_block_chol(st, E, m, B.G1, (long long)m * m, m, B.G0, (long long)m * m, m, defl, B.Rinv, nullptr, 0,
-                          0, B.Rtmp, (long long)m * m, m, B.live + nv, kcap, B.active);
-      } else {
-        launch_block_chol(st, E, m, B.G1, (long long)m * m, m, nullptr, 0, 0, defl, B.Rinv, B.Rtmp,
-                          (long long)m * m, m, B.H + size_t(nv) + size_t(b) * m * kcap, B.hs_e, kcap, B.live + nv,
-                          kcap, B.active);
-      }
+      launch_block_chol(st, E, m, B.G1, (long long)m * m, m, n0, n0s, n0ld, defl, B.Rinv, nullptr, 0, 0, nullptr, 0,
+                        0, B.live + nv, kcap, B.active, true, dtol, n0out);
       if (m <= 32) {
         launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.V, ws_e, nv, m, 1.0, 0.0,
                        B.active);
       } else {
-        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.Wt, (long long)m * n, 0, m, 1.0,
+        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.Wt2, (long long)m * n, 0, m, 1.0,
                        0.0, B.active);
-        PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.V + size_t(nv) * n, ws_e * sizeof(double), B.Wt, size_t(m) * n * sizeof(double),
-                                        size_t(m) * n * sizeof(double), E, cudaMemcpyDeviceToDevice, st));
+        PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.V + size_t(nv) * n, ws_e * sizeof(double), B.Wt2,
+                                        size_t(m) * n * sizeof(double), size_t(m) * n * sizeof(double), E,
+                                        cudaMemcpyDeviceToDevice, st));
       }
+    };
+    chol_combine(B.G0, (long long)m * m, m, 1e-8, B.n0p);
+    // stage B: explicit CGS2 of the deferred columns against the accepted ones
+    for (int rep = 0; rep < 2; ++rep) {
+      launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0,
+                 false, B.active);
+      launch_defer_corr(st, E, m, B.G1, (long long)m * m, B.live + nv, kcap, B.Rinv, B.active);
+      if (m <= 32)
+        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.V, ws_e, nv, m, 1.0, 1.0, B.active);
+      else
+        fail(1, "block width > 32 with deferred columns not supported");
     }
+    // stage C: final pivoted CholQR of the whole block (accepted columns are orthonormal, deferred
+    // remainders are orthogonal to them), deflating remainders below defl * |W0|
+    chol_combine(B.n0p, m, 0, 0.0, nullptr);
+    // BCGS pass 2 (re-orthogonalisation against V) + CholQR of the nearly orthonormal block
+    launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.T, (long long)kcap * B.mcap, nv,
+               0, 0, false, B.active);
+    launch_combine(st, E, n, B.V, ws_e, 0, nv, B.T, (long long)kcap * B.mcap, nv, B.V, ws_e, nv, m, -1.0, 1.0,
+                   B.active);
+    chol_combine(nullptr, 0, 0, 0.0, nullptr);
+    // subdiagonal block: H[nv:nv+m, block b] = Q^T W0
+    launch_xty(st, E, n, B.V, ws_e, nv, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.H, B.hs_e, kcap, nv,
+               b * m, false, B.active);
     ++steps;
     const int K = steps * m;
     if (K >= next_check || (steps + 2) * m > kcap) {
       do_check(K);
-      next_check = std::max(K + m, (int)std::ceil(K * 1.25));
+      int geo = std::max(K + m, (int)std::ceil(K * 1.25));
+      next_check = geo;
+      if (predicted_next > 0) next_check = std::max(K + m, std::min(predicted_next, 2 * K));
     }
   }
   info.unconverged = remaining;
@@ -368,7 +442,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
       launch_xty(st, E, n, U, gs_e, 0, s, U, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false,
                  nullptr);
       launch_block_chol(st, E, s, S.Gs, (long long)s * s, s, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0, 0,
-                        nullptr, 0, nullptr);
+                        nullptr, 0, nullptr, false);
       launch_combine(st, E, n, U, gs_e, 0, s, S.Rinv, (long long)s * s, s, Fr, gs_e, 0, s, 1.0, 0.0, nullptr);
       std::swap(U, Fr);
     }
@@ -392,7 +466,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
     launch_xty(st, E, n, B->V, B->vs_e, 0, mb, B->V, B->vs_e, 0, mb, part, part_cap, S.Gs, (long long)mb * mb, mb, 0, 0,
                false, nullptr);
     launch_block_chol(st, E, mb, S.Gs, (long long)mb * mb, mb, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0,
-                      0, nullptr, 0, nullptr);
+                      0, nullptr, 0, nullptr, false);
     if (mb <= 32) {
       launch_combine(st, E, n, B->V, B->vs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, B->V, B->vs_e, 0, mb, 1.0, 0.0,
                      nullptr);
@@ -677,8 +751,9 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
       k_hom_start<<<Eh, PEXP_THREADS, 0, st>>>(P, n, L.Yend, n, L.Bh.beta, L.Bh.V, L.Bh.vs_e);
       count_launch();
       PEXP_LAUNCH_CHECK();
-      launch_hom_setup(st, Eh, 0, P, s, h, eta, L.Bh.beta, L.Bh.crit, L.Bh.npieces, L.Bh.active);
-      rh = ebk_run(st, L.Bh, L.F, L.O, periodic, 1, 1, h, 0, s - 1, P, o.stop_rule);
+      // legs are only needed at T_{j+1+q}: integrate the projected problem with step dT
+      launch_hom_setup(st, Eh, 0, P, 2, dT, eta, L.Bh.beta, L.Bh.crit, L.Bh.npieces, L.Bh.active);
+      rh = ebk_run(st, L.Bh, L.F, L.O, periodic, 1, 1, dT, 0, 1, P, o.stop_rule);
       launch_combine(st, Eh, n, L.Bh.V, L.Bh.vs_e, 0, std::max(rh.max_k, 1), L.Bh.Z, L.Bh.zs_e, L.Bh.kcap, L.Yh,
                      (long long)P * n, 0, P, 1.0, 0.0, nullptr, L.Bh.kfin);
     }

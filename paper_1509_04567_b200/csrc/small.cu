@@ -11,6 +11,7 @@
 //   * k_small_problem   : projected SaI problem: H^{-1}, A_hat = (I - H^{-1})/gamma, Pade-13
 //                         exponential of the augmented matrix, exact chaining over the cubic
 //                         pieces, residual norms at every node (subsystem 4)
+#include <cstdlib>
 #include "common.cuh"
 #include "dense.cuh"
 #include "kernels.cuh"
@@ -18,6 +19,7 @@
 namespace pexp {
 
 constexpr int MAXS = 64;
+double g_piv_tol = getenv("PEXP_PIVTOL") ? atof(getenv("PEXP_PIVTOL")) : 1e-14;  // developer override
 constexpr size_t SM2 = 2 * MAXS * (MAXS + 1) * sizeof(double);  // two padded 64x64 tiles
 
 __device__ inline void jacobi_pair(int Ne, int r, int k, int& p, int& q) {
@@ -142,87 +144,133 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
 }
 
 // ---------------------------------------------------------------- deflating Cholesky-QR
-// G: [E] N x N Gram (ld ldg, stride gs_e).  norm0 (nullable): squared norms of the columns
-// before orthogonalisation against the previous basis; a column is deflated (dead) when
-// G_kk <= defl^2 * norm0_k, when G_kk == 0, or when its scaled Cholesky pivot is <= 1e-14
-// (it lies within 1e-7 of the span of the earlier columns of the block).
-// Outputs Rinv (N x N, ld N, stride N*N): Q = W Rinv has orthonormal live columns and zero
-// dead columns; R (= R_this * Rprev if Rprev) written to Rout (ld ldr, stride rs_e);
-// live flags to live (stride ls_e).
+// G: [E] N x N Gram (ld ldg, stride gs_e).  norm0 (nullable, diagonal read with ld ldn):
+// squared norms of the columns before orthogonalisation against the previous basis; a column
+// is deflated (dead) when G_kk <= defl^2 * norm0_k or G_kk == 0.
+// PIVOTED Cholesky of the diagonally scaled Gram matrix: at each step the remaining column
+// with the largest Schur-complement pivot is eliminated; elimination stops when the largest
+// remaining scaled pivot is <= 1e-14 (those columns lie within 1e-7 of the span already
+// built).  Tiny-but-accepted pivots are therefore processed last and cannot corrupt larger
+// ones (the failure mode of unpivoted CholQR on nearly dependent Krylov blocks).
+// With perm the pivot order, W[:, perm] = Q Rp (Rp upper triangular).  Outputs:
+//   Rinv (N x N, ld N, stride N*N):  Q = W Rinv  (live new columns first, dead columns 0)
+//   Rout (= R, or R * Rprev):  W = Q R with R[t][perm[a]] = Rp[t][a]  (column-permuted)
+//   live flags: new column t is live iff t < number of accepted pivots.
 __global__ void __launch_bounds__(PEXP_THREADS)
 k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm0, long long ns_e,
              int ldn, double defl, double* Rinv, const double* Rprev, long long rps_e, int ldrp, double* Rout,
-             long long rs_e, int ldr, int* live, long long ls_e, const int* active) {
+             long long rs_e, int ldr, int* live, long long ls_e, const int* active, int pivoted, double piv_tol,
+             double dtol, double* norm0_out) {
   const int e = blockIdx.x;
   if (active && !active[e]) return;
   extern __shared__ double dsm[];
-  double (*L)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm);
-  double (*X)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm + MAXS * (MAXS + 1));
+  double (*S)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm);                       // scaled Gram / Schur
+  double (*X)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm + MAXS * (MAXS + 1));   // work
   __shared__ double d[MAXS];
-  __shared__ int dead[MAXS];
+  __shared__ double Lp[MAXS][MAXS + 1];  // Lp[a][t]: permuted lower factor (position a, pivot t)
+  __shared__ int dead[MAXS], perm[MAXS], used[MAXS];
+  __shared__ int s_np, s_j;
+  __shared__ double s_piv;
   const double* Ge = G + e * gs_e;
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     double g = Ge[k + size_t(k) * ldg];
     bool dk = !(g > 0.0);
     if (norm0 && !(g > defl * defl * norm0[e * ns_e + k + size_t(k) * ldn])) dk = true;
     dead[k] = dk;
+    used[k] = 0;
     d[k] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
     int i = idx % N, j = idx / N;
-    L[i][j] = d[i] * d[j] * 0.5 * (Ge[i + size_t(j) * ldg] + Ge[j + size_t(i) * ldg]);
+    S[i][j] = d[i] * d[j] * 0.5 * (Ge[i + size_t(j) * ldg] + Ge[j + size_t(i) * ldg]);
+    Lp[i][j] = 0.0;
+  }
+  if (threadIdx.x == 0) s_np = 0;
+  __syncthreads();
+  for (int t = 0; t < N; ++t) {
+    if (threadIdx.x == 0) {
+      int jb = -1;
+      double best = dtol > 0.0 ? dtol : piv_tol;
+      if (pivoted) {
+        for (int j = 0; j < N; ++j)
+          if (!used[j] && !dead[j] && S[j][j] > best) { best = S[j][j]; jb = j; }
+      } else {  // natural order (keeps the column order of an already well-conditioned block)
+        for (int j = 0; j < N && jb < 0; ++j) {
+          if (used[j] || dead[j]) continue;
+          if (S[j][j] > best) { best = S[j][j]; jb = j; } else dead[j] = 1;
+        }
+      }
+      s_j = jb;
+      if (jb >= 0) {
+        used[jb] = 1;
+        perm[t] = jb;
+        s_piv = sqrt(best);
+        s_np = t + 1;
+      }
+    }
+    __syncthreads();
+    const int jb = s_j;
+    if (jb < 0) break;
+    const double pv = s_piv;
+    // column of the factor for pivot t: l_i = S[i][jb] / pv for every not-yet-used column i
+    for (int i = threadIdx.x; i < N; i += blockDim.x) X[i][0] = (i == jb) ? pv : (used[i] ? 0.0 : S[i][jb] / pv);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+      int i = idx % N, k = idx / N;
+      if (!used[i] && !used[k]) S[i][k] -= X[i][0] * X[k][0];
+    }
+    // record l for every column (by original index) in slot t
+    for (int i = threadIdx.x; i < N; i += blockDim.x) Lp[i][t] = X[i][0];
+    __syncthreads();
+  }
+  const int np = s_np;
+  // order: positions 0..np-1 = pivots, then the remaining columns in original order
+  // (deferred mode: non-dead remaining columns are passed through raw at positions np..np+nd-1)
+  __shared__ int s_nd;
+  if (threadIdx.x == 0) {
+    int q = np, nd = 0;
+    if (dtol > 0.0)
+      for (int j = 0; j < N; ++j)
+        if (!used[j] && !dead[j]) { perm[q++] = j; ++nd; }
+    for (int j = 0; j < N; ++j)
+      if (!used[j] && (dtol <= 0.0 || dead[j])) perm[q++] = j;
+    s_nd = nd;
   }
   __syncthreads();
-  __shared__ double s_piv;
-  for (int k = 0; k < N; ++k) {
-    if (threadIdx.x == 0) {
-      double p = L[k][k];
-      if (dead[k] || !(p > 1e-14)) {
-        dead[k] = 1;
-        s_piv = 0.0;
-      } else {
-        s_piv = sqrt(p);
-      }
-    }
-    __syncthreads();
-    const double pv = s_piv;
-    for (int i = k + threadIdx.x; i < N; i += blockDim.x) L[i][k] = (pv > 0.0) ? (i == k ? pv : L[i][k] / pv) : 0.0;
-    __syncthreads();
-    if (pv > 0.0) {
-      const int h = N - k - 1;
-      for (int idx = threadIdx.x; idx < h * h; idx += blockDim.x) {
-        int i = k + 1 + idx % h, j = k + 1 + idx / h;
-        if (j <= i) L[i][j] -= L[i][k] * L[j][k];
-      }
-    }
-    __syncthreads();
-  }
-  // Rs = L^T (upper): Rs[k][j] = L[j][k] for j >= k.  X = Rs^{-1} on live rows/cols.
+  const int nd = s_nd;
+  // Rp[t][a] (upper, t <= a, t < np) = Lp[perm[a]][t];  X = Rp^{-1} on the leading np x np block
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     for (int k = 0; k < N; ++k) X[k][j] = 0.0;
-    if (!dead[j]) {
+    if (j < np) {
       for (int k = j; k >= 0; --k) {
-        if (dead[k]) continue;
         double sum = (k == j) ? 1.0 : 0.0;
-        for (int p = k + 1; p <= j; ++p) sum -= L[p][k] * X[p][j];
-        X[k][j] = sum / L[k][k];
+        for (int q = k + 1; q <= j; ++q) sum -= Lp[perm[q]][k] * X[q][j];
+        X[k][j] = sum / Lp[perm[k]][k];
       }
     }
   }
   __syncthreads();
+  // Rinv[perm[a]][t] = d[perm[a]] * X[a][t]  (Q_t = sum_a W[:, perm[a]] Rinv[perm[a]][t])
   double* Ri = Rinv + size_t(e) * N * N;
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
-    int k = idx % N, j = idx / N;
-    Ri[idx] = d[k] * X[k][j];
-  }
-  if (live)
-    for (int k = threadIdx.x; k < N; k += blockDim.x) live[e * ls_e + k] = dead[k] ? 0 : 1;
-  // R = Rs D^{-1}: R[k][j] = L[j][k] / d[j]  (j >= k), 0 if d[j] == 0
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) Ri[idx] = 0.0;
   __syncthreads();
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
-    int k = idx % N, j = idx / N;
-    X[k][j] = (j >= k && d[j] > 0.0) ? L[j][k] / d[j] : 0.0;
+    int a = idx % N, t = idx / N;
+    Ri[perm[a] + size_t(t) * N] = d[perm[a]] * X[a][t];
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nd; q += blockDim.x) Ri[perm[np + q] + size_t(np + q) * N] = 1.0;  // raw copy
+  if (live)
+    for (int k = threadIdx.x; k < N; k += blockDim.x) live[e * ls_e + k] = k < np ? 1 : (k < np + nd ? 2 : 0);
+  if (norm0_out && norm0)
+    for (int k = threadIdx.x; k < N; k += blockDim.x)
+      norm0_out[e * N + k] = norm0[e * ns_e + perm[k] + size_t(perm[k]) * ldn];
+  __syncthreads();
+  // R[t][c] = Lp[c][t] / d[c] for t < np (W[:, c] = sum_t Q_t R[t][c]); 0 if d[c] == 0
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int t = idx % N, c = idx / N;
+    X[t][c] = (t < np && d[c] > 0.0) ? Lp[c][t] / d[c] : 0.0;
   }
   __syncthreads();
   if (Rout) {
@@ -233,13 +281,36 @@ k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm
       if (Rprev) {
         const double* Rp = Rprev + e * rps_e;
         v = 0.0;
-        for (int p = k; p <= j; ++p) v += X[k][p] * Rp[p + size_t(j) * ldrp];
+        for (int p = 0; p < N; ++p) v += X[k][p] * Rp[p + size_t(j) * ldrp];
       } else {
         v = X[k][j];
       }
       Ro[k + size_t(j) * ldr] = v;
     }
   }
+}
+
+// Correction for deferred columns (class 2) against accepted orthonormal columns (class 1):
+// Mc[a][k] = -Gb[a][k] for a in A, k in D (so that Block += Block * Mc is one CGS step).
+__global__ void k_defer_corr(int N, const double* Gb, long long gs_e, const int* cls, long long cs_e, double* Mc,
+                             const int* active) {
+  const int e = blockIdx.x;
+  if (active && !active[e]) return;
+  const int* c = cls + e * cs_e;
+  const double* G = Gb + e * gs_e;
+  double* M = Mc + size_t(e) * N * N;
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    int a = idx % N, k = idx / N;
+    M[idx] = (c[a] == 1 && c[k] == 2) ? -G[a + size_t(k) * N] : 0.0;
+  }
+}
+
+void launch_defer_corr(cudaStream_t st, int E, int N, const double* Gb, long long gs_e, const int* cls, long long cs_e,
+                       double* Mc, const int* active) {
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_defer_corr<<<E, 128, 0, st>>>(N, Gb, gs_e, cls, cs_e, Mc, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- one-sided Jacobi SVD
@@ -578,11 +649,12 @@ void launch_sym_eig_select(cudaStream_t st, int E, int s, const double* G, doubl
 void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long gs_e, int ldg,
                        const double* norm0, long long ns_e, int ldn, double defl, double* Rinv, const double* Rprev,
                        long long rps_e, int ldrp, double* Rout, long long rs_e, int ldr, int* live,
-                       long long ls_e, const int* active) {
+                       long long ls_e, const int* active, bool pivoted, double dtol, double* norm0_out) {
   if (N > MAXS) fail(1, "block width > 64 not supported");
   ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
   k_block_chol<<<E, PEXP_THREADS, SM2, st>>>(N, G, gs_e, ldg, norm0, ns_e, ldn, defl, Rinv, Rprev, rps_e, ldrp,
-                                            Rout, rs_e, ldr, live, ls_e, active);
+                                            Rout, rs_e, ldr, live, ls_e, active, pivoted ? 1 : 0, g_piv_tol, dtol,
+                                            norm0_out);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }

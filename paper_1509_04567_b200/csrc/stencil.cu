@@ -174,7 +174,7 @@ __global__ void k_add_block(int rows, int cols, const double* S, long long ss_e,
   }
 }
 
-// H_e[0:rows, 0:m] += T_e[0:rows, 0:m] * R_e (m x m upper triangular)
+// H_e[0:rows, 0:m] += T_e[0:rows, 0:m] * R_e (m x m, general: pivoted CholQR factors)
 __global__ void k_hupdate(int rows, int m, const double* T, long long ts_e, int ldt, const double* R, long long rs_e,
                           int ldr, double* H, long long hs_e, int ldh, const int* active) {
   const int e = blockIdx.y;
@@ -185,7 +185,7 @@ __global__ void k_hupdate(int rows, int m, const double* T, long long ts_e, int 
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < rows * m; k += gridDim.x * blockDim.x) {
     int i = k % rows, j = k / rows;
     double a = 0.0;
-    for (int p = 0; p <= j; ++p) a = fma(Te[i + size_t(p) * ldt], Re[p + size_t(j) * ldr], a);
+    for (int p = 0; p < m; ++p) a = fma(Te[i + size_t(p) * ldt], Re[p + size_t(j) * ldr], a);
     He[i + size_t(j) * ldh] += a;
   }
 }

@@ -84,6 +84,70 @@ k_xty_partial(int n, int rch, const double* X, long long xs_e, int x0, int nx, c
   }
 }
 
+// Tall-skinny X^T Y for ny <= 32 (the BCGS projections V^T W and block Grams): the CTA's
+// row chunk of Y is staged once in shared memory (column-major, conflict-free); every warp
+// streams whole X columns of the chunk (coalesced 256-B loads, 4 rows per lane in flight),
+// accumulates the ny dot products per lane and reduces them with warp shuffles.  X is read
+// exactly once from HBM; Y once per chunk.
+template <int NYB>
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_xty_tall(int n, int rch, int rsub, const double* X, long long xs_e, int x0, int nx, const double* Y, long long ys_e,
+           int y0, int ny, double* part, const int* active) {
+  extern __shared__ double sm[];
+  double* Ys = sm;                 // [ny][rsub]   current sub-chunk of Y (column-major)
+  double* Ps = sm + ny * rsub;     // [nx][ny]     CTA partial
+  const int e = blockIdx.y, ch = blockIdx.x, nch = gridDim.x;
+  if (active && !active[e]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = PEXP_THREADS / 32;
+  for (int i = threadIdx.x; i < nx * ny; i += PEXP_THREADS) Ps[i] = 0.0;
+  const int cbeg = ch * rch, cend = min(n, cbeg + rch);
+  for (int r0 = cbeg; r0 < cend; r0 += rsub) {
+    const int rows = min(rsub, cend - r0);
+    const double* Xe = X + e * xs_e + size_t(x0) * n + r0;
+    const double* Ye = Y + e * ys_e + size_t(y0) * n + r0;
+    __syncthreads();
+    for (int b = 0; b < ny; ++b)
+      for (int r = threadIdx.x; r < rsub; r += PEXP_THREADS) Ys[b * rsub + r] = r < rows ? Ye[size_t(b) * n + r] : 0.0;
+    __syncthreads();
+    for (int a = warp; a < nx; a += nw) {
+      const double* xc = Xe + size_t(a) * n;
+      double acc[NYB];
+#pragma unroll
+      for (int b = 0; b < NYB; ++b) acc[b] = 0.0;
+      int r = lane;
+      for (; r + 96 < rows; r += 128) {
+        double x0v = xc[r], x1v = xc[r + 32], x2v = xc[r + 64], x3v = xc[r + 96];
+#pragma unroll
+        for (int b = 0; b < NYB; ++b) {
+          if (b < ny) {
+            const double* yb = Ys + b * rsub + r;
+            acc[b] = fma(x0v, yb[0], acc[b]);
+            acc[b] = fma(x1v, yb[32], acc[b]);
+            acc[b] = fma(x2v, yb[64], acc[b]);
+            acc[b] = fma(x3v, yb[96], acc[b]);
+          }
+        }
+      }
+      for (; r < rows; r += 32) {
+        double xv = xc[r];
+#pragma unroll
+        for (int b = 0; b < NYB; ++b)
+          if (b < ny) acc[b] = fma(xv, Ys[b * rsub + r], acc[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < NYB; ++b) {
+        if (b < ny) {
+          double v = warp_sum(acc[b]);
+          if (lane == 0) Ps[a + b * nx] += v;  // column a is owned by this warp: no race
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* P = part + (size_t(e) * nch + ch) * size_t(nx) * ny;
+  for (int i = threadIdx.x; i < nx * ny; i += PEXP_THREADS) P[i] = Ps[i];
+}
+
 // D_e[row0 + a, col0 + b] (= or +=) sum_ch part[e][ch][a + b*nx]
 __global__ void k_reduce(int nx, int ny, int nch, const double* part, double* D, long long ds_e,
                          int ldd, int row0, int col0, int accumulate, const int* active) {
@@ -102,16 +166,17 @@ __global__ void k_reduce(int nx, int ny, int nch, const double* part, double* D,
 
 constexpr int NB = 32;  // max output columns per combine launch
 
+template <int NBT>
 __global__ void __launch_bounds__(PEXP_THREADS)
 k_combine(int n, const double* X, long long xs_e, int x0, int nx, const double* M, long long ms_e,
           int ldm, double* O, long long os_e, int o0, int ny, double alpha, double beta,
           const int* active, const int* nxe) {
-  extern __shared__ double Ms[];  // [nx][NB]
+  extern __shared__ double Ms[];  // [nx][NBT]
   const int e = blockIdx.y;
   if (active && !active[e]) return;
   const double* Me = M + e * ms_e;
-  for (int idx = threadIdx.x; idx < nx * NB; idx += PEXP_THREADS) {
-    int a = idx / NB, b = idx % NB;
+  for (int idx = threadIdx.x; idx < nx * NBT; idx += PEXP_THREADS) {
+    int a = idx / NBT, b = idx % NBT;
     Ms[idx] = b < ny ? Me[a + size_t(b) * ldm] : 0.0;
   }
   __syncthreads();
@@ -119,18 +184,31 @@ k_combine(int n, const double* X, long long xs_e, int x0, int nx, const double* 
   if (row >= n) return;
   const double* Xe = X + e * xs_e + size_t(x0) * n + row;
   const int nxl = nxe ? min(nx, nxe[e]) : nx;
-  double acc[NB];
+  double acc[NBT];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) acc[b] = 0.0;
-  for (int a = 0; a < nxl; ++a) {
+  for (int b = 0; b < NBT; ++b) acc[b] = 0.0;
+  int a = 0;
+  for (; a + 3 < nxl; a += 4) {  // 4 independent column loads in flight
+    double x0v = Xe[size_t(a) * n], x1v = Xe[size_t(a + 1) * n], x2v = Xe[size_t(a + 2) * n],
+           x3v = Xe[size_t(a + 3) * n];
+    const double* mr = Ms + a * NBT;
+#pragma unroll
+    for (int b = 0; b < NBT; ++b) {
+      acc[b] = fma(x0v, mr[b], acc[b]);
+      acc[b] = fma(x1v, mr[NBT + b], acc[b]);
+      acc[b] = fma(x2v, mr[2 * NBT + b], acc[b]);
+      acc[b] = fma(x3v, mr[3 * NBT + b], acc[b]);
+    }
+  }
+  for (; a < nxl; ++a) {
     double xv = Xe[size_t(a) * n];
-    const double* mr = Ms + a * NB;
+    const double* mr = Ms + a * NBT;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) acc[b] = fma(xv, mr[b], acc[b]);
+    for (int b = 0; b < NBT; ++b) acc[b] = fma(xv, mr[b], acc[b]);
   }
   double* Oe = O + e * os_e + size_t(o0) * n + row;
 #pragma unroll
-  for (int b = 0; b < NB; ++b)
+  for (int b = 0; b < NBT; ++b)
     if (b < ny) {
       double v = alpha * acc[b];
       if (beta != 0.0) v = fma(beta, Oe[size_t(b) * n], v);
@@ -139,6 +217,19 @@ k_combine(int n, const double* X, long long xs_e, int x0, int nx, const double* 
 }
 
 // ---------------------------------------------------------------- host wrappers
+// Tall path plan: Y sub-chunks of rsub rows (<= 48 KB of shared memory), CTA row range rch
+// (multiple of rsub) chosen for ~6 waves over 148 SMs; partial count E*nch stays small.
+void xty_tall_plan(int n, int E, int nx, int ny, int& rsub, int& rch, int& nch) {
+  rsub = std::max(128, std::min(2048, (48 * 1024 / 8) / std::max(ny, 1)) / 128 * 128);
+  if (long(cdiv(n, rsub)) * E < 148 * 6)  // few evaluations: smaller chunks for more CTAs
+    rsub = std::max(128, std::min(rsub, int(long(n) * E / (148 * 6)) / 128 * 128));
+  long want = std::max(1L, long(148 * 6) / std::max(E, 1));  // chunks per eval
+  long per = std::max(1L, long(cdiv(n, rsub)) / want);        // sub-chunks per CTA
+  rch = int(per * rsub);
+  nch = cdiv(n, rch);
+  (void)nx;
+}
+
 int xty_chunks(int n, int E) {
   // aim for >= ~4 waves of CTAs over 148 SMs, chunks of >= 512 rows
   int rch = 512;
@@ -151,6 +242,31 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
                 double* D, long long ds_e, int ldd, int row0, int col0, bool accumulate,
                 const int* active) {
   if (E == 0 || nx == 0 || ny == 0) return;
+  if (ny <= 32) {
+    int rsub, rch, nch;
+    xty_tall_plan(n, E, nx, ny, rsub, rch, nch);
+    if (size_t(E) * nch * nx * ny > part_cap) fail(2, "xty partial buffer too small");
+    const bool same = (X == Y && xs_e == ys_e && y0 >= x0 && y0 + ny <= x0 + nx);
+    ProfScope ps(PC_XTY, st, double(E) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * E * double(n) * nx * ny);
+    size_t smem = (size_t(rsub) * ny + size_t(nx) * ny) * sizeof(double);
+    if (smem > 200 * 1024) fail(1, "xty: nx*ny too large for the tall path");
+    dim3 grid(nch, E);
+    if (ny <= 4)
+      k_xty_tall<4><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+    else if (ny <= 8)
+      k_xty_tall<8><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+    else if (ny <= 16)
+      k_xty_tall<16><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+    else
+      k_xty_tall<32><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+    dim3 g2(std::min(cdiv(nx * ny, PEXP_THREADS), 64), E);
+    k_reduce<<<g2, PEXP_THREADS, 0, st>>>(nx, ny, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, active);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+    return;
+  }
   int rch = xty_chunks(n, E);
   int nch = cdiv(n, rch);
   if (size_t(E) * nch * nx * ny > part_cap) fail(2, "xty partial buffer too small");
@@ -190,11 +306,19 @@ void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs
     }
     if (ny > NB && O == X && o0 < x0 + nx && x0 < o0 + ny && xs_e == os_e)
       fail(1, "combine: in-place product with more than 32 output columns");
-    size_t smem = size_t(std::max(nx, 1)) * NB * sizeof(double);
+    const int nbt = nb <= 4 ? 4 : nb <= 8 ? 8 : nb <= 16 ? 16 : 32;
+    size_t smem = size_t(std::max(nx, 1)) * nbt * sizeof(double);
     ProfScope ps(PC_COMBINE, st, double(E) * n * 8.0 * (nx + nb * (beta != 0.0 ? 2 : 1)), 2.0 * E * double(n) * nx * nb);
     dim3 grid(cdiv(n, PEXP_THREADS), E);
-    k_combine<<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, M + size_t(b0) * ldm, ms_e, ldm,
-                                                 O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
+    const double* Mb = M + size_t(b0) * ldm;
+    if (nbt == 4)
+      k_combine<4><<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, Mb, ms_e, ldm, O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
+    else if (nbt == 8)
+      k_combine<8><<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, Mb, ms_e, ldm, O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
+    else if (nbt == 16)
+      k_combine<16><<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, Mb, ms_e, ldm, O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
+    else
+      k_combine<32><<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, Mb, ms_e, ldm, O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
     count_launch();
     PEXP_LAUNCH_CHECK();
   }
@@ -206,7 +330,14 @@ void tsmm_init() {
   cudaFuncSetAttribute(k_xty_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_xty_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_xty_partial<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_combine<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_combine<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_combine<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_combine<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_tall<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_tall<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_tall<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_xty_tall<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 }  // namespace pexp

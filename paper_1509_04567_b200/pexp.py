@@ -89,7 +89,7 @@ class Context:
     """One pexp context (an operator A = nu*D2 - a*D1 on n points, or a batch of them)."""
 
     def __init__(self, n: int, bc: str = "periodic", nu=1e-2, a=0.0, *, s: int = 32, k_max: int = 256,
-                 svd_tau_factor: float = 0.01, stop_factor: float = 0.01, restart_blocks: int = 20,
+                 svd_tau_factor: float = 0.01, stop_factor: float = 0.1, restart_blocks: int = 20,
                  stream: Optional[torch.cuda.Stream] = None, stop_rule: int = 0):
         self.n, self.bc, self.s = int(n), bc, int(s)
         self._stream = stream
