@@ -228,10 +228,10 @@ def main():
             return ctx.solve_linear(u0, src, p.T, p.P, p.tol, out=out)[1]
         return ctx.solve_burgers(u0, p.nu, p.T, p.P, p.tol, p.max_wr_iters, out=out)[1]
 
+    st = None
     for _ in range(args.warmup):
         st = step()
     torch.cuda.synchronize()
-    evals_per_step = st["evals"]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -251,6 +251,7 @@ def main():
             launches += st["kernel_launches"]
     prof = pexp.profile_read()
     pexp.profile_enable(False)
+    evals_per_step = st["evals"]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -7,48 +7,73 @@
 namespace pexp {
 
 // C = alpha*A*B + beta*C ; A: M x K (lda), B: K x N (ldb), C: M x N (ldc); C must not alias.
-// 64x64 output tiles, K-steps of 16 staged in shared memory, 4x4 register tile per thread.
-__device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda,
-                                const double* B, int ldb, double beta, double* C, int ldc) {
-  __shared__ double As[16][64 + 1];
-  __shared__ double Bs[16][64 + 1];
-  const int t = threadIdx.x, tr = t % 16, tc = t / 16;  // 16 x 16 threads, 4x4 each
-  for (int i0 = 0; i0 < M; i0 += 64)
-    for (int j0 = 0; j0 < N; j0 += 64) {
-      double acc[4][4];
+// Tiles TM x TM (TM = 128 or 64) with K-steps of 16 staged in shared memory; 256 threads as a
+// 16 x 16 grid, each owning (TM/16)^2 outputs strided by 16 (conflict-free shared reads, 4 FMA
+// per shared load at TM = 128); the next K-step is prefetched into registers while the current
+// one is consumed (hides the L2 latency of these L2-resident operands).
+// one shared staging buffer per kernel, shared by both tile instantiations
+__device__ inline double* gemm_smem() {
+  __shared__ double buf[2 * 16 * (128 + 1)];
+  return buf;
+}
+
+template <int TM>
+__device__ inline void cta_gemm_t(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
+                                  int ldb, double beta, double* C, int ldc) {
+  constexpr int R = TM / 16;          // outputs per thread per dimension
+  constexpr int LA = TM * 16 / 256;   // A-tile elements loaded per thread
+  double (*As)[TM + 1] = reinterpret_cast<double (*)[TM + 1]>(gemm_smem());
+  double (*Bs)[TM + 1] = reinterpret_cast<double (*)[TM + 1]>(gemm_smem() + 16 * (TM + 1));
+  const int t = threadIdx.x, tx = t % 16, ty = t / 16;
+  for (int i0 = 0; i0 < M; i0 += TM)
+    for (int j0 = 0; j0 < N; j0 += TM) {
+      double acc[R][R];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < R; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int b = 0; b < R; ++b) acc[a][b] = 0.0;
+      double pa[LA], pb[LA];
+      auto load = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < LA; ++q) {
+          int idx = t + q * 256;
+          int r = idx % TM, kk = idx / TM;        // A: rows fastest (coalesced)
+          int gi = i0 + r, gk = k0 + kk;
+          pa[q] = (gi < M && gk < K) ? A[gi + size_t(gk) * lda] : 0.0;
+          int kb = idx % 16, c = idx / 16;        // B: k fastest within a column
+          int gkb = k0 + kb, gj = j0 + c;
+          pb[q] = (gkb < K && gj < N) ? B[gkb + size_t(gj) * ldb] : 0.0;
+        }
+      };
+      load(0);
       for (int k0 = 0; k0 < K; k0 += 16) {
         __syncthreads();
-        for (int idx = t; idx < 16 * 64; idx += blockDim.x) {
-          int r = idx % 64, kk = idx / 64;  // A tile: rows i0+r, col k0+kk (coalesced in r)
-          int gi = i0 + r, gk = k0 + kk;
-          As[kk][r] = (gi < M && gk < K) ? A[gi + size_t(gk) * lda] : 0.0;
-          int kb = idx % 16, c = idx / 16;  // B tile: row k0+kb, col j0+c
-          int gkb = k0 + kb, gj = j0 + c;
-          Bs[kb][c] = (gkb < K && gj < N) ? B[gkb + size_t(gj) * ldb] : 0.0;
+#pragma unroll
+        for (int q = 0; q < LA; ++q) {
+          int idx = t + q * 256;
+          As[idx / TM][idx % TM] = pa[q];
+          Bs[idx % 16][idx / 16] = pb[q];
         }
         __syncthreads();
+        if (k0 + 16 < K) load(k0 + 16);
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {
-          double av[4], bv[4];
+          double av[R], bv[R];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) av[a] = As[kk][tr + 16 * a];
+          for (int a = 0; a < R; ++a) av[a] = As[kk][ty + 16 * a];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tc + 16 * b];
+          for (int b = 0; b < R; ++b) bv[b] = Bs[kk][tx + 16 * b];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < R; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            for (int b = 0; b < R; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
         }
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < R; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          int gi = i0 + tr + 16 * a, gj = j0 + tc + 16 * b;
+        for (int b = 0; b < R; ++b) {
+          int gi = i0 + ty + 16 * a, gj = j0 + tx + 16 * b;
           if (gi < M && gj < N) {
             double* c = C + gi + size_t(gj) * ldc;
             double v = alpha * acc[a][b];
@@ -58,6 +83,14 @@ __device__ inline void cta_gemm(int M, int N, int K, double alpha, const double*
         }
     }
   __syncthreads();
+}
+
+__device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
+                                int ldb, double beta, double* C, int ldc) {
+  if (M > 64 && N > 64)
+    cta_gemm_t<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else
+    cta_gemm_t<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 // Y = alpha*X + beta*Y (+ gamma*I) on N x N

@@ -50,7 +50,33 @@ struct SPArgs {
   long long iwork_slot;
   int Nmax;
   int stop_rule;                 // 0: SaI residual ||t||/gamma ; 1: true residual sqrt(t^T Gt t)/gamma
+  // kind 2 (grouped homogeneous legs): block 0 = QR of m start vectors, z0 = R0
+  const double* R0;              // [E] m x m (ld m)
+  const double* critc;           // [E][m] per-leg residual targets
+  const int* horc;               // [E][m] per-leg horizons in steps of h (0: unused column)
+  int groups;                    // legs of eval e start at j0 = (e % groups) * m
 };
+
+// Arguments of the fused Arnoldi step (arnoldi.cu), one CTA per evaluation.
+struct StepArgs {
+  int E, n, m, b, kcap, periodic;
+  double* V;
+  long long vs_e;
+  double* H;                      // ld = kcap
+  long long hs_e;
+  int* live;                      // [E][kcap]
+  const int* fidx;
+  const double *fl, *fdinv, *fsup, *fz, *fw;
+  double* W0;                     // [E] m x n scratch (raw SaI image)
+  long long w0s_e;
+  const int* active;
+  double defl, piv_tol;
+  int rc;
+};
+
+// arnoldi.cu
+bool arnoldi_fused_ok(int m, int kcap);
+void launch_arnoldi_step(cudaStream_t st, StepArgs a);
 
 // tridiag.cu
 void launch_ade_rows(cudaStream_t st, int nops, int n, bool dirichlet, const double* nu, const double* a,
@@ -68,7 +94,8 @@ int xty_chunks(int n, int E);
 void xty_tall_plan(int n, int E, int nx, int ny, int& rsub, int& rch, int& nch);
 void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
                 const double* Y, long long ys_e, int y0, int ny, double* part, size_t part_cap, double* D,
-                long long ds_e, int ldd, int row0, int col0, bool accumulate, const int* active);
+                long long ds_e, int ldd, int row0, int col0, bool accumulate, const int* active,
+                int* cnt = nullptr);
 void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
                     const double* M, long long ms_e, int ldm, double* O, long long os_e, int o0, int ny,
                     double alpha, double beta, const int* active, const int* nxe = nullptr);
@@ -91,6 +118,7 @@ void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, 
 void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, const double* Cfin, double h,
                    double eta, double* coef, double* crit);
 void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots);
+void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots);
 void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
                          long long work_slot, int* iwork, int nslots);
 void small_init();
@@ -113,7 +141,11 @@ void launch_burgers_source(cudaStream_t st, int P, int s, int n, double nu, cons
 void launch_wr_step(cudaStream_t st, int s, int n, const double* u0, const double* Wh, const double* Y,
                     const double* Uold, double* Unew, double* uhat_end, double* delta);
 void launch_superpose(cudaStream_t st, int batch, int P, int n, const double* u0, const double* Yend,
-                      const double* Yh, long long yh_e, long long yh_node, double* out);
+                      const double* Yh, long long yh_e, long long yh_node, int groups, double* out);
+void launch_hom_start_block(cudaStream_t st, int Eh, int mh, int groups, int P, int n, const double* Y, double* V,
+                            long long vs_e, double* beta);
+void launch_hom_setup_block(cudaStream_t st, int Eh, int mh, int groups, int P, double dT, double eta,
+                            const double* beta, double* critc, int* horc, int* active);
 void launch_copy_end(cudaStream_t st, int P, int s, int n, const double* U, double* out);
 void launch_norms(cudaStream_t st, int E, int n, const double* X, long long xs_e, double* nrm);
 void launch_scale_cols(cudaStream_t st, int E, int n, const double* X, long long xs_e, const double* nrm,

@@ -20,9 +20,10 @@ bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 
 // ---------------------------------------------------------------- helper kernels
-__global__ void k_set_live0(int E, int kcap, int m, int* live) {
+__global__ void k_set_live0(int E, int kcap, int m, int* live, int keep_block0) {
   const int e = blockIdx.x;
-  for (int c = threadIdx.x; c < kcap; c += blockDim.x) live[size_t(e) * kcap + c] = c < m ? 1 : 0;
+  for (int c = threadIdx.x; c < kcap; c += blockDim.x)
+    if (!(keep_block0 && c < m)) live[size_t(e) * kcap + c] = c < m ? 1 : 0;
 }
 
 __global__ void k_active_from_m(int E, const int* m, int* active) {
@@ -77,10 +78,10 @@ static Opts norm_opts(const pexp_options& o) {
 
 // ---------------------------------------------------------------- EBK buffers
 struct EbkBufs {
-  int E = 0, n = 0, kcap = 0, mcap = 0, nout = 0, s = 0;
+  int E = 0, n = 0, kcap = 0, mcap = 0, nout = 0, s = 0, groups = 1;
   long long vs_e = 0, hs_e = 0, zs_e = 0;
-  double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p;
-  int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx;
+  double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p, *R0, *critc;
+  int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc;
   double* part;
   size_t part_cap;
   double* work;
@@ -107,10 +108,13 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, i
   B.G1 = ar.take<double>(size_t(E) * mcap * mcap);
   B.Rinv = ar.take<double>(size_t(E) * mcap * mcap);
   B.Rtmp = ar.take<double>(size_t(E) * mcap * mcap);
+  B.R0 = ar.take<double>(size_t(E) * mcap * mcap);
+  B.critc = ar.take<double>(size_t(E) * mcap);
+  B.horc = ar.take<int>(size_t(E) * mcap);
   B.res = ar.take<double>(E);
   B.gam = ar.take<double>(E);
   B.crit = ar.take<double>(E);
-  B.beta = ar.take<double>(E);
+  B.beta = ar.take<double>(size_t(E) * mcap);
   B.coef = forced ? ar.take<double>(size_t(E) * (s - 1) * 4 * mcap) : nullptr;
   B.live = ar.take<int>(size_t(E) * kcap);
   B.active = ar.take<int>(E);
@@ -120,6 +124,7 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, i
   B.count = ar.take<int>(4);
   B.fidx = ar.take<int>(E);
   B.opidx = ar.take<int>(E);
+  B.xcnt = ar.take<int>(E);
   // bound on E'*nch(E') for every E' <= E (xty_chunks stops at <= 1184 CTAs or one chunk)
   size_t ech = std::max<size_t>(size_t(E) * cdiv(n, xty_chunks(n, E)), 2 * 148 * 8 + size_t(E));
   ech = std::min<size_t>(ech, size_t(E) * cdiv(n, 512));
@@ -137,6 +142,46 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, i
   B.iwork = ar.take<int>(size_t(B.nslots) * B.iwork_slot);
 }
 
+// Pivoted deflating Cholesky-QR of the m columns of V at column offset c0 (in place):
+// Gram -> k_block_chol -> W <- W Rinv.  norm0 (nullable) = pre-orthogonalisation norms for
+// the deflation test; dtol > 0 defers nearly dependent columns (class 2, passed through raw).
+static void chol_combine_block(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0, const double* n0,
+                               long long n0s, int n0ld, double dtol, double defl, double* n0out, const int* active) {
+  const long long ws_e = B.vs_e;
+  launch_xty(st, E, n, B.V, ws_e, c0, m, B.V, ws_e, c0, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0, false,
+             active, B.xcnt);
+  launch_block_chol(st, E, m, B.G1, (long long)m * m, m, n0, n0s, n0ld, defl, B.Rinv, nullptr, 0, 0, nullptr, 0, 0,
+                    B.live + c0, B.kcap, active, true, dtol, n0out);
+  if (m <= 32) {
+    launch_combine(st, E, n, B.V, ws_e, c0, m, B.Rinv, (long long)m * m, m, B.V, ws_e, c0, m, 1.0, 0.0, active);
+  } else {
+    launch_combine(st, E, n, B.V, ws_e, c0, m, B.Rinv, (long long)m * m, m, B.Wt2, (long long)m * n, 0, m, 1.0, 0.0,
+                   active);
+    PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.V + size_t(c0) * n, ws_e * sizeof(double), B.Wt2, size_t(m) * n * sizeof(double),
+                                    size_t(m) * n * sizeof(double), E, cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+// Robust in-block QR of the m columns at offset c0 (already orthogonal to earlier columns up to
+// the first BCGS pass): stage A accepts well-separated columns (scaled pivot > 1e-8), defers
+// nearly dependent ones; stage B re-orthogonalises deferred columns explicitly (CGS2); stage C
+// accepts or deflates them relative to their pre-orthogonalisation norms norm0.
+static void inblock_qr(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0, const double* norm0, long long n0s,
+                       int n0ld, double defl, const int* active) {
+  const long long ws_e = B.vs_e;
+  chol_combine_block(st, B, E, n, m, c0, norm0, n0s, n0ld, 1e-8, defl, B.n0p, active);
+  for (int rep = 0; rep < 2; ++rep) {
+    launch_xty(st, E, n, B.V, ws_e, c0, m, B.V, ws_e, c0, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0, false,
+               active, B.xcnt);
+    launch_defer_corr(st, E, m, B.G1, (long long)m * m, B.live + c0, B.kcap, B.Rinv, active);
+    if (m <= 32)
+      launch_combine(st, E, n, B.V, ws_e, c0, m, B.Rinv, (long long)m * m, m, B.V, ws_e, c0, m, 1.0, 1.0, active);
+    else
+      fail(1, "block width > 32 with deferred columns not supported");
+  }
+  chol_combine_block(st, B, E, n, m, c0, B.n0p, m, 0, 0.0, defl, nullptr, active);
+}
+
 struct RunInfo {
   int max_k = 0;
   int unconverged = 0;
@@ -152,13 +197,16 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   const int E = B.E, n = B.n, kcap = B.kcap;
   if (E == 0) return info;
   if (m > B.mcap) fail(1, "block width exceeds capacity");
-  k_set_live0<<<E, 128, 0, st>>>(E, kcap, m, B.live);
+  PEXP_CUDA_TRY(cudaMemsetAsync(B.xcnt, 0, E * sizeof(int), st));
+  k_set_live0<<<E, 128, 0, st>>>(E, kcap, m, B.live, kind == 2 ? 1 : 0);
   count_launch();
   launch_fill_f64(st, B.H, size_t(E) * kcap * kcap, 0.0);
   launch_fill_f64(st, B.Z, size_t(E) * nout * kcap, 0.0);
   launch_fill_i32(st, B.kfin, E, 0);
   launch_fill_i32(st, B.conv, E, 0);
   PEXP_LAUNCH_CHECK();
+  static const bool nofuse = getenv("PEXP_NOFUSE") != nullptr;  // developer switch
+  const bool fused = !nofuse && E >= 512 && n <= 16384 && arnoldi_fused_ok(m, kcap);
   int steps = 0, last_check = -1;
   int next_check = std::max(4, 2 * m);
   // deflation: a new column is dropped when BCGS leaves < 1e-10 of ||(I - gamma A)^{-1} v|| (well
@@ -179,6 +227,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   a.res = B.res; a.conv = B.conv; a.kfin = B.kfin; a.active = B.active;
   a.work = B.work; a.work_slot = B.work_slot; a.iwork = B.iwork; a.iwork_slot = B.iwork_slot; a.Nmax = B.Nmax;
   a.stop_rule = stop_rule;
+  a.R0 = B.R0; a.critc = B.critc; a.horc = B.horc; a.groups = std::max(1, B.groups);
   int remaining = E;
   std::vector<double> prevq(E, -1.0), curq(E, -1.0);
   std::vector<int> prevK(E, -1);
@@ -189,11 +238,14 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     if (stop_rule == 1) {  // true residual: tail Gram of Wt = (I - gamma A) V[:, K:K+m]
       launch_apply_M(st, O, B.opidx, B.gam, E, m, B.V, B.vs_e, K, B.Wt, (long long)m * n, 0, periodic, B.active);
       launch_xty(st, E, n, B.Wt, (long long)m * n, 0, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.Gt,
-                 (long long)m * m, m, 0, 0, false, B.active);
+                 (long long)m * m, m, 0, 0, false, B.active, B.xcnt);
     }
     a.K = K;
     if (K + m > a.Nmax - (kind == 0 ? 4 * m : 0) + m) fail(1, "small problem exceeds workspace");
-    launch_small_problem(st, a, B.nslots);
+    if (kind == 2)
+      launch_small_hom(st, a, B.nslots);
+    else
+      launch_small_problem(st, a, B.nslots);
     PEXP_CUDA_TRY(cudaMemsetAsync(B.count, 0, sizeof(int), st));
     launch_update_active(st, E, B.conv, B.active, B.count);
     int h_count = 0;
@@ -212,8 +264,8 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       PEXP_CUDA_TRY(cudaStreamSynchronize(st));
       std::vector<double> preds;
       for (int e = 0; e < E; ++e) {
-        if (!hact[e] || !(hcrit[e] > 0)) continue;
-        double q = hres[e] / hcrit[e];
+        if (!hact[e] || !(kind == 2 || hcrit[e] > 0)) continue;
+        double q = kind == 2 ? hres[e] : hres[e] / hcrit[e];
         if (prevK[e] >= 0 && prevq[e] > 0 && q > 0 && q < prevq[e]) {
           double slope = (std::log(q) - std::log(prevq[e])) / double(K - prevK[e]);
           preds.push_back(K + std::log(0.5 / q) / slope);
@@ -258,7 +310,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       std::vector<double> q;
       int tail_live = 0, dead_total = 0;
       for (int e = 0; e < E; ++e) {
-        q.push_back(c[e] > 0 ? r[e] / c[e] : -1);
+        q.push_back(kind == 2 ? r[e] : (c[e] > 0 ? r[e] / c[e] : -1));
         for (int j = K; j < K + m; ++j) tail_live += lv[size_t(e) * kcap + j];
         for (int j = 0; j < K; ++j) dead_total += !lv[size_t(e) * kcap + j];
       }
@@ -283,6 +335,14 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     }
     const int b = steps, nv = (b + 1) * m;
     const long long ws_e = B.vs_e;
+    if (fused) {  // one CTA per evaluation does the whole step (arnoldi.cu)
+      StepArgs sa{};
+      sa.E = E; sa.n = n; sa.m = m; sa.b = b; sa.kcap = kcap; sa.periodic = F.periodic;
+      sa.V = B.V; sa.vs_e = B.vs_e; sa.H = B.H; sa.hs_e = B.hs_e; sa.live = B.live; sa.fidx = B.fidx;
+      sa.fl = F.l; sa.fdinv = F.dinv; sa.fsup = F.sup; sa.fz = F.z; sa.fw = F.w;
+      sa.W0 = B.Wt; sa.w0s_e = (long long)m * n; sa.active = B.active; sa.defl = defl;
+      launch_arnoldi_step(st, sa);
+    } else {
     // W = (I - gamma A)^{-1} V_b  -> columns [nv, nv+m)
     launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
     // keep the raw image W0 = (I - gamma A)^{-1} V_b: the subdiagonal block of H is computed
@@ -292,54 +352,23 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
                                     cudaMemcpyDeviceToDevice, st));
     // norms of W0 (deflation reference)
     launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G0, (long long)m * m, m, 0, 0,
-               false, B.active);
+               false, B.active, B.xcnt);
     // BCGS pass 1: H[0:nv, block b] = V^T W0 ; W = W0 - V H
     launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.H, B.hs_e, kcap, 0, b * m,
-               false, B.active);
+               false, B.active, B.xcnt);
     launch_combine(st, E, n, B.V, ws_e, 0, nv, B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.V, ws_e, nv, m, -1.0, 1.0,
                    B.active);
-    // in-block QR, stage A: pivoted CholQR accepting only well-separated columns (scaled pivot
-    // > 1e-8, i.e. kappa <= 1e4); nearly dependent columns are DEFERRED (passed through raw,
-    // class 2), columns below defl * |W0| are dead.  norm0 is re-ordered to the new positions.
-    auto chol_combine = [&](const double* n0, long long n0s, int n0ld, double dtol, double* n0out) {
-      launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0,
-                 false, B.active);
-      launch_block_chol(st, E, m, B.G1, (long long)m * m, m, n0, n0s, n0ld, defl, B.Rinv, nullptr, 0, 0, nullptr, 0,
-                        0, B.live + nv, kcap, B.active, true, dtol, n0out);
-      if (m <= 32) {
-        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.V, ws_e, nv, m, 1.0, 0.0,
-                       B.active);
-      } else {
-        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.Wt2, (long long)m * n, 0, m, 1.0,
-                       0.0, B.active);
-        PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.V + size_t(nv) * n, ws_e * sizeof(double), B.Wt2,
-                                        size_t(m) * n * sizeof(double), size_t(m) * n * sizeof(double), E,
-                                        cudaMemcpyDeviceToDevice, st));
-      }
-    };
-    chol_combine(B.G0, (long long)m * m, m, 1e-8, B.n0p);
-    // stage B: explicit CGS2 of the deferred columns against the accepted ones
-    for (int rep = 0; rep < 2; ++rep) {
-      launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0,
-                 false, B.active);
-      launch_defer_corr(st, E, m, B.G1, (long long)m * m, B.live + nv, kcap, B.Rinv, B.active);
-      if (m <= 32)
-        launch_combine(st, E, n, B.V, ws_e, nv, m, B.Rinv, (long long)m * m, m, B.V, ws_e, nv, m, 1.0, 1.0, B.active);
-      else
-        fail(1, "block width > 32 with deferred columns not supported");
-    }
-    // stage C: final pivoted CholQR of the whole block (accepted columns are orthonormal, deferred
-    // remainders are orthogonal to them), deflating remainders below defl * |W0|
-    chol_combine(B.n0p, m, 0, 0.0, nullptr);
+    inblock_qr(st, B, E, n, m, nv, B.G0, (long long)m * m, m, defl, B.active);
     // BCGS pass 2 (re-orthogonalisation against V) + CholQR of the nearly orthonormal block
     launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.T, (long long)kcap * B.mcap, nv,
-               0, 0, false, B.active);
+               0, 0, false, B.active, B.xcnt);
     launch_combine(st, E, n, B.V, ws_e, 0, nv, B.T, (long long)kcap * B.mcap, nv, B.V, ws_e, nv, m, -1.0, 1.0,
                    B.active);
-    chol_combine(nullptr, 0, 0, 0.0, nullptr);
+    chol_combine_block(st, B, E, n, m, nv, nullptr, 0, 0, 0.0, defl, nullptr, B.active);
     // subdiagonal block: H[nv:nv+m, block b] = Q^T W0
     launch_xty(st, E, n, B.V, ws_e, nv, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.H, B.hs_e, kcap, nv,
-               b * m, false, B.active);
+               b * m, false, B.active, B.xcnt);
+    }
     ++steps;
     const int K = steps * m;
     if (K >= next_check || (steps + 2) * m > kcap) {
@@ -356,7 +385,8 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     PEXP_CUDA_TRY(cudaMemcpyAsync(c.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
     PEXP_CUDA_TRY(cudaStreamSynchronize(st));
     for (int e = 0; e < E; ++e)
-      if (c[e] > 0 && last_check >= 0) info.worst_res_ratio = std::max(info.worst_res_ratio, r[e] / c[e]);
+      if (last_check >= 0 && (kind == 2 || c[e] > 0))
+        info.worst_res_ratio = std::max(info.worst_res_ratio, kind == 2 ? r[e] : r[e] / c[e]);
   }
   return info;
 }
@@ -421,6 +451,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
   npass = std::min(npass, 4);
   double* part = B->part;
   size_t part_cap = B->part_cap;
+  PEXP_CUDA_TRY(cudaMemsetAsync(B->xcnt, 0, E * sizeof(int), st));
   PEXP_CUDA_TRY(cudaMemsetAsync(S.U, 0, size_t(E) * s * n * sizeof(double), st));
   launch_fill_i32(st, S.off, E, 0);
   double* U = S.U;   // current orthonormal basis (zero columns beyond off[e])
@@ -429,18 +460,18 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
     const double* X = G;
     if (p > 0) {
       // residual R = G - U (U^T G), explicit (pass p resolves what pass p-1 could not)
-      launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr);
+      launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
       PEXP_CUDA_TRY(cudaMemcpyAsync(Fr, G, size_t(E) * s * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
       launch_combine(st, E, n, U, gs_e, 0, s, S.Cb, (long long)s * s, s, Fr, gs_e, 0, s, -1.0, 1.0, nullptr);
       X = Fr;
     }
-    launch_xty(st, E, n, X, gs_e, 0, s, X, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false, nullptr);
+    launch_xty(st, E, n, X, gs_e, 0, s, X, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
     launch_sym_eig_select(st, E, s, S.Gs, S.lam, S.Msel, S.off, S.sigma1, p, tau, theta, nullptr);
     launch_combine(st, E, n, X, gs_e, 0, s, S.Msel, (long long)s * s, s, U, gs_e, 0, s, 1.0, 1.0, nullptr);
     // CholQR2 of U (masked: zero columns stay zero); ping-pong U <-> Fr
     for (int q = 0; q < 2; ++q) {
       launch_xty(st, E, n, U, gs_e, 0, s, U, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false,
-                 nullptr);
+                 nullptr, B->xcnt);
       launch_block_chol(st, E, s, S.Gs, (long long)s * s, s, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0, 0,
                         nullptr, 0, nullptr, false);
       launch_combine(st, E, n, U, gs_e, 0, s, S.Rinv, (long long)s * s, s, Fr, gs_e, 0, s, 1.0, 0.0, nullptr);
@@ -448,7 +479,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
     }
   }
   // C = U^T G, one-sided Jacobi SVD, truncation
-  launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr);
+  launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
   launch_onesided_svd(st, E, s, S.Cb, S.off, tau, S.Qs, S.sig, S.Cs, S.me, nullptr);
   std::vector<int> mh(E);
   PEXP_CUDA_TRY(cudaMemcpyAsync(mh.data(), S.me, E * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -464,7 +495,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
   launch_fill_random(st, E, n, mb, S.fill, B->V, B->vs_e, 12345u);
   for (int q = 0; q < 2; ++q) {
     launch_xty(st, E, n, B->V, B->vs_e, 0, mb, B->V, B->vs_e, 0, mb, part, part_cap, S.Gs, (long long)mb * mb, mb, 0, 0,
-               false, nullptr);
+               false, nullptr, B->xcnt);
     launch_block_chol(st, E, mb, S.Gs, (long long)mb * mb, mb, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0,
                       0, nullptr, 0, nullptr, false);
     if (mb <= 32) {
@@ -553,12 +584,15 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   L.Yend = ar.take<double>(size_t(E) * n);
   alloc_svd(ar, L.S, E, n, s);
   alloc_ebk(ar, L.B, E, n, o.kcap, s, 2, s, true, L.S.R);
-  if (Eh > 0) {
-    alloc_ebk(ar, L.Bh, Eh, n, o.kcap, 1, P, s, false, nullptr);
-    L.Yh = ar.take<double>(size_t(Eh) * P * n);
+  if (P > 1) {
+    const int mh = std::min(16, P - 1), G = cdiv(P - 1, mh), Eg = Bt * G;
+    alloc_ebk(ar, L.Bh, Eg, n, o.kcap, mh, P, s, false, nullptr);
+    L.Bh.groups = G;
+    L.Yh = ar.take<double>(size_t(Eg) * P * n);
   } else {
     L.Yh = nullptr;
   }
+  (void)Eh;
 }
 
 struct BurPlan {
@@ -741,23 +775,40 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     } else {
       PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
     }
-    if (Eh > 0) {
-      std::vector<int> fh(Eh), oh(Eh);
-      std::vector<double> gh(Eh, T / 10);
-      for (int e = 0; e < Eh; ++e) { fh[e] = Bt + e / (P - 1); oh[e] = e / (P - 1); }
-      h2d(st, L.Bh.fidx, fh);
-      h2d(st, L.Bh.opidx, oh);
-      h2d(st, L.Bh.gam, gh);
-      k_hom_start<<<Eh, PEXP_THREADS, 0, st>>>(P, n, L.Yend, n, L.Bh.beta, L.Bh.V, L.Bh.vs_e);
-      count_launch();
-      PEXP_LAUNCH_CHECK();
-      // legs are only needed at T_{j+1+q}: integrate the projected problem with step dT
-      launch_hom_setup(st, Eh, 0, P, 2, dT, eta, L.Bh.beta, L.Bh.crit, L.Bh.npieces, L.Bh.active);
-      rh = ebk_run(st, L.Bh, L.F, L.O, periodic, 1, 1, dT, 0, 1, P, o.stop_rule);
-      launch_combine(st, Eh, n, L.Bh.V, L.Bh.vs_e, 0, std::max(rh.max_k, 1), L.Bh.Z, L.Bh.zs_e, L.Bh.kcap, L.Yh,
-                     (long long)P * n, 0, P, 1.0, 0.0, nullptr, L.Bh.kfin);
+    int G = 0;
+    if (P > 1) {
+      // homogeneous legs, grouped: up to 16 consecutive legs share one block Krylov space
+      // (EBK for the homogeneous part too); group eh = b*G + g holds legs
+      // j = g*mh .. g*mh+mh-1 of problem b
+      const int mh = std::min(16, P - 1);
+      G = cdiv(P - 1, mh);
+      const int Eg = Bt * G;
+      EbkBufs& Bh = L.Bh;
+      std::vector<int> fh(Eg), oh(Eg);
+      std::vector<double> gh(Eg, T / 10);
+      for (int e = 0; e < Eg; ++e) { fh[e] = Bt + e / G; oh[e] = e / G; }
+      h2d(st, Bh.fidx, fh);
+      h2d(st, Bh.opidx, oh);
+      h2d(st, Bh.gam, gh);
+      launch_hom_start_block(st, Eg, mh, G, P, n, L.Yend, Bh.V, Bh.vs_e, Bh.beta);
+      // block 0 = orthonormal basis Q of the start vectors Y0 (robust pivoted/deferred in-block
+      // QR, legs below 1e-10 of their own norm deflated), z0 = R0 = Q^T Y0 (exact to eps)
+      PEXP_CUDA_TRY(cudaMemsetAsync(Bh.xcnt, 0, Eg * sizeof(int), st));
+      PEXP_CUDA_TRY(cudaMemcpy2DAsync(Bh.Wt, size_t(mh) * n * sizeof(double), Bh.V, Bh.vs_e * sizeof(double),
+                                      size_t(mh) * n * sizeof(double), Eg, cudaMemcpyDeviceToDevice, st));
+      launch_xty(st, Eg, n, Bh.V, Bh.vs_e, 0, mh, Bh.V, Bh.vs_e, 0, mh, Bh.part, Bh.part_cap, Bh.G0,
+                 (long long)mh * mh, mh, 0, 0, false, nullptr, Bh.xcnt);
+      static const double defl_h = getenv("PEXP_DEFL") ? atof(getenv("PEXP_DEFL")) : 1e-10;
+      inblock_qr(st, Bh, Eg, n, mh, 0, Bh.G0, (long long)mh * mh, mh, defl_h, nullptr);
+      chol_combine_block(st, Bh, Eg, n, mh, 0, nullptr, 0, 0, 0.0, defl_h, nullptr, nullptr);
+      launch_xty(st, Eg, n, Bh.V, Bh.vs_e, 0, mh, Bh.Wt, (long long)mh * n, 0, mh, Bh.part, Bh.part_cap, Bh.R0,
+                 (long long)mh * mh, mh, 0, 0, false, nullptr, Bh.xcnt);
+      launch_hom_setup_block(st, Eg, mh, G, P, dT, eta, Bh.beta, Bh.critc, Bh.horc, Bh.active);
+      rh = ebk_run(st, Bh, L.F, L.O, periodic, mh, 2, dT, 0, 1, P, o.stop_rule);
+      launch_combine(st, Eg, n, Bh.V, Bh.vs_e, 0, std::max(rh.max_k, 1), Bh.Z, Bh.zs_e, Bh.kcap, L.Yh,
+                     (long long)P * n, 0, P, 1.0, 0.0, nullptr, Bh.kfin);
     }
-    launch_superpose(st, Bt, P, n, u0, L.Yend, L.Yh, (long long)P * n, n, out);
+    launch_superpose(st, Bt, P, n, u0, L.Yend, P > 1 ? L.Yh : nullptr, (long long)P * n, n, G, out);
     PEXP_CUDA_TRY(cudaEventRecord(e1, st));
     PEXP_CUDA_TRY(cudaEventSynchronize(e1));
     float ms = 0;

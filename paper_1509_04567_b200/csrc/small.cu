@@ -69,22 +69,20 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
     Q[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
+  __shared__ int s_rot;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    double off2 = 0.0, dg2 = 0.0;
-    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
-      int i = idx % Ne, j = idx / Ne;
-      double v = A[i][j] * A[i][j];
-      if (i == j) dg2 += v; else off2 += v;
-    }
-    off2 = block_sum(off2, red);
-    dg2 = block_sum(dg2, red);
-    if (off2 <= 1e-32 * dg2 || off2 == 0.0) break;
+    if (threadIdx.x == 0) s_rot = 0;
+    __syncthreads();
     for (int r = 0; r < Ne - 1; ++r) {
       if (threadIdx.x < Ne / 2) {
         int p, q;
         jacobi_pair(Ne, r, threadIdx.x, p, q);
-        double c, sn;
-        sym_schur2(A[p][p], A[q][q], A[p][q], c, sn);
+        double c = 1.0, sn = 0.0;
+        // rotate only pairs that are not yet decoupled to working precision
+        if (fabs(A[p][q]) > 1e-16 * sqrt(fabs(A[p][p] * A[q][q])) && fabs(A[p][q]) > 1e-300) {
+          sym_schur2(A[p][p], A[q][q], A[p][q], c, sn);
+          s_rot = 1;
+        }
         rp[threadIdx.x] = p; rq[threadIdx.x] = q; rc[threadIdx.x] = c; rs[threadIdx.x] = sn;
       }
       __syncthreads();
@@ -106,7 +104,9 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
       }
       __syncthreads();
     }
+    if (!s_rot) break;
   }
+  (void)red;
   if (threadIdx.x == 0) {
     for (int i = 0; i < s; ++i) perm[i] = i;
     for (int i = 0; i < s; ++i) {
@@ -621,6 +621,135 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------- grouped homogeneous legs
+// One CTA per group of m legs (kind 2).  Block 0 of the Krylov basis is the QR of the legs'
+// start vectors v_j(T_{j+1}) = Q R0, so z_c(0) = R0[:, c].  With F = exp(dT * A_hat) the
+// projected states z_c(q dT) = F^q z_c(0) are advanced together (one K x K x m GEMM per step);
+// the contribution of leg j = j0 + c to output i = j + q (q >= 1) is accumulated in
+// Zsum[e][i] (K-vectors), so that Yh_e[i] = V_e Zsum[e][i] is the group's share of
+// sum_{j<i} exp((T_{i+1} - T_{j+1}) A) v_j(T_{j+1}) (Eq.(superposition)).
+// Residual per leg and step (SaI form) against crit_c; convergence when every leg passes.
+__global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
+  __shared__ int idx[KSMALL_MAX];
+  __shared__ int tidx[MAXS], lpos[MAXS];
+  __shared__ int s_K, s_mt, s_ml;
+  __shared__ double red[32];
+  __shared__ double xs[16 * 16], ts[16 * 16];  // (ml, mt <= m <= 16) x m
+  const int slot = blockIdx.x;
+  double* S0 = a.work + slot * a.work_slot;
+  const int ld = a.Nmax;
+  const size_t MM = size_t(ld) * ld;
+  double* S1 = S0 + MM;
+  double* S2 = S1 + MM;
+  double* WK = S2 + MM;
+  int* piv = a.iwork + slot * a.iwork_slot;
+  const int K = a.K, m = a.m;
+  for (int e = blockIdx.x; e < a.E; e += gridDim.x) {
+    if (a.active && !a.active[e]) continue;
+    const double* He = a.H + e * a.hs_e;
+    const int* lv = a.live + e * a.ls_e;
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int c = 0; c < K; ++c)
+        if (lv[c]) idx[k++] = c;
+      s_K = k;
+      int mt = 0;
+      for (int c = K; c < K + m; ++c)
+        if (lv[c]) tidx[mt++] = c;
+      s_mt = mt;
+      int ml = 0;
+      for (int r = 0; r < k; ++r)
+        if (idx[r] >= K - m) lpos[ml++] = r;
+      s_ml = ml;
+    }
+    __syncthreads();
+    const int Kp = s_K, mt = s_mt, ml = s_ml;
+    const double gam = a.gam[e];
+    for (int t = threadIdx.x; t < Kp * Kp; t += blockDim.x) {
+      int i = t % Kp, j = t / Kp;
+      S0[i + size_t(j) * ld] = He[idx[i] + size_t(idx[j]) * a.ldh];
+    }
+    __syncthreads();
+    cta_identity(Kp, S1, ld);
+    cta_lu(Kp, S0, ld, piv, red);
+    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp);
+    for (int t = threadIdx.x; t < Kp * Kp; t += blockDim.x) {
+      int i = t % Kp, j = t / Kp;
+      S2[i + size_t(j) * ld] = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
+    }
+    __syncthreads();
+    cta_expm_pade13(Kp, S2, ld, WK, ld, piv, red);
+    // Z (Kp x m) and Zn in the (now free) expm workspace
+    double* Z = WK;
+    double* Zn = WK + size_t(ld) * m;
+    const double* R0 = a.R0 + size_t(e) * m * m;
+    for (int t = threadIdx.x; t < Kp * m; t += blockDim.x) {
+      int r = t % Kp, c = t / Kp;
+      Z[r + size_t(c) * ld] = idx[r] < m ? R0[idx[r] + c * m] : 0.0;
+    }
+    double* Ze = a.Z + e * a.zs_e;
+    for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
+    __syncthreads();
+    const int j0 = (e % a.groups) * m;
+    const double* cc = a.critc + size_t(e) * m;
+    const int* hc = a.horc + size_t(e) * m;
+    int qmax = 0;
+    for (int c = 0; c < m; ++c) qmax = max(qmax, hc[c]);
+    double worst = 0.0;
+    for (int q = 1; q <= qmax; ++q) {
+      cta_gemm(Kp, m, Kp, 1.0, S2, ld, Z, ld, 0.0, Zn, ld);
+      double* tmp = Z; Z = Zn; Zn = tmp;
+      if (mt > 0) {
+        for (int t = threadIdx.x; t < ml * m; t += blockDim.x) {
+          int cidx = t % ml, c = t / ml;
+          double v = 0.0;
+          for (int j = 0; j < Kp; ++j) v = fma(S1[lpos[cidx] + size_t(j) * ld], Z[j + size_t(c) * ld], v);
+          xs[cidx + c * 16] = v;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < mt * m; t += blockDim.x) {
+          int tc = t % mt, c = t / mt;
+          double v = 0.0;
+          for (int cidx = 0; cidx < ml; ++cidx)
+            v = fma(He[tidx[tc] + size_t(idx[lpos[cidx]]) * a.ldh], xs[cidx + c * 16], v);
+          ts[tc + c * 16] = v;
+        }
+        __syncthreads();
+        double wq = 0.0;
+        for (int c = threadIdx.x; c < m; c += blockDim.x) {
+          if (q > hc[c]) continue;
+          double s2 = 0.0;
+          for (int tc = 0; tc < mt; ++tc) s2 += ts[tc + c * 16] * ts[tc + c * 16];
+          wq = fmax(wq, sqrt(s2) / gam / cc[c]);
+        }
+        worst = fmax(worst, block_max(wq, red));
+      }
+      for (int c = 0; c < m; ++c) {
+        if (q > hc[c]) continue;
+        const int i = j0 + c + q;
+        for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[size_t(i) * a.kcap + idx[r]] += Z[r + size_t(c) * ld];
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      a.res[e] = worst;
+      int cv = (mt == 0) || (worst <= 1.0);
+      a.conv[e] = cv;
+      if (cv && a.kfin) a.kfin[e] = K;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
+  if (a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
+  if (a.m > 16) fail(1, "grouped legs: at most 16 legs per group");
+  ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * a.K * a.K * a.K));
+  k_small_hom<<<std::min(a.E, nslots), PEXP_THREADS, 0, st>>>(a);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- batched expm (stage API)

@@ -129,14 +129,53 @@ __global__ void k_wr_step(int s, int n, const double* u0, const double* Wh, cons
   if (threadIdx.x == 0) atomic_max_nonneg(delta, mx);
 }
 
-// out[b][i] = u0[b] + Yend[b*P+i] + sum_{j<i} Yh[b*(P-1)+j][node i-j]   (Eq.(superposition))
+// out[b][i] = u0[b] + Yend[b*P+i] + sum_g Yh[b*groups+g][i]   (Eq.(superposition) PAPER.md:226;
+// Yh[.][i] already sums the legs of group g that reach T_{i+1})
 __global__ void k_superpose(int P, int n, const double* u0, const double* Yend, const double* Yh, long long yh_e,
-                            long long yh_node, double* out) {
+                            long long yh_node, int groups, double* out) {
   const int i = blockIdx.y, b = blockIdx.z;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     double a = u0[size_t(b) * n + r] + Yend[(size_t(b) * P + i) * n + r];
-    for (int j = 0; j < i; ++j) a += Yh[(long long)(b * (P - 1) + j) * yh_e + (i - j) * yh_node + r];
+    if (Yh)
+      for (int g = 0; g < groups; ++g) a += Yh[(long long)(b * groups + g) * yh_e + i * yh_node + r];
     out[(size_t(b) * P + i) * n + r] = a;
+  }
+}
+
+// Grouped legs: column c of group eh = b*groups + g starts from v_j(T_{j+1}) = Y[b*P + j],
+// j = g*mh + c (zero column when j >= P-1); beta = its norm.
+__global__ void k_hom_start_block(int mh, int groups, int P, int n, const double* Y, double* V, long long vs_e,
+                                  double* beta) {
+  const int eh = blockIdx.x, c = blockIdx.y;
+  __shared__ double red[32];
+  const int b = eh / groups, g = eh % groups, j = g * mh + c;
+  double* v = V + eh * vs_e + size_t(c) * n;
+  const bool ok = j < P - 1;
+  const double* y = Y + (size_t(b) * P + (ok ? j : 0)) * n;
+  double a = 0.0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double x = ok ? y[r] : 0.0;
+    v[r] = x;
+    a = fma(x, x, a);
+  }
+  a = block_sum(a, red);
+  if (threadIdx.x == 0) beta[size_t(eh) * mh + c] = sqrt(a);
+}
+
+__global__ void k_hom_setup_block(int Eh, int mh, int groups, int P, double dT, double eta, const double* beta,
+                                  double* critc, int* horc, int* active) {
+  for (int eh = blockIdx.x * blockDim.x + threadIdx.x; eh < Eh; eh += gridDim.x * blockDim.x) {
+    const int g = eh % groups;
+    int any = 0;
+    for (int c = 0; c < mh; ++c) {
+      const int j = g * mh + c;
+      const double bt = beta[size_t(eh) * mh + c];
+      const int hor = (j < P - 1 && bt > 0.0) ? (P - 1 - j) : 0;
+      horc[size_t(eh) * mh + c] = hor;
+      critc[size_t(eh) * mh + c] = hor > 0 ? eta * bt / (hor * dT) : 1.0;
+      any |= hor > 0;
+    }
+    active[eh] = any;
   }
 }
 
@@ -317,10 +356,10 @@ void launch_wr_step(cudaStream_t st, int s, int n, const double* u0, const doubl
 }
 
 void launch_superpose(cudaStream_t st, int batch, int P, int n, const double* u0, const double* Yend,
-                      const double* Yh, long long yh_e, long long yh_node, double* out) {
+                      const double* Yh, long long yh_e, long long yh_node, int groups, double* out) {
   dim3 grid(gx_small(n, batch * P), P, batch);
   { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
-  k_superpose<<<grid, PEXP_THREADS, 0, st>>>(P, n, u0, Yend, Yh, yh_e, yh_node, out);
+  k_superpose<<<grid, PEXP_THREADS, 0, st>>>(P, n, u0, Yend, Yh, yh_e, yh_node, groups, out);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();
@@ -372,6 +411,26 @@ void launch_hupdate(cudaStream_t st, int E, int rows, int m, const double* T, lo
   dim3 grid(std::min(cdiv(rows * m, PEXP_THREADS), 64), E);
   { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
   k_hupdate<<<grid, PEXP_THREADS, 0, st>>>(rows, m, T, ts_e, ldt, R, rs_e, ldr, H, hs_e, ldh, active);
+  }
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_hom_start_block(cudaStream_t st, int Eh, int mh, int groups, int P, int n, const double* Y, double* V,
+                            long long vs_e, double* beta) {
+  if (Eh == 0) return;
+  { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
+  k_hom_start_block<<<dim3(Eh, mh), PEXP_THREADS, 0, st>>>(mh, groups, P, n, Y, V, vs_e, beta);
+  }
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_hom_setup_block(cudaStream_t st, int Eh, int mh, int groups, int P, double dT, double eta,
+                            const double* beta, double* critc, int* horc, int* active) {
+  if (Eh == 0) return;
+  { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
+  k_hom_setup_block<<<cdiv(Eh, 128), 128, 0, st>>>(Eh, mh, groups, P, dT, eta, beta, critc, horc, active);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();

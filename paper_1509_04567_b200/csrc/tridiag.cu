@@ -13,6 +13,7 @@
 // accumulated during the forward pass, so no third pass is needed.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "scan.cuh"
 
 namespace pexp {
 
@@ -107,55 +108,6 @@ __global__ void k_factor(int nf, int n, int periodic, const int* opidx, const do
   if (bad) atomicExch(err, 1);
 }
 
-// ---------------------------------------------------------------- affine-map block scan
-// Map f(y) = A*y + B.  compose(first, then) = then ∘ first.
-struct Aff {
-  double A, B;
-};
-__device__ __forceinline__ Aff after(Aff first, Aff then) {
-  return {then.A * first.A, fma(then.A, first.B, then.B)};
-}
-
-// Exclusive scan over the block (ordered by `rank`, 0..255) of the per-thread maps.
-// rank = threadIdx.x (forward) or 255 - threadIdx.x (reverse, REV = true); in the reverse
-// order the lane of rank-predecessor k-o is the PHYSICAL lane +o, hence shfl_down.
-// Returns the composition of all maps of lower rank (identity for rank 0) and, through
-// `total`, the composition of all 256.
-template <bool REV>
-__device__ __forceinline__ Aff block_excl_scan(Aff v, int rank, Aff* wsm, Aff& total) {
-  const int lane = rank & 31, w = rank >> 5;
-  Aff inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    double pa = REV ? __shfl_down_sync(0xffffffffu, inc.A, o) : __shfl_up_sync(0xffffffffu, inc.A, o);
-    double pb = REV ? __shfl_down_sync(0xffffffffu, inc.B, o) : __shfl_up_sync(0xffffffffu, inc.B, o);
-    if (lane >= o) inc = after(Aff{pa, pb}, inc);
-  }
-  double ea = REV ? __shfl_down_sync(0xffffffffu, inc.A, 1) : __shfl_up_sync(0xffffffffu, inc.A, 1);
-  double eb = REV ? __shfl_down_sync(0xffffffffu, inc.B, 1) : __shfl_up_sync(0xffffffffu, inc.B, 1);
-  Aff exc = lane == 0 ? Aff{1.0, 0.0} : Aff{ea, eb};
-  __syncthreads();
-  if (lane == 31) wsm[w] = inc;
-  __syncthreads();
-  if (rank == 0) {
-    Aff acc{1.0, 0.0};
-    for (int k = 0; k < PEXP_THREADS / 32; ++k) {
-      Aff t = wsm[k];
-      wsm[k] = acc;  // exclusive prefix of warp k
-      acc = after(acc, t);
-    }
-    wsm[PEXP_THREADS / 32] = acc;
-  }
-  __syncthreads();
-  Aff pre = wsm[w];
-  total = wsm[PEXP_THREADS / 32];
-  return after(pre, exc);
-}
-
-constexpr int EPT = 8;                       // rows per thread per chunk
-constexpr int CHUNK = EPT * PEXP_THREADS;    // 2048 rows
-constexpr int SPAD = EPT + 1;                // smem row padding (bank spread)
-
 // Grid (ncols, E).  Column c of eval e: rhs at rhs + e*rs_e + (cin0+c)*n, result at
 // out + e*os_e + (cout0+c)*n (may alias rhs only if identical).  fidx[e] selects the factor.
 __global__ void __launch_bounds__(PEXP_THREADS)
@@ -169,89 +121,10 @@ k_sai_solve(int n, int periodic, const int* fidx, const double* fl, const double
   __shared__ double s1[PEXP_THREADS * SPAD];
   __shared__ Aff wsm[PEXP_THREADS / 32 + 1];
   __shared__ double red[32];
-  __shared__ double carry_s;
-  const int t = threadIdx.x;
   const size_t fo = size_t(fidx ? fidx[e] : e) * n;
-  const double *l = fl + fo, *di = fdinv + fo, *cs = fsup + fo;
-  const double* b = rhs + e * rs_e + size_t(cin0 + c) * n;
-  double* x = out + e * os_e + size_t(cout0 + c) * n;
-  const int nchunk = (n + CHUNK - 1) / CHUNK;
-  double carry = 0.0, dot = 0.0;
-  // ---- forward: y_i = b_i - l_i y_{i-1}
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const int base = ch * CHUNK;
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      int si = (i / EPT) * SPAD + (i % EPT);
-      double bv = g < n ? b[g] : 0.0;
-      s0[si] = bv;
-      s1[si] = g < n ? -l[g] : 1.0;
-      if (periodic && g < n) dot = fma(fw[fo + g], bv, dot);
-    }
-    __syncthreads();
-    Aff m{1.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
-    Aff tot;
-    Aff pre = block_excl_scan<false>(m, t, wsm, tot);
-    double y = fma(pre.A, carry, pre.B);
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      y = fma(s1[t * SPAD + k], y, s0[t * SPAD + k]);
-      s0[t * SPAD + k] = y;
-    }
-    carry = fma(tot.A, carry, tot.B);
-    __syncthreads();
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      if (g < n) x[g] = s0[(i / EPT) * SPAD + (i % EPT)];
-    }
-    __syncthreads();
-  }
-  double f = 0.0;
-  if (periodic) f = block_sum(dot, red);
-  // ---- backward: x_i = dinv_i*(y_i - msup_i*x_{i+1}) = (-dinv_i msup_i) x_{i+1} + dinv_i y_i
-  carry = 0.0;
-  const int r = PEXP_THREADS - 1 - t;  // reversed rank: highest rows first
-  for (int ch = nchunk - 1; ch >= 0; --ch) {
-    const int base = ch * CHUNK;
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      int si = (i / EPT) * SPAD + (i % EPT);
-      if (g < n) {
-        double dv = di[g];
-        s0[si] = dv * x[g];
-        s1[si] = -dv * cs[g];
-      } else {
-        s0[si] = 0.0;
-        s1[si] = 1.0;
-      }
-    }
-    __syncthreads();
-    Aff m{1.0, 0.0};
-#pragma unroll
-    for (int k = EPT - 1; k >= 0; --k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
-    Aff tot;
-    Aff pre = block_excl_scan<true>(m, r, wsm, tot);
-    double y = fma(pre.A, carry, pre.B);
-#pragma unroll
-    for (int k = EPT - 1; k >= 0; --k) {
-      y = fma(s1[t * SPAD + k], y, s0[t * SPAD + k]);
-      s0[t * SPAD + k] = y;
-    }
-    carry = fma(tot.A, carry, tot.B);
-    __syncthreads();
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      if (g < n) {
-        double v = s0[(i / EPT) * SPAD + (i % EPT)];
-        if (periodic) v = fma(-f, fz[fo + g], v);
-        x[g] = v;
-      }
-    }
-    __syncthreads();
-  }
-  (void)carry_s;
+  cta_sai_solve(n, periodic, fl + fo, fdinv + fo, fsup + fo, periodic ? fz + fo : nullptr, periodic ? fw + fo : nullptr,
+                rhs + e * rs_e + size_t(cin0 + c) * n, out + e * os_e + size_t(cout0 + c) * n, nullptr, s0, s1, wsm,
+                red);
 }
 
 // ---------------------------------------------------------------- host wrappers

@@ -89,10 +89,41 @@ k_xty_partial(int n, int rch, const double* X, long long xs_e, int x0, int nx, c
 // streams whole X columns of the chunk (coalesced 256-B loads, 4 rows per lane in flight),
 // accumulates the ny dot products per lane and reduces them with warp shuffles.  X is read
 // exactly once from HBM; Y once per chunk.
+// Deterministic fused split-K reduction: every CTA publishes its partial, the LAST CTA of the
+// evaluation (ticket counter) sums the partials in chunk order and writes D; the counter is
+// reset for the next launch.
+struct RedArgs {
+  double* D;
+  long long ds_e;
+  int ldd, row0, col0, accumulate;
+  int* cnt;  // [E] zero-initialised tickets (nullptr: separate k_reduce launch)
+};
+
+__device__ __forceinline__ void last_cta_reduce(const RedArgs& ra, const double* part, int e, int nch, int nx,
+                                                int ny) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ra.cnt + e, 1) == nch - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const size_t sz = size_t(nx) * ny;
+  const double* pe = part + size_t(e) * nch * sz;
+  for (int idx = threadIdx.x; idx < nx * ny; idx += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < nch; ++c) acc += __ldcg(pe + c * sz + idx);
+    int a = idx % nx, b = idx / nx;
+    double* d = ra.D + e * ra.ds_e + (ra.row0 + a) + size_t(ra.col0 + b) * ra.ldd;
+    *d = ra.accumulate ? *d + acc : acc;
+  }
+  if (threadIdx.x == 0) ra.cnt[e] = 0;
+}
+
 template <int NYB>
 __global__ void __launch_bounds__(PEXP_THREADS)
 k_xty_tall(int n, int rch, int rsub, const double* X, long long xs_e, int x0, int nx, const double* Y, long long ys_e,
-           int y0, int ny, double* part, const int* active) {
+           int y0, int ny, double* part, const int* active, RedArgs ra) {
   extern __shared__ double sm[];
   double* Ys = sm;                 // [ny][rsub]   current sub-chunk of Y (column-major)
   double* Ps = sm + ny * rsub;     // [nx][ny]     CTA partial
@@ -146,6 +177,7 @@ k_xty_tall(int n, int rch, int rsub, const double* X, long long xs_e, int x0, in
   __syncthreads();
   double* P = part + (size_t(e) * nch + ch) * size_t(nx) * ny;
   for (int i = threadIdx.x; i < nx * ny; i += PEXP_THREADS) P[i] = Ps[i];
+  if (ra.cnt) last_cta_reduce(ra, part, e, nch, nx, ny);
 }
 
 // D_e[row0 + a, col0 + b] (= or +=) sum_ch part[e][ch][a + b*nx]
@@ -240,8 +272,9 @@ int xty_chunks(int n, int E) {
 void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, int x0, int nx,
                 const double* Y, long long ys_e, int y0, int ny, double* part, size_t part_cap,
                 double* D, long long ds_e, int ldd, int row0, int col0, bool accumulate,
-                const int* active) {
+                const int* active, int* cnt) {
   if (E == 0 || nx == 0 || ny == 0) return;
+  RedArgs ra{D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, cnt};
   if (ny <= 32) {
     int rsub, rch, nch;
     xty_tall_plan(n, E, nx, ny, rsub, rch, nch);
@@ -252,19 +285,21 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
     if (smem > 200 * 1024) fail(1, "xty: nx*ny too large for the tall path");
     dim3 grid(nch, E);
     if (ny <= 4)
-      k_xty_tall<4><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+      k_xty_tall<4><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active, ra);
     else if (ny <= 8)
-      k_xty_tall<8><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+      k_xty_tall<8><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active, ra);
     else if (ny <= 16)
-      k_xty_tall<16><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+      k_xty_tall<16><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active, ra);
     else
-      k_xty_tall<32><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+      k_xty_tall<32><<<grid, PEXP_THREADS, smem, st>>>(n, rch, rsub, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active, ra);
     count_launch();
     PEXP_LAUNCH_CHECK();
-    dim3 g2(std::min(cdiv(nx * ny, PEXP_THREADS), 64), E);
-    k_reduce<<<g2, PEXP_THREADS, 0, st>>>(nx, ny, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, active);
-    count_launch();
-    PEXP_LAUNCH_CHECK();
+    if (!cnt) {
+      dim3 g2(std::min(cdiv(nx * ny, PEXP_THREADS), 64), E);
+      k_reduce<<<g2, PEXP_THREADS, 0, st>>>(nx, ny, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, active);
+      count_launch();
+      PEXP_LAUNCH_CHECK();
+    }
     return;
   }
   int rch = xty_chunks(n, E);

@@ -140,7 +140,7 @@ def test_linear_generic_deep_arnoldi(bc, n, nu, a):
 
 def test_linear_config2_reduced():
     p = synth.config2(n=1200, P=16, T=0.25, s=64)     # same subinterval length dT = 1/64 as C2
-    out, st = _linear(p)
+    out, st = _linear(p, k_max=384)
     ref = _oracle_linear(p)
     assert rel(out, ref) < 1e-8, st
 
