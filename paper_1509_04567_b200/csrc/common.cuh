@@ -23,11 +23,14 @@ struct Error {
       throw ::pexp::Error{3, std::string(#expr) + ": " + cudaGetErrorString(_e)};    \
   } while (0)
 
+extern bool g_sync_debug;  // PEXP_SYNC=1: synchronise after every launch (fault localisation)
 #define PEXP_LAUNCH_CHECK()                                                          \
   do {                                                                               \
     cudaError_t _e = cudaGetLastError();                                             \
+    if (_e == cudaSuccess && ::pexp::g_sync_debug) _e = cudaDeviceSynchronize();     \
     if (_e != cudaSuccess)                                                           \
-      throw ::pexp::Error{3, std::string("kernel launch: ") + cudaGetErrorString(_e)}; \
+      throw ::pexp::Error{3, std::string("kernel launch (") + __FILE__ + ":" +        \
+                                 std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)}; \
   } while (0)
 
 inline void fail(int code, const std::string& m) { throw Error{code, m}; }

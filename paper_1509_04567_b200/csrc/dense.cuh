@@ -6,6 +6,32 @@
 
 namespace pexp {
 
+// A group of CTAs cooperating on one evaluation: a thread-block cluster (rank, size), or a
+// single CTA (size 1).  Operands live in global memory (L2), so a cluster barrier with
+// release/acquire semantics (plus a device-scope fence) orders the phases.
+struct Grp {
+  int rank, size;
+};
+
+__device__ inline Grp this_grp() {
+  unsigned r, s;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(s));
+  return Grp{int(r), int(s)};
+}
+
+__device__ inline void grp_sync(const Grp& g) {
+  if (g.size == 1) {
+    __syncthreads();
+    return;
+  }
+  __threadfence();
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+constexpr Grp kSolo{0, 1};
+
 // C = alpha*A*B + beta*C ; A: M x K (lda), B: K x N (ldb), C: M x N (ldc); C must not alias.
 // Tiles TM x TM (TM = 128 or 64) with K-steps of 16 staged in shared memory; 256 threads as a
 // 16 x 16 grid, each owning (TM/16)^2 outputs strided by 16 (conflict-free shared reads, 4 FMA
@@ -19,14 +45,16 @@ __device__ inline double* gemm_smem() {
 
 template <int TM>
 __device__ inline void cta_gemm_t(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
-                                  int ldb, double beta, double* C, int ldc) {
+                                  int ldb, double beta, double* C, int ldc, Grp g) {
   constexpr int R = TM / 16;          // outputs per thread per dimension
   constexpr int LA = TM * 16 / 256;   // A-tile elements loaded per thread
   double (*As)[TM + 1] = reinterpret_cast<double (*)[TM + 1]>(gemm_smem());
   double (*Bs)[TM + 1] = reinterpret_cast<double (*)[TM + 1]>(gemm_smem() + 16 * (TM + 1));
   const int t = threadIdx.x, tx = t % 16, ty = t / 16;
-  for (int i0 = 0; i0 < M; i0 += TM)
-    for (int j0 = 0; j0 < N; j0 += TM) {
+  const int nti = (M + TM - 1) / TM, ntj = (N + TM - 1) / TM;
+  for (int tile = g.rank; tile < nti * ntj; tile += g.size) {
+    const int i0 = (tile % nti) * TM, j0 = (tile / nti) * TM;
+    {
       double acc[R][R];
 #pragma unroll
       for (int a = 0; a < R; ++a)
@@ -82,43 +110,44 @@ __device__ inline void cta_gemm_t(int M, int N, int K, double alpha, const doubl
           }
         }
     }
-  __syncthreads();
+  }
+  grp_sync(g);
 }
 
 __device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
-                                int ldb, double beta, double* C, int ldc) {
+                                int ldb, double beta, double* C, int ldc, Grp g = kSolo) {
   if (M > 64 && N > 64)
-    cta_gemm_t<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    cta_gemm_t<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
   else
-    cta_gemm_t<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    cta_gemm_t<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
 }
 
 // Y = alpha*X + beta*Y (+ gamma*I) on N x N
 __device__ inline void cta_axpby(int N, double alpha, const double* X, int ldx, double beta,
-                                 double* Y, int ldy, double diag_add = 0.0) {
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+                                 double* Y, int ldy, double diag_add = 0.0, Grp g = kSolo) {
+  for (int idx = threadIdx.x + g.rank * blockDim.x; idx < N * N; idx += blockDim.x * g.size) {
     int i = idx % N, j = idx / N;
     double v = alpha * X[i + size_t(j) * ldx] + (beta != 0.0 ? beta * Y[i + size_t(j) * ldy] : 0.0);
     if (i == j) v += diag_add;
     Y[i + size_t(j) * ldy] = v;
   }
-  __syncthreads();
+  grp_sync(g);
 }
 
-__device__ inline void cta_copy(int M, int N, const double* X, int ldx, double* Y, int ldy) {
-  for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) {
+__device__ inline void cta_copy(int M, int N, const double* X, int ldx, double* Y, int ldy, Grp g = kSolo) {
+  for (int idx = threadIdx.x + g.rank * blockDim.x; idx < M * N; idx += blockDim.x * g.size) {
     int i = idx % M, j = idx / M;
     Y[i + size_t(j) * ldy] = X[i + size_t(j) * ldx];
   }
-  __syncthreads();
+  grp_sync(g);
 }
 
-__device__ inline void cta_identity(int N, double* Y, int ldy, double d = 1.0) {
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+__device__ inline void cta_identity(int N, double* Y, int ldy, double d = 1.0, Grp g = kSolo) {
+  for (int idx = threadIdx.x + g.rank * blockDim.x; idx < N * N; idx += blockDim.x * g.size) {
     int i = idx % N, j = idx / N;
     Y[i + size_t(j) * ldy] = (i == j) ? d : 0.0;
   }
-  __syncthreads();
+  grp_sync(g);
 }
 
 // max column abs-sum
@@ -134,7 +163,7 @@ __device__ inline double cta_norm1(int N, const double* A, int lda, double* red)
 
 // Blocked right-looking LU with partial pivoting, in place.  piv[k] = row swapped with k.
 // Returns false if a zero pivot was met.
-__device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red) {
+__device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red, Grp g = kSolo) {
   __shared__ int s_ip;
   __shared__ double s_pv;
   __shared__ int s_bad;
@@ -143,7 +172,8 @@ __device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red) 
   constexpr int NBL = 32;
   for (int k0 = 0; k0 < N; k0 += NBL) {
     const int kb = min(NBL, N - k0);
-    // --- unblocked panel factorisation of columns k0..k0+kb-1 (rows k0..N-1)
+    // --- unblocked panel factorisation of columns k0..k0+kb-1 (rows k0..N-1), rank 0 only
+    if (g.rank == 0)
     for (int k = k0; k < k0 + kb; ++k) {
       // pivot search
       double best = -1.0;
@@ -197,28 +227,41 @@ __device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red) 
       }
       __syncthreads();
     }
+    grp_sync(g);
     const int rest = N - (k0 + kb);
     if (rest > 0) {
-      // U12 = L11^{-1} A12 (unit lower), one thread per column
-      for (int j = k0 + kb + threadIdx.x; j < N; j += blockDim.x)
+      // U12 = L11^{-1} A12 (unit lower), one thread per column (columns split over the group)
+      for (int j = k0 + kb + threadIdx.x + g.rank * blockDim.x; j < N; j += blockDim.x * g.size)
         for (int i = k0; i < k0 + kb; ++i) {
           double s = A[i + size_t(j) * lda];
           for (int p = k0; p < i; ++p) s = fma(-A[i + size_t(p) * lda], A[p + size_t(j) * lda], s);
           A[i + size_t(j) * lda] = s;
         }
-      __syncthreads();
+      grp_sync(g);
       // A22 -= L21 U12
       cta_gemm(rest, rest, kb, -1.0, A + (k0 + kb) + size_t(k0) * lda, lda,
-               A + k0 + size_t(k0 + kb) * lda, lda, 1.0, A + (k0 + kb) + size_t(k0 + kb) * lda, lda);
+               A + k0 + size_t(k0 + kb) * lda, lda, 1.0, A + (k0 + kb) + size_t(k0 + kb) * lda, lda, g);
     }
   }
-  __syncthreads();
+  grp_sync(g);
   return s_bad == 0;
 }
 
 // Solve (LU) X = P B in place on B (N x nrhs), blocked; uses cta_gemm for off-diagonal blocks.
-__device__ inline void cta_lu_solve(int N, const double* LU, int lda, const int* piv, double* B,
-                                    int ldb, int nrhs) {
+__device__ inline void cta_lu_solve_local(int N, const double* LU, int lda, const int* piv, double* B,
+                                          int ldb, int nrhs);
+
+// RHS columns are split into contiguous ranges, one per CTA of the group
+__device__ inline void cta_lu_solve(int N, const double* LU, int lda, const int* piv, double* B, int ldb, int nrhs,
+                                    Grp g = kSolo) {
+  const int per = (nrhs + g.size - 1) / g.size;
+  const int c0 = g.rank * per, c1 = min(nrhs, c0 + per);
+  if (c1 > c0) cta_lu_solve_local(N, LU, lda, piv, B + size_t(c0) * ldb, ldb, c1 - c0);
+  grp_sync(g);
+}
+
+__device__ inline void cta_lu_solve_local(int N, const double* LU, int lda, const int* piv, double* B,
+                                          int ldb, int nrhs) {
   // row interchanges
   for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
     for (int k = 0; k < N; ++k) {
@@ -264,7 +307,7 @@ __device__ inline void cta_lu_solve(int N, const double* LU, int lda, const int*
 // Pade-13 scaling-and-squaring exponential (Higham 2005), in place on X (N x N, ld = ldx).
 // work: 7 matrices of ld x N.  Returns the number of squarings.
 __device__ inline int cta_expm_pade13(int N, double* X, int ldx, double* work, int ldw, int* piv,
-                                      double* red) {
+                                      double* red, Grp g = kSolo) {
   const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                         1187353796428800.0,  129060195264000.0,   10559470521600.0,
                         670442572800.0,      33522128640.0,       1323241920.0,
@@ -277,46 +320,47 @@ __device__ inline int cta_expm_pade13(int N, double* X, int ldx, double* work, i
   double nrm = cta_norm1(N, X, ldx, red);
   int s = 0;
   if (nrm > theta13) s = max(0, (int)ceil(log2(nrm / theta13)));
-  if (s > 0) cta_axpby(N, ldexp(1.0, -s), X, ldx, 0.0, X, ldx);
-  cta_gemm(N, N, N, 1.0, X, ldx, X, ldx, 0.0, A2, ldw);
-  cta_gemm(N, N, N, 1.0, A2, ldw, A2, ldw, 0.0, A4, ldw);
-  cta_gemm(N, N, N, 1.0, A4, ldw, A2, ldw, 0.0, A6, ldw);
+  grp_sync(g);  // every CTA has read X before it is rescaled
+  if (s > 0) cta_axpby(N, ldexp(1.0, -s), X, ldx, 0.0, X, ldx, 0.0, g);
+  cta_gemm(N, N, N, 1.0, X, ldx, X, ldx, 0.0, A2, ldw, g);
+  cta_gemm(N, N, N, 1.0, A2, ldw, A2, ldw, 0.0, A4, ldw, g);
+  cta_gemm(N, N, N, 1.0, A4, ldw, A2, ldw, 0.0, A6, ldw, g);
   // U = X [A6 (b13 A6 + b11 A4 + b9 A2) + b7 A6 + b5 A4 + b3 A2 + b1 I]
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+  for (int idx = threadIdx.x + g.rank * blockDim.x; idx < N * N; idx += blockDim.x * g.size) {
     int i = idx % N, j = idx / N;
     size_t o = i + size_t(j) * ldw;
     T1[o] = b[13] * A6[o] + b[11] * A4[o] + b[9] * A2[o];
     T2[o] = b[7] * A6[o] + b[5] * A4[o] + b[3] * A2[o] + (i == j ? b[1] : 0.0);
   }
-  __syncthreads();
-  cta_gemm(N, N, N, 1.0, A6, ldw, T1, ldw, 1.0, T2, ldw);
-  cta_gemm(N, N, N, 1.0, X, ldx, T2, ldw, 0.0, U, ldw);
+  grp_sync(g);
+  cta_gemm(N, N, N, 1.0, A6, ldw, T1, ldw, 1.0, T2, ldw, g);
+  cta_gemm(N, N, N, 1.0, X, ldx, T2, ldw, 0.0, U, ldw, g);
   // V = A6 (b12 A6 + b10 A4 + b8 A2) + b6 A6 + b4 A4 + b2 A2 + b0 I
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+  for (int idx = threadIdx.x + g.rank * blockDim.x; idx < N * N; idx += blockDim.x * g.size) {
     int i = idx % N, j = idx / N;
     size_t o = i + size_t(j) * ldw;
     T1[o] = b[12] * A6[o] + b[10] * A4[o] + b[8] * A2[o];
     V[o] = b[6] * A6[o] + b[4] * A4[o] + b[2] * A2[o] + (i == j ? b[0] : 0.0);
   }
-  __syncthreads();
-  cta_gemm(N, N, N, 1.0, A6, ldw, T1, ldw, 1.0, V, ldw);
+  grp_sync(g);
+  cta_gemm(N, N, N, 1.0, A6, ldw, T1, ldw, 1.0, V, ldw, g);
   // (V - U) R = (V + U)
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+  for (int idx = threadIdx.x + g.rank * blockDim.x; idx < N * N; idx += blockDim.x * g.size) {
     int i = idx % N, j = idx / N;
     size_t o = i + size_t(j) * ldw;
     T1[o] = V[o] - U[o];
     T2[o] = V[o] + U[o];
   }
-  __syncthreads();
-  cta_lu(N, T1, ldw, piv, red);
-  cta_lu_solve(N, T1, ldw, piv, T2, ldw, N);
+  grp_sync(g);
+  cta_lu(N, T1, ldw, piv, red, g);
+  cta_lu_solve(N, T1, ldw, piv, T2, ldw, N, g);
   // squarings, ping-pong T2 <-> T1
   double *cur = T2, *nxt = T1;
   for (int q = 0; q < s; ++q) {
-    cta_gemm(N, N, N, 1.0, cur, ldw, cur, ldw, 0.0, nxt, ldw);
+    cta_gemm(N, N, N, 1.0, cur, ldw, cur, ldw, 0.0, nxt, ldw, g);
     double* tmp = cur; cur = nxt; nxt = tmp;
   }
-  cta_copy(N, N, cur, ldw, X, ldx);
+  cta_copy(N, N, cur, ldw, X, ldx, g);
   return s;
 }
 

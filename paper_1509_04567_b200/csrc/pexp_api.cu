@@ -17,6 +17,7 @@
 namespace pexp {
 thread_local long g_launches = 0;
 bool g_prof_on = false;
+bool g_sync_debug = getenv("PEXP_SYNC") != nullptr;
 std::vector<ProfRec> g_prof;
 
 // ---------------------------------------------------------------- helper kernels
@@ -586,7 +587,10 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   alloc_ebk(ar, L.B, E, n, o.kcap, s, 2, s, true, L.S.R);
   if (P > 1) {
     const int mh = std::min(16, P - 1), G = cdiv(P - 1, mh), Eg = Bt * G;
-    alloc_ebk(ar, L.Bh, Eg, n, o.kcap, mh, P, s, false, nullptr);
+    // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
+    // 16 legs -> 288 columns); give it at least 24 block steps
+    const int kcap_h = std::min(KSMALL_MAX - 64, std::max(o.kcap, 24 * mh));
+    alloc_ebk(ar, L.Bh, Eg, n, kcap_h, mh, P, s, false, nullptr);
     L.Bh.groups = G;
     L.Yh = ar.take<double>(size_t(Eg) * P * n);
   } else {

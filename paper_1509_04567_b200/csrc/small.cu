@@ -22,6 +22,32 @@ constexpr int MAXS = 64;
 double g_piv_tol = getenv("PEXP_PIVTOL") ? atof(getenv("PEXP_PIVTOL")) : 1e-14;  // developer override
 constexpr size_t SM2 = 2 * MAXS * (MAXS + 1) * sizeof(double);  // two padded 64x64 tiles
 
+// Cluster size so that (evaluations x cluster) fills the 148 SMs (portable maximum 8).
+static int cluster_size_for(int E) {
+  static const int force = getenv("PEXP_CLUSTER") ? atoi(getenv("PEXP_CLUSTER")) : 0;  // developer override
+  if (force > 0) return force;
+  int cs = 1;
+  while (cs < 8 && E * cs * 2 <= 148) cs *= 2;
+  return cs;
+}
+
+template <class Kern, class... Args>
+static void launch_clustered(Kern kern, int nclusters, int cs, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nclusters * cs);
+  cfg.blockDim = dim3(PEXP_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PEXP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 __device__ inline void jacobi_pair(int Ne, int r, int k, int& p, int& q) {
   if (k == 0) {
     p = r;
@@ -57,6 +83,7 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
   __shared__ int perm[MAXS];
   __shared__ double red[32];
   double* M = Msel + size_t(e) * s * s;
+
   if (active && !active[e]) {
     for (int i = threadIdx.x; i < s * s; i += blockDim.x) M[i] = 0.0;
     return;
@@ -104,7 +131,9 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
       }
       __syncthreads();
     }
-    if (!s_rot) break;
+    const int rotated = s_rot;
+    __syncthreads();  // every thread has read s_rot before thread 0 resets it
+    if (!rotated) break;
   }
   (void)red;
   if (threadIdx.x == 0) {
@@ -499,7 +528,8 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
   extern __shared__ double zsm[];  // 2 * KSMALL_MAX doubles
   double* z = zsm;
   double* zn = zsm + KSMALL_MAX;
-  const int slot = blockIdx.x;
+  const Grp g = this_grp();
+  const int slot = blockIdx.x / g.size, nslot = gridDim.x / g.size;
   double* S0 = a.work + slot * a.work_slot;
   const int ld = a.Nmax;
   const size_t MM = size_t(ld) * ld;
@@ -508,7 +538,7 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
   double* WK = S2 + MM;
   int* piv = a.iwork + slot * a.iwork_slot;
   const int K = a.K, m = a.m;
-  for (int e = blockIdx.x; e < a.E; e += gridDim.x) {
+  for (int e = slot; e < a.E; e += nslot) {
     if (a.active && !a.active[e]) continue;
     const double* He = a.H + e * a.hs_e;
     const int* lv = a.live + e * a.ls_e;
@@ -532,16 +562,16 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     const int forced = a.kind == 0;
     const int Nn = Kp + (forced ? 4 * m : 0);
     // Hs -> S0, Hinv -> S1
-    for (int t = threadIdx.x; t < Kp * Kp; t += blockDim.x) {
+    for (int t = threadIdx.x + g.rank * blockDim.x; t < Kp * Kp; t += blockDim.x * g.size) {
       int i = t % Kp, j = t / Kp;
       S0[i + size_t(j) * ld] = He[idx[i] + size_t(idx[j]) * a.ldh];
     }
-    __syncthreads();
-    cta_identity(Kp, S1, ld);
-    cta_lu(Kp, S0, ld, piv, red);
-    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp);
+    grp_sync(g);
+    cta_identity(Kp, S1, ld, 1.0, g);
+    cta_lu(Kp, S0, ld, piv, red, g);
+    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g);
     // augmented matrix in S2
-    for (int t = threadIdx.x; t < Nn * Nn; t += blockDim.x) {
+    for (int t = threadIdx.x + g.rank * blockDim.x; t < Nn * Nn; t += blockDim.x * g.size) {
       int i = t % Nn, j = t / Nn;
       double v = 0.0;
       if (i < Kp && j < Kp) v = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
@@ -549,8 +579,9 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
       else if (forced && i >= Kp && j >= Kp && j - i == m && i < Kp + 3 * m) v = 1.0;
       S2[i + size_t(j) * ld] = v;
     }
-    __syncthreads();
-    cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red);
+    grp_sync(g);
+    cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red, g);
+    if (g.rank == 0) {  // chaining and residuals: rank 0 of the cluster
     // chain
     const int np = a.npieces ? a.npieces[e] : a.npieces_const;
     for (int r = threadIdx.x; r < Kp; r += blockDim.x) z[r] = (!forced && r == 0) ? a.beta[e] : 0.0;
@@ -619,7 +650,8 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
       a.conv[e] = cv;
       if (cv && a.kfin) a.kfin[e] = K;
     }
-    __syncthreads();
+    }  // rank 0
+    grp_sync(g);
   }
 }
 
@@ -637,7 +669,8 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
   __shared__ int s_K, s_mt, s_ml;
   __shared__ double red[32];
   __shared__ double xs[16 * 16], ts[16 * 16];  // (ml, mt <= m <= 16) x m
-  const int slot = blockIdx.x;
+  const Grp g = this_grp();
+  const int slot = blockIdx.x / g.size, nslot = gridDim.x / g.size;
   double* S0 = a.work + slot * a.work_slot;
   const int ld = a.Nmax;
   const size_t MM = size_t(ld) * ld;
@@ -646,7 +679,7 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
   double* WK = S2 + MM;
   int* piv = a.iwork + slot * a.iwork_slot;
   const int K = a.K, m = a.m;
-  for (int e = blockIdx.x; e < a.E; e += gridDim.x) {
+  for (int e = slot; e < a.E; e += nslot) {
     if (a.active && !a.active[e]) continue;
     const double* He = a.H + e * a.hs_e;
     const int* lv = a.live + e * a.ls_e;
@@ -667,31 +700,33 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
     __syncthreads();
     const int Kp = s_K, mt = s_mt, ml = s_ml;
     const double gam = a.gam[e];
-    for (int t = threadIdx.x; t < Kp * Kp; t += blockDim.x) {
+    for (int t = threadIdx.x + g.rank * blockDim.x; t < Kp * Kp; t += blockDim.x * g.size) {
       int i = t % Kp, j = t / Kp;
       S0[i + size_t(j) * ld] = He[idx[i] + size_t(idx[j]) * a.ldh];
     }
-    __syncthreads();
-    cta_identity(Kp, S1, ld);
-    cta_lu(Kp, S0, ld, piv, red);
-    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp);
-    for (int t = threadIdx.x; t < Kp * Kp; t += blockDim.x) {
+    grp_sync(g);
+    cta_identity(Kp, S1, ld, 1.0, g);
+    cta_lu(Kp, S0, ld, piv, red, g);
+    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g);
+    for (int t = threadIdx.x + g.rank * blockDim.x; t < Kp * Kp; t += blockDim.x * g.size) {
       int i = t % Kp, j = t / Kp;
       S2[i + size_t(j) * ld] = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
     }
-    __syncthreads();
-    cta_expm_pade13(Kp, S2, ld, WK, ld, piv, red);
+    grp_sync(g);
+    cta_expm_pade13(Kp, S2, ld, WK, ld, piv, red, g);
     // Z (Kp x m) and Zn in the (now free) expm workspace
     double* Z = WK;
     double* Zn = WK + size_t(ld) * m;
     const double* R0 = a.R0 + size_t(e) * m * m;
-    for (int t = threadIdx.x; t < Kp * m; t += blockDim.x) {
-      int r = t % Kp, c = t / Kp;
-      Z[r + size_t(c) * ld] = idx[r] < m ? R0[idx[r] + c * m] : 0.0;
-    }
     double* Ze = a.Z + e * a.zs_e;
-    for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
-    __syncthreads();
+    if (g.rank == 0) {
+      for (int t = threadIdx.x; t < Kp * m; t += blockDim.x) {
+        int r = t % Kp, c = t / Kp;
+        Z[r + size_t(c) * ld] = idx[r] < m ? R0[idx[r] + c * m] : 0.0;
+      }
+      for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
+    }
+    grp_sync(g);
     const int j0 = (e % a.groups) * m;
     const double* cc = a.critc + size_t(e) * m;
     const int* hc = a.horc + size_t(e) * m;
@@ -699,8 +734,9 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
     for (int c = 0; c < m; ++c) qmax = max(qmax, hc[c]);
     double worst = 0.0;
     for (int q = 1; q <= qmax; ++q) {
-      cta_gemm(Kp, m, Kp, 1.0, S2, ld, Z, ld, 0.0, Zn, ld);
+      cta_gemm(Kp, m, Kp, 1.0, S2, ld, Z, ld, 0.0, Zn, ld, g);
       double* tmp = Z; Z = Zn; Zn = tmp;
+      if (g.rank != 0) continue;  // residuals and accumulation on rank 0
       if (mt > 0) {
         for (int t = threadIdx.x; t < ml * m; t += blockDim.x) {
           int cidx = t % ml, c = t / ml;
@@ -733,13 +769,13 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
         __syncthreads();
       }
     }
-    if (threadIdx.x == 0) {
+    if (g.rank == 0 && threadIdx.x == 0) {
       a.res[e] = worst;
       int cv = (mt == 0) || (worst <= 1.0);
       a.conv[e] = cv;
       if (cv && a.kfin) a.kfin[e] = K;
     }
-    __syncthreads();
+    grp_sync(g);
   }
 }
 
@@ -747,7 +783,8 @@ void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
   if (a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
   if (a.m > 16) fail(1, "grouped legs: at most 16 legs per group");
   ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * a.K * a.K * a.K));
-  k_small_hom<<<std::min(a.E, nslots), PEXP_THREADS, 0, st>>>(a);
+  const int ncl = std::min(a.E, nslots);
+  launch_clustered(k_small_hom, ncl, cluster_size_for(ncl), 0, st, a);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }
@@ -756,13 +793,14 @@ void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
 __global__ void __launch_bounds__(PEXP_THREADS)
 k_expm_batched(int E, int N, const double* A, double* X, double* work, long long work_slot, int* iwork) {
   __shared__ double red[32];
-  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+  const Grp g = this_grp();
+  const int slot = blockIdx.x / g.size, nslot = gridDim.x / g.size;
+  for (int e = slot; e < E; e += nslot) {
     double* Xe = X + size_t(e) * N * N;
     const double* Ae = A + size_t(e) * N * N;
-    for (int t = threadIdx.x; t < N * N; t += blockDim.x) Xe[t] = Ae[t];
-    __syncthreads();
-    cta_expm_pade13(N, Xe, N, work + blockIdx.x * work_slot, N, iwork + blockIdx.x * N, red);
-    __syncthreads();
+    for (int t = threadIdx.x + g.rank * blockDim.x; t < N * N; t += blockDim.x * g.size) Xe[t] = Ae[t];
+    grp_sync(g);
+    cta_expm_pade13(N, Xe, N, work + slot * work_slot, N, iwork + slot * N, red, g);
   }
 }
 
@@ -820,7 +858,8 @@ void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots) {
   {
   const double N = a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
   ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
-  k_small_problem<<<std::min(a.E, nslots), PEXP_THREADS, smem, st>>>(a);
+  const int ncl = std::min(a.E, nslots);
+  launch_clustered(k_small_problem, ncl, cluster_size_for(ncl), smem, st, a);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();
@@ -828,7 +867,8 @@ void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots) {
 
 void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
                          long long work_slot, int* iwork, int nslots) {
-  k_expm_batched<<<std::min(E, nslots), PEXP_THREADS, 0, st>>>(E, N, A, X, work, work_slot, iwork);
+  const int ncl = std::min(E, nslots);
+  launch_clustered(k_expm_batched, ncl, cluster_size_for(ncl), 0, st, E, N, A, X, work, work_slot, iwork);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }

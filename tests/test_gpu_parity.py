@@ -153,6 +153,18 @@ def test_linear_config4_subset():
         assert rel(out[b], ref[b]) < 1e-8, (b, st)
 
 
+def test_linear_config4_full_batch_sampled():
+    """C4 at its full size (512 problems, one batched call, the bench's k_max); the oracle
+    recomputes sampled problems, which are bit-identical rows of the full batch (synth streams)."""
+    p = synth.config4()
+    out, st = _linear(p, k_max=96)
+    assert np.all(np.isfinite(out))
+    for b in (0, 257, 511):
+        q = synth.config4(indices=[b])
+        ref = _oracle_linear(q)
+        assert rel(out[b], ref[0]) < 1e-8, (b, st)
+
+
 def test_linear_P1_and_unforced_and_zero():
     n = 300
     x = synth.grid_x(n, "periodic")
