@@ -66,11 +66,17 @@ typedef struct {
   int32_t node_rule;      /* 0 = uniform incl. endpoints (only value supported)         */
   double svd_tau_factor;  /* truncation tau_svd = factor*tol relative to sigma_1 (0.01)  */
   double stop_factor;     /* Krylov stop eta = factor*tol (default 0.1; DESIGN.md §3 #6)  */
-  int32_t restart_blocks; /* paper restarts every 20 blocks    */
-  int32_t k_max;          /* Krylov column capacity per evaluation (default 256)         */
+  int32_t restart_blocks; /* restart a Krylov cycle after this many block steps (P:451:
+                             "restarted every 20 iterations"); 0 = default 20; < 0 = only
+                             when the basis capacity basis_cols is full.  Exact nested
+                             restart, DESIGN.md §3 #5                                       */
+  int32_t k_max;          /* total Krylov dimension per evaluation over all restart
+                             cycles (default 256; k_max + 4 s <= 1024)                     */
   void* stream;           /* cudaStream_t; NULL = legacy default stream                  */
   int32_t stop_rule;      /* 0 = shift-and-invert residual ||(I-gamma A)^{-1} r(t)|| (default),
                              1 = true residual ||r(t)|| = ||A y + U p - y'|| (DESIGN.md §3 #6) */
+  int32_t basis_cols;     /* basis columns kept per evaluation in one cycle (device memory:
+                             8 n basis_cols bytes per evaluation); 0 = k_max               */
 } pexp_options;
 
 /* Per-solve statistics (host memory, caller-owned). */

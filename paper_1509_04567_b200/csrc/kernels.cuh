@@ -55,6 +55,19 @@ struct SPArgs {
   const double* critc;           // [E][m] per-leg residual targets
   const int* horc;               // [E][m] per-leg horizons in steps of h (0: unused column)
   int groups;                    // legs of eval e start at j0 = (e % groups) * m
+  // exact nested restart (kinds 0/1; DESIGN.md §3 #5).  Completed cycles form the block
+  // lower-bidiagonal matrix NA (D x D, compressed coordinates, ld na_ld): diagonal blocks
+  // A_hat_c, coupling CPL_c = R_{c+1} TX_c from cycle c into block 0 of cycle c+1.
+  double* NA;                    // [E] na_ld x na_ld (nullptr: no restart support)
+  int na_ld;
+  long long nas_e;
+  const int* Dn;                 // [E] nested dimension D
+  const int* Kl;                 // [E] compressed width of the last completed cycle
+  const double* CPL;             // [E] m x kcap (ld m): coupling rows into the current cycle
+  long long cpls_e;
+  double* TX;                    // [E] m x kcap (ld m): (1/gamma) H_tail X (written at a restart check)
+  int* kplast;                   // [E] compressed width of the current cycle at this check
+  int restart_write;             // 1: this check closes a cycle (append to NA, write TX)
 };
 
 // Arguments of the fused Arnoldi step (arnoldi.cu), one CTA per evaluation.
@@ -117,7 +130,10 @@ void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, 
                         const double* sig, const double* Cs, const int* m, double* Msel, double* Cfin, int* fill);
 void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, const double* Cfin, double h,
                    double eta, double* coef, double* crit);
-void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots);
+void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax = 0);
+void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double* R, const double* TX, double* CPL,
+                           int* Dn, int* Kl, const int* kplast, double* H, long long hs_e, int* live,
+                           const int* active);
 void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots);
 void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
                          long long work_slot, int* iwork, int nslots);

@@ -61,7 +61,7 @@ static void h2d(cudaStream_t st, T* dst, const std::vector<T>& v) {
 struct Opts {
   int s;
   double tau_f, eta_f;
-  int restart_blocks, kcap, stop_rule;
+  int restart_blocks, kcap, stop_rule, kcyc;
   cudaStream_t st;
 };
 
@@ -70,8 +70,9 @@ static Opts norm_opts(const pexp_options& o) {
   r.s = o.s > 0 ? o.s : 32;
   r.tau_f = o.svd_tau_factor > 0 ? o.svd_tau_factor : 0.01;
   r.eta_f = o.stop_factor > 0 ? o.stop_factor : 0.1;
-  r.restart_blocks = o.restart_blocks > 0 ? o.restart_blocks : 20;
+  r.restart_blocks = o.restart_blocks > 0 ? o.restart_blocks : (o.restart_blocks < 0 ? 0 : 20);
   r.kcap = o.k_max > 0 ? o.k_max : 256;
+  r.kcyc = o.basis_cols > 0 ? std::min(o.basis_cols, r.kcap) : r.kcap;
   r.st = (cudaStream_t)o.stream;
   r.stop_rule = o.stop_rule;
   return r;
@@ -79,7 +80,7 @@ static Opts norm_opts(const pexp_options& o) {
 
 // ---------------------------------------------------------------- EBK buffers
 struct EbkBufs {
-  int E = 0, n = 0, kcap = 0, mcap = 0, nout = 0, s = 0, groups = 1;
+  int E = 0, n = 0, kcap = 0, ktot = 0, mcap = 0, nout = 0, s = 0, groups = 1;
   long long vs_e = 0, hs_e = 0, zs_e = 0;
   double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p, *R0, *critc;
   int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc;
@@ -89,11 +90,16 @@ struct EbkBufs {
   int* iwork;
   int nslots, Nmax;
   long long work_slot, iwork_slot;
+  // exact nested restart (nullptr when the run cannot restart)
+  double *NA = nullptr, *CPL = nullptr, *TX = nullptr;
+  int *Dn = nullptr, *Kl = nullptr, *kplast = nullptr;
 };
 
-static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, int nout, int s, bool forced,
-                      double* Wt_shared) {
-  B.E = E; B.n = n; B.kcap = kcap; B.mcap = mcap; B.nout = nout; B.s = s;
+// kcap: basis columns per evaluation and cycle; ktot: total Krylov dimension over all cycles
+// (ktot > kcap or restart_blocks > 0 allocates the nested-restart state).
+static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int ktot, int mcap, int nout, int s,
+                      bool forced, double* Wt_shared, bool restartable) {
+  B.E = E; B.n = n; B.kcap = kcap; B.ktot = ktot; B.mcap = mcap; B.nout = nout; B.s = s;
   B.vs_e = (long long)kcap * n;
   B.hs_e = (long long)kcap * kcap;
   B.zs_e = (long long)nout * kcap;
@@ -135,12 +141,21 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int mcap, i
   size_t tall = (size_t(E) + 2 * 148 * 6) * size_t(std::max(kcap, s)) * nyt;
   B.part_cap = std::max(B.part_cap, tall);
   B.part = ar.take<double>(B.part_cap);
-  B.nslots = std::min(E, 512);
-  B.Nmax = kcap + (forced ? 4 * mcap : 0);
+  B.Nmax = ktot + (forced ? 4 * mcap : 0);
   B.work_slot = 10LL * B.Nmax * B.Nmax;
   B.iwork_slot = B.Nmax;
+  // one workspace slot per resident cluster; large projected problems get one per SM
+  B.nslots = std::min(E, B.Nmax > 512 ? 148 : 512);
   B.work = ar.take<double>(size_t(B.nslots) * B.work_slot);
   B.iwork = ar.take<int>(size_t(B.nslots) * B.iwork_slot);
+  if (restartable) {
+    B.NA = ar.take<double>(size_t(E) * ktot * ktot);
+    B.CPL = ar.take<double>(size_t(E) * mcap * kcap);
+    B.TX = ar.take<double>(size_t(E) * mcap * kcap);
+    B.Dn = ar.take<int>(E);
+    B.Kl = ar.take<int>(E);
+    B.kplast = ar.take<int>(E);
+  }
 }
 
 // Pivoted deflating Cholesky-QR of the m columns of V at column offset c0 (in place):
@@ -184,16 +199,27 @@ static void inblock_qr(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0,
 }
 
 struct RunInfo {
-  int max_k = 0;
+  int max_k = 0;     // largest basis width of a cycle (columns of V to combine)
+  int max_ktot = 0;  // largest total Krylov dimension over the cycles
+  int restarts = 0;
   int unconverged = 0;
   double worst_res_ratio = 0.0;
+};
+
+// Where a restart accumulates the outputs of a closed cycle: Y[e*ys_e + j*n] += V_c z_c at
+// output o0 + j, j < no.  The caller's final combine then adds (beta = 1) when restarts > 0.
+struct Accum {
+  double* Y = nullptr;
+  long long ys_e = 0;
+  int o0 = 0, no = 0;
 };
 
 // SaI block Arnoldi with BCGS2 + deflating CholQR2, projected problem checks on a geometric
 // schedule.  Preconditions: V block 0 (m columns) orthonormal; active, gam, fidx, opidx set;
 // forced: coef and crit set; homogeneous: beta, crit, npieces set.
 static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops& O, bool periodic, int m,
-                       int kind, double h, int npieces_const, int out_stride, int nout, int stop_rule) {
+                       int kind, double h, int npieces_const, int out_stride, int nout, int stop_rule,
+                       Accum acc = Accum{}, int restart_blocks = 0) {
   RunInfo info;
   const int E = B.E, n = B.n, kcap = B.kcap;
   if (E == 0) return info;
@@ -229,24 +255,35 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   a.work = B.work; a.work_slot = B.work_slot; a.iwork = B.iwork; a.iwork_slot = B.iwork_slot; a.Nmax = B.Nmax;
   a.stop_rule = stop_rule;
   a.R0 = B.R0; a.critc = B.critc; a.horc = B.horc; a.groups = std::max(1, B.groups);
+  const bool can_restart = kind != 2 && acc.Y != nullptr && B.NA != nullptr;
+  if (can_restart) {
+    a.NA = B.NA; a.na_ld = B.ktot; a.nas_e = (long long)B.ktot * B.ktot;
+    a.Dn = B.Dn; a.Kl = B.Kl; a.CPL = B.CPL; a.cpls_e = (long long)m * kcap;
+    a.TX = B.TX; a.kplast = B.kplast;
+    launch_fill_i32(st, B.Dn, E, 0);
+    launch_fill_i32(st, B.Kl, E, 0);
+    launch_fill_f64(st, B.NA, size_t(E) * B.ktot * B.ktot, 0.0);  // blocks above/below the bidiagonal
+  }
+  int Koff = 0;  // columns (uncompressed) of the closed cycles
   int remaining = E;
   std::vector<double> prevq(E, -1.0), curq(E, -1.0);
   std::vector<int> prevK(E, -1);
   std::vector<double> hres(E), hcrit(E);
   std::vector<int> hact(E);
   int predicted_next = -1;
-  auto do_check = [&](int K) {
+  auto do_check = [&](int K, bool closing) {
     if (stop_rule == 1) {  // true residual: tail Gram of Wt = (I - gamma A) V[:, K:K+m]
       launch_apply_M(st, O, B.opidx, B.gam, E, m, B.V, B.vs_e, K, B.Wt, (long long)m * n, 0, periodic, B.active);
       launch_xty(st, E, n, B.Wt, (long long)m * n, 0, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.Gt,
                  (long long)m * m, m, 0, 0, false, B.active, B.xcnt);
     }
     a.K = K;
-    if (K + m > a.Nmax - (kind == 0 ? 4 * m : 0) + m) fail(1, "small problem exceeds workspace");
+    a.restart_write = closing ? 1 : 0;
+    if (Koff + K > B.ktot) fail(1, "small problem exceeds workspace");
     if (kind == 2)
       launch_small_hom(st, a, B.nslots);
     else
-      launch_small_problem(st, a, B.nslots);
+      launch_small_problem(st, a, B.nslots, Koff);
     PEXP_CUDA_TRY(cudaMemsetAsync(B.count, 0, sizeof(int), st));
     launch_update_active(st, E, B.conv, B.active, B.count);
     int h_count = 0;
@@ -255,6 +292,8 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     remaining = h_count;
     last_check = K;
     info.max_k = std::max(info.max_k, K);
+    info.max_ktot = std::max(info.max_ktot, Koff + K);
+    const int Kt = Koff + K;  // the residual decays with the total dimension
     // predict the K at which the still-active evaluations converge: the residual ratio
     // q = res/crit decays roughly geometrically in K; extrapolate from the last two checks
     predicted_next = -1;
@@ -267,12 +306,12 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       for (int e = 0; e < E; ++e) {
         if (!hact[e] || !(kind == 2 || hcrit[e] > 0)) continue;
         double q = kind == 2 ? hres[e] : hres[e] / hcrit[e];
-        if (prevK[e] >= 0 && prevq[e] > 0 && q > 0 && q < prevq[e]) {
-          double slope = (std::log(q) - std::log(prevq[e])) / double(K - prevK[e]);
-          preds.push_back(K + std::log(0.5 / q) / slope);
+        if (prevK[e] >= 0 && prevK[e] < Kt && prevq[e] > 0 && q > 0 && q < prevq[e]) {
+          double slope = (std::log(q) - std::log(prevq[e])) / double(Kt - prevK[e]);
+          preds.push_back(Kt + std::log(0.5 / q) / slope - Koff);
         }
         prevq[e] = q;
-        prevK[e] = K;
+        prevK[e] = Kt;
       }
       if (!preds.empty()) {
         std::sort(preds.begin(), preds.end());
@@ -330,9 +369,43 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     remaining = h_count;
   }
   while (remaining > 0) {
-    if ((steps + 2) * m > kcap) {
-      if (steps >= 1 && last_check != steps * m) do_check(steps * m);
+    const bool cyc_full = (steps + 2) * m > kcap;            // no room for another block + tail
+    const bool tot_full = Koff + (steps + 1) * m > B.ktot;    // total dimension cap
+    const bool count_hit = can_restart && restart_blocks > 0 && steps >= restart_blocks;
+    if (tot_full || (cyc_full && !can_restart)) {
+      if (steps >= 1 && last_check != steps * m) do_check(steps * m, false);
       break;
+    }
+    if (cyc_full || count_hit) {
+      if (steps == 0) fail(1, "basis capacity below two blocks");
+      // ---- exact nested restart (DESIGN.md §3 #5): close cycle c at K = steps*m
+      const int K = steps * m;
+      do_check(K, true);  // z at the outputs, NA extended by this cycle, TX = H_tail X / gamma
+      if (remaining == 0) break;
+      const long long ws_e = B.vs_e;
+      if (info.restarts == 0)
+        PEXP_CUDA_TRY(cudaMemsetAsync(acc.Y, 0, size_t(E) * acc.ys_e * sizeof(double), st));
+      // outputs of the closed cycle: Y += V_c z_c
+      launch_combine(st, E, n, B.V, ws_e, 0, K, B.Z + size_t(acc.o0) * kcap, B.zs_e, kcap, acc.Y, acc.ys_e, 0,
+                     acc.no, 1.0, 1.0, B.active);
+      // residual r(t) = (1/gamma) W TX z(t),  W = (I - gamma A) V_tail  ->  new block 0 = Q, W = Q R
+      launch_apply_M(st, O, B.opidx, B.gam, E, m, B.V, ws_e, K, B.V, ws_e, 0, periodic, B.active);
+      PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.Wt, size_t(m) * n * sizeof(double), B.V, ws_e * sizeof(double),
+                                      size_t(m) * n * sizeof(double), E, cudaMemcpyDeviceToDevice, st));
+      launch_xty(st, E, n, B.V, ws_e, 0, m, B.V, ws_e, 0, m, B.part, B.part_cap, B.G0, (long long)m * m, m, 0, 0,
+                 false, B.active, B.xcnt);
+      inblock_qr(st, B, E, n, m, 0, B.G0, (long long)m * m, m, defl, B.active);
+      launch_xty(st, E, n, B.V, ws_e, 0, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.Rtmp,
+                 (long long)m * m, m, 0, 0, false, B.active, B.xcnt);
+      launch_restart_finish(st, E, m, kcap, B.Rtmp, B.TX, B.CPL, B.Dn, B.Kl, B.kplast, B.H, B.hs_e, B.live,
+                            B.active);
+      Koff += K;
+      ++info.restarts;
+      steps = 0;
+      last_check = -1;
+      next_check = std::max(4, 2 * m);
+      if (predicted_next > 0) next_check = std::max(m, std::min(predicted_next - K, kcap));
+      continue;
     }
     const int b = steps, nv = (b + 1) * m;
     const long long ws_e = B.vs_e;
@@ -372,8 +445,10 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     }
     ++steps;
     const int K = steps * m;
-    if (K >= next_check || (steps + 2) * m > kcap) {
-      do_check(K);
+    const bool closing_next = (steps + 2) * m > kcap || Koff + (steps + 1) * m > B.ktot ||
+                              (can_restart && restart_blocks > 0 && steps >= restart_blocks);
+    if (!(closing_next && can_restart) && (K >= next_check || closing_next)) {
+      do_check(K, false);
       int geo = std::max(K + m, (int)std::ceil(K * 1.25));
       next_check = geo;
       if (predicted_next > 0) next_check = std::max(K + m, std::min(predicted_next, 2 * K));
@@ -584,13 +659,14 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   L.G = ar.take<double>(size_t(E) * s * n);
   L.Yend = ar.take<double>(size_t(E) * n);
   alloc_svd(ar, L.S, E, n, s);
-  alloc_ebk(ar, L.B, E, n, o.kcap, s, 2, s, true, L.S.R);
+  const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
+  alloc_ebk(ar, L.B, E, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable);
   if (P > 1) {
     const int mh = std::min(16, P - 1), G = cdiv(P - 1, mh), Eg = Bt * G;
     // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
     // 16 legs -> 288 columns); give it at least 24 block steps
     const int kcap_h = std::min(KSMALL_MAX - 64, std::max(o.kcap, 24 * mh));
-    alloc_ebk(ar, L.Bh, Eg, n, kcap_h, mh, P, s, false, nullptr);
+    alloc_ebk(ar, L.Bh, Eg, n, kcap_h, kcap_h, mh, P, s, false, nullptr, false);
     L.Bh.groups = G;
     L.Yh = ar.take<double>(size_t(Eg) * P * n);
   } else {
@@ -632,8 +708,10 @@ static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
   L.iota = ar.take<int>(P);
   L.err = ar.take<int>(4);
   alloc_svd(ar, L.S, E, n, s);
-  alloc_ebk(ar, L.B, E, n, o.kcap, s, s, s, true, L.S.R);
-  alloc_ebk(ar, L.B1, 1, n, std::min(o.kcap, 512), 1, s, s, false, nullptr);
+  const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
+  alloc_ebk(ar, L.B, E, n, o.kcyc, o.kcap, s, s, s, true, L.S.R, restartable);
+  const int k1 = std::min(o.kcap, 512);  // scan: single vectors, short spaces, no restart
+  alloc_ebk(ar, L.B1, 1, n, k1, k1, 1, s, s, false, nullptr, false);
 }
 
 static size_t lin_bytes(const pexp_ctx* c, int P) {
@@ -681,6 +759,7 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
   if (o.node_rule != 0) return PEXP_EINVAL;
   if (o.k_max < 0 || o.k_max > KSMALL_MAX - 64) return PEXP_EINVAL;
   if (o.stop_rule < 0 || o.stop_rule > 1) return PEXP_EINVAL;
+  if (o.basis_cols < 0) return PEXP_EINVAL;
   pexp_ctx* c = new pexp_ctx;
   c->n = n;
   c->bc = bc;
@@ -773,9 +852,10 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
     RunInfo ri{}, rh{};
     if (mmax > 0) {
-      ri = ebk_run(st, L.B, L.F, L.O, periodic, mmax, 0, h, s - 1, s - 1, 2, o.stop_rule);
+      ri = ebk_run(st, L.B, L.F, L.O, periodic, mmax, 0, h, s - 1, s - 1, 2, o.stop_rule, Accum{L.Yend, n, 1, 1},
+                   o.restart_blocks);
       launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, ri.max_k, L.B.Z + L.B.kcap, L.B.zs_e, L.B.kcap, L.Yend, n, 0, 1,
-                     1.0, 0.0, nullptr, L.B.kfin);
+                     1.0, ri.restarts ? 1.0 : 0.0, nullptr, L.B.kfin);
     } else {
       PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
     }
@@ -823,7 +903,8 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     if (st_out) {
       std::memset(st_out, 0, sizeof(*st_out));
       st_out->max_m = mmax;
-      st_out->max_k = std::max(ri.max_k, rh.max_k);
+      st_out->max_k = std::max(ri.max_ktot, rh.max_ktot);
+      st_out->restarts = ri.restarts;
       st_out->best_residual = std::max(ri.worst_res_ratio, rh.worst_res_ratio);
       st_out->ms_total = ms;
       st_out->evals = E;
@@ -834,7 +915,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
                              std::to_string(ri.unconverged) + " nonhomogeneous, " + std::to_string(rh.unconverged) +
                              " homogeneous evaluations; worst residual/target " +
                              std::to_string(std::max(ri.worst_res_ratio, rh.worst_res_ratio)) + ", max_k " +
-                             std::to_string(std::max(ri.max_k, rh.max_k)) + ", m " + std::to_string(mmax) + ")");
+                             std::to_string(std::max(ri.max_ktot, rh.max_ktot)) + ", m " + std::to_string(mmax) + ")");
   });
 }
 
@@ -872,7 +953,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
     h2d(st, L.B.fidx, iota);
     h2d(st, L.B.opidx, iota);
     launch_broadcast_waveform(st, P, s, n, u0, L.Uk);
-    int iters = 0, max_m = 0, max_k = 0;
+    int iters = 0, max_m = 0, max_k = 0, restarts = 0;
     double delta = 0.0, delta0 = -1.0;
     for (int k = 0; k < max_wr_iters; ++k) {
       launch_ubar_gamma(st, P, s, n, L.Uk, dT, L.ubar, L.B.gam);
@@ -887,11 +968,13 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
       max_m = std::max(max_m, mmax);
       if (mmax > 0) {
-        RunInfo ri = ebk_run(st, L.B, L.F, L.O, true, mmax, 0, h, s - 1, 1, s, o.stop_rule);
+        RunInfo ri = ebk_run(st, L.B, L.F, L.O, true, mmax, 0, h, s - 1, 1, s, o.stop_rule,
+                             Accum{L.Y, (long long)s * n, 0, s}, o.restart_blocks);
         if (ri.unconverged) fail(PEXP_ENOCONV, "Krylov capacity reached (nonhomogeneous, WR iteration " + std::to_string(k + 1) + ")");
-        max_k = std::max(max_k, ri.max_k);
+        max_k = std::max(max_k, ri.max_ktot);
+        restarts += ri.restarts;
         launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, ri.max_k, L.B.Z, L.B.zs_e, L.B.kcap, L.Y, (long long)s * n, 0, s,
-                       1.0, 0.0, nullptr, L.B.kfin);
+                       1.0, ri.restarts ? 1.0 : 0.0, nullptr, L.B.kfin);
       } else {
         PEXP_CUDA_TRY(cudaMemsetAsync(L.Y, 0, size_t(P) * s * n * sizeof(double), st));
       }
@@ -940,6 +1023,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       st_out->wr_last_delta = delta;
       st_out->max_m = max_m;
       st_out->max_k = max_k;
+      st_out->restarts = restarts;
       st_out->ms_total = ms;
       st_out->evals = P * iters;
       st_out->kernel_launches = (int)g_launches;

@@ -519,6 +519,13 @@ __global__ void k_spline(int s, int mmax, const double* Kinv, const double* Cfin
 }
 
 // ---------------------------------------------------------------- projected SaI problem
+// One cluster per evaluation.  Current cycle: A_hat = (I - H^{-1})/gamma on the live columns.
+// With restarts the completed cycles precede it (NA, D x D) and feed it through the coupling
+// rows CPL into its block-0 coordinates; the full system
+//     [z_old; z]' = [[NA, 0], [CPL, A_hat]] [z_old; z] + E_1 p(t)      (forced: rows [0, m))
+// is integrated exactly over the s-1 cubic pieces with ONE Pade-13 expm of the augmented
+// matrix (size D + Kp + 4m).  The residual is the current cycle's (it is the residual of the
+// whole accumulated approximation).
 __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
   __shared__ int idx[KSMALL_MAX];
   __shared__ int tidx[MAXS], lpos[MAXS];
@@ -560,7 +567,12 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     const int Kp = s_K, mt = s_mt, ml = s_ml;
     const double gam = a.gam[e];
     const int forced = a.kind == 0;
-    const int Nn = Kp + (forced ? 4 * m : 0);
+    const int D = a.Dn ? a.Dn[e] : 0;
+    const int Kl = a.Kl ? a.Kl[e] : 0;
+    const int Dz = D + Kp;
+    const int Nn = Dz + (forced ? 4 * m : 0);
+    double* NAe = a.NA ? a.NA + e * a.nas_e : nullptr;
+    const double* CPe = a.CPL ? a.CPL + e * a.cpls_e : nullptr;
     // Hs -> S0, Hinv -> S1
     for (int t = threadIdx.x + g.rank * blockDim.x; t < Kp * Kp; t += blockDim.x * g.size) {
       int i = t % Kp, j = t / Kp;
@@ -570,37 +582,61 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     cta_identity(Kp, S1, ld, 1.0, g);
     cta_lu(Kp, S0, ld, piv, red, g);
     cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g);
-    // augmented matrix in S2
+    // augmented matrix (times h) in S2; on a restart check the new cycle is appended to NA
+    const bool wr = a.restart_write && NAe;
     for (int t = threadIdx.x + g.rank * blockDim.x; t < Nn * Nn; t += blockDim.x * g.size) {
       int i = t % Nn, j = t / Nn;
       double v = 0.0;
-      if (i < Kp && j < Kp) v = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
-      else if (forced && i < m && j >= Kp && j < Kp + m && (j - Kp) == i) v = a.h;
-      else if (forced && i >= Kp && j >= Kp && j - i == m && i < Kp + 3 * m) v = 1.0;
-      S2[i + size_t(j) * ld] = v;
+      if (j >= Dz) {
+        if (forced && i < m && j - Dz == i) v = 1.0;  // h E_1: forcing into cycle 0, block 0
+      } else if (i < D && j < D) {
+        v = NAe[i + size_t(j) * a.na_ld];
+      } else if (i >= D && i < Dz) {
+        const int r = i - D;
+        if (j >= D && j < Dz) {
+          v = ((r == j - D ? 1.0 : 0.0) - S1[r + size_t(j - D) * ld]) / gam;
+          if (wr) NAe[i + size_t(j) * a.na_ld] = v;
+        } else if (j >= D - Kl && j < D && idx[r] < m) {
+          v = CPe[idx[r] + size_t(j - (D - Kl)) * m];
+          if (wr) NAe[i + size_t(j) * a.na_ld] = v;
+        }
+      }
+      // polynomial chain: unscaled identity blocks (the h^q factors are applied in the chain)
+      if (forced && i >= Dz && j - i == m && i < Dz + 3 * m) S2[i + size_t(j) * ld] = 1.0;
+      else S2[i + size_t(j) * ld] = a.h * v;
     }
+    if (wr && g.rank == 0) {  // TX = (1/gamma) H_tail X, X = last-block rows of H^{-1}
+      double* TXe = a.TX + e * (long long)m * a.kcap;
+      for (int t = threadIdx.x; t < m * Kp; t += blockDim.x) {
+        const int j = t % m, r = t / m;
+        double v = 0.0;
+        if (lv[K + j])
+          for (int c = 0; c < ml; ++c) v = fma(He[K + j + size_t(idx[lpos[c]]) * a.ldh], S1[lpos[c] + size_t(r) * ld], v);
+        TXe[j + size_t(r) * m] = v / gam;
+      }
+    }
+    if (a.kplast && g.rank == 0 && threadIdx.x == 0) a.kplast[e] = Kp;
     grp_sync(g);
     cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red, g);
     if (g.rank == 0) {  // chaining and residuals: rank 0 of the cluster
-    // chain
     const int np = a.npieces ? a.npieces[e] : a.npieces_const;
-    for (int r = threadIdx.x; r < Kp; r += blockDim.x) z[r] = (!forced && r == 0) ? a.beta[e] : 0.0;
+    for (int r = threadIdx.x; r < Dz; r += blockDim.x) z[r] = (!forced && r == 0) ? a.beta[e] : 0.0;
     double* Ze = a.Z + e * a.zs_e;
     for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
     __syncthreads();
-    for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[idx[r]] = z[r];
+    for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[idx[r]] = z[D + r];
     double maxres = 0.0;
     const double* cf = forced ? a.coef + size_t(e) * (a.s - 1) * 4 * m : nullptr;
     for (int i = 0; i < np; ++i) {
       __syncthreads();
-      for (int r = threadIdx.x; r < Kp; r += blockDim.x) {
+      for (int r = threadIdx.x; r < Dz; r += blockDim.x) {
         double v = 0.0;
-        for (int j = 0; j < Kp; ++j) v = fma(S2[r + size_t(j) * ld], z[j], v);
+        for (int j = 0; j < Dz; ++j) v = fma(S2[r + size_t(j) * ld], z[j], v);
         if (forced) {
           const double* ci = cf + size_t(i) * 4 * m;
           double hq = 1.0;
           for (int q = 0; q < 4; ++q) {
-            const double* B = S2 + size_t(Kp + q * m) * ld;
+            const double* B = S2 + size_t(Dz + q * m) * ld;
             double acc = 0.0;
             for (int c = 0; c < m; ++c) acc = fma(B[r + size_t(c) * ld], ci[q * m + c], acc);
             v = fma(hq, acc, v);
@@ -610,17 +646,17 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
         zn[r] = v;
       }
       __syncthreads();
-      for (int r = threadIdx.x; r < Kp; r += blockDim.x) z[r] = zn[r];
+      for (int r = threadIdx.x; r < Dz; r += blockDim.x) z[r] = zn[r];
       __syncthreads();
       const int node = i + 1;
       if (node % a.out_stride == 0 && node / a.out_stride < a.nout)
-        for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[size_t(node / a.out_stride) * a.kcap + idx[r]] = z[r];
+        for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[size_t(node / a.out_stride) * a.kcap + idx[r]] = z[D + r];
       // residual ||r(t)|| = (1/gamma) || (I - gamma A) Vtail Htail x ||, x = (H^{-1} z)[last block]
       if (mt > 0) {
         for (int c = threadIdx.x; c < ml; c += blockDim.x) {
           double v = 0.0;
           const int row = lpos[c];
-          for (int j = 0; j < Kp; ++j) v = fma(S1[row + size_t(j) * ld], z[j], v);
+          for (int j = 0; j < Kp; ++j) v = fma(S1[row + size_t(j) * ld], z[D + j], v);
           xs[c] = v;
         }
         __syncthreads();
@@ -653,6 +689,42 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     }  // rank 0
     grp_sync(g);
   }
+}
+
+// Finish a restart for the still-active evaluations: CPL = R TX (R = Q^T W0 of the new
+// block 0), D += width of the closed cycle, fresh H and live flags for the new cycle.
+__global__ void k_restart_finish(int E, int m, int kcap, const double* R, const double* TX, double* CPL,
+                                 int* Dn, int* Kl, const int* kplast, double* H, long long hs_e, int* live,
+                                 const int* active) {
+  const int e = blockIdx.x;
+  if (active && !active[e]) return;
+  const int kp = kplast[e];
+  const double* Re = R + size_t(e) * m * m;
+  const double* Te = TX + size_t(e) * m * kcap;
+  double* Ce = CPL + size_t(e) * m * kcap;
+  for (int t = threadIdx.x; t < m * kp; t += blockDim.x) {
+    const int i = t % m, r = t / m;
+    double v = 0.0;
+    for (int j = 0; j < m; ++j) v = fma(Re[i + size_t(j) * m], Te[j + size_t(r) * m], v);
+    Ce[i + size_t(r) * m] = v;
+  }
+  double* He = H + e * hs_e;
+  for (long long t = threadIdx.x; t < hs_e; t += blockDim.x) He[t] = 0.0;
+  for (int c = threadIdx.x + m; c < kcap; c += blockDim.x) live[size_t(e) * kcap + c] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Dn[e] += kp;
+    Kl[e] = kp;
+  }
+}
+
+void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double* R, const double* TX, double* CPL,
+                           int* Dn, int* Kl, const int* kplast, double* H, long long hs_e, int* live,
+                           const int* active) {
+  ProfScope ps(PC_SMALL, st, 0.0, 0.0);
+  k_restart_finish<<<E, PEXP_THREADS, 0, st>>>(E, m, kcap, R, TX, CPL, Dn, Kl, kplast, H, hs_e, live, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- grouped homogeneous legs
@@ -852,11 +924,11 @@ void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, 
   PEXP_LAUNCH_CHECK();
 }
 
-void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots) {
-  if (a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
+void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax) {
+  if (Dmax + a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
   size_t smem = 2 * KSMALL_MAX * sizeof(double);
   {
-  const double N = a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
+  const double N = Dmax + a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
   ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
   const int ncl = std::min(a.E, nslots);
   launch_clustered(k_small_problem, ncl, cluster_size_for(ncl), smem, st, a);

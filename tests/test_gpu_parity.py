@@ -111,7 +111,7 @@ def test_expm_batched_vs_scipy():
 # ---------------------------------------------------------------- linear Paraexp-EBK solves
 
 def _linear(p, k_max=256, **kw):
-    c = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=p.s, k_max=k_max)
+    c = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=p.s, k_max=k_max, **kw)
     out, st = c.solve_linear(t(p.u0), t(p.src), p.T, p.P, p.tol)
     return out.cpu().numpy(), st
 
@@ -165,6 +165,26 @@ def test_linear_config4_full_batch_sampled():
         assert rel(out[b], ref[0]) < 1e-8, (b, st)
 
 
+@pytest.mark.parametrize("restart_blocks,basis_cols", [(3, 0), (-1, 40), (20, 0)])
+def test_linear_restart_nested_exact(restart_blocks, basis_cols):
+    """Exact nested restart (DESIGN.md §3 #5): the cycle residual becomes the next cycle's
+    source; the result must match the unrestarted oracle to the same 1e-8."""
+    p = synth.generic_linear(n=777, bc="periodic", nu=5e-3, a=1.3, P=5, s=12, T=0.5, seed=7)
+    out, st = _linear(p, k_max=512, restart_blocks=restart_blocks, basis_cols=basis_cols)
+    ref = _oracle_linear(p)
+    assert rel(out, ref) < 1e-8, st
+    if restart_blocks != 20:
+        assert st["restarts"] >= 1, st
+
+
+def test_linear_config2_reduced_restarted():
+    p = synth.config2(n=1200, P=16, T=0.25, s=64)
+    out, st = _linear(p, k_max=512, restart_blocks=-1, basis_cols=72)
+    ref = _oracle_linear(p)
+    assert rel(out, ref) < 1e-8, st
+    assert st["restarts"] >= 1, st
+
+
 def test_linear_P1_and_unforced_and_zero():
     n = 300
     x = synth.grid_x(n, "periodic")
@@ -190,8 +210,8 @@ def test_linear_config2_full_size_sampled():
 
 # ---------------------------------------------------------------- Burgers WR
 
-def _burgers(p, k_max=256):
-    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=k_max)
+def _burgers(p, k_max=256, **kw):
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=k_max, **kw)
     out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters)
     return out.cpu().numpy(), st
 
@@ -211,3 +231,12 @@ def test_burgers_config3_full():
     ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
+
+
+def test_burgers_small_restarted():
+    p = synth.config3(n=256, P=4, s=12, T=0.2, nu=0.02)
+    out, st = _burgers(p, k_max=512, restart_blocks=-1, basis_cols=40)
+    ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
+    assert st["wr_iters"] == info["iters"], (st, info["delta"])
+    assert rel(out, ref) < 1e-8, st
+    assert st["restarts"] >= 1, st
