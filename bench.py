@@ -58,7 +58,9 @@ def workload(name):
         return p, dict(kind="burgers", s=p.s, k_max=256)
     if name == "C5":
         p = synth.config5()
-        return p, dict(kind="burgers", s=p.s, k_max=384)
+        # 256 subintervals x 65536 points: the basis of one restart cycle is capped at 256
+        # columns per subinterval (34 GiB); total dimension up to 768 (exact nested restart)
+        return p, dict(kind="burgers", s=p.s, k_max=768, basis_cols=256)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -213,7 +215,8 @@ def main():
         src_h = torch.tensor(p.src).pin_memory()
         out = torch.empty((p.batch, p.P, p.n), dtype=torch.float64, device=dev)
     else:
-        ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"])
+        ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"],
+                           basis_cols=cfg.get("basis_cols", 0))
         ctx.ensure_workspace(p.P, dev, kind=1)
         u0_h = torch.tensor(p.u0).pin_memory()
         src_h = None

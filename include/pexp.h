@@ -77,6 +77,8 @@ typedef struct {
                              1 = true residual ||r(t)|| = ||A y + U p - y'|| (DESIGN.md §3 #6) */
   int32_t basis_cols;     /* basis columns kept per evaluation in one cycle (device memory:
                              8 n basis_cols bytes per evaluation); 0 = k_max               */
+  int32_t eval_chunk;     /* nonhomogeneous EBK evaluations resident at once (the basis
+                             memory is eval_chunk * basis_cols * n * 8 bytes); 0 = all      */
 } pexp_options;
 
 /* Per-solve statistics (host memory, caller-owned). */

@@ -61,7 +61,7 @@ static void h2d(cudaStream_t st, T* dst, const std::vector<T>& v) {
 struct Opts {
   int s;
   double tau_f, eta_f;
-  int restart_blocks, kcap, stop_rule, kcyc;
+  int restart_blocks, kcap, stop_rule, kcyc, chunk;
   cudaStream_t st;
 };
 
@@ -73,6 +73,7 @@ static Opts norm_opts(const pexp_options& o) {
   r.restart_blocks = o.restart_blocks > 0 ? o.restart_blocks : (o.restart_blocks < 0 ? 0 : 20);
   r.kcap = o.k_max > 0 ? o.k_max : 256;
   r.kcyc = o.basis_cols > 0 ? std::min(o.basis_cols, r.kcap) : r.kcap;
+  r.chunk = o.eval_chunk > 0 ? o.eval_chunk : (1 << 30);
   r.st = (cudaStream_t)o.stream;
   r.stop_rule = o.stop_rule;
   return r;
@@ -95,35 +96,35 @@ struct EbkBufs {
   int *Dn = nullptr, *Kl = nullptr, *kplast = nullptr;
 };
 
+// xty partial-sum capacity for E evaluations of an (nx x ny) product (see launch_xty)
+static size_t part_need(int E, int n, int nx, int ny) {
+  // bound on E'*nch(E') for every E' <= E (xty_chunks stops at <= 1184 CTAs or one chunk)
+  size_t ech = std::max<size_t>(size_t(E) * cdiv(n, xty_chunks(n, E)), 2 * 148 * 8 + size_t(E));
+  ech = std::min<size_t>(ech, size_t(E) * cdiv(n, 512));
+  size_t cap = ech * nx * ny;
+  // tall path (ny <= 32): E' * nch(E') <= E' + 2*148*6 chunks for any E' <= E
+  size_t tall = (size_t(E) + 2 * 148 * 6) * size_t(nx) * std::min(ny, 32);
+  return std::max(cap, tall);
+}
+
+// E evaluations run through the EBK in chunks of at most Ec (eval_chunk option): the light
+// per-evaluation arrays (inputs set by the SVD stage / callers, flags, residuals) cover all E,
+// the basis and everything else that scales with the Krylov dimension covers one chunk.
 // kcap: basis columns per evaluation and cycle; ktot: total Krylov dimension over all cycles
 // (ktot > kcap or restart_blocks > 0 allocates the nested-restart state).
-static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int ktot, int mcap, int nout, int s,
+static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int ktot, int mcap, int nout, int s,
                       bool forced, double* Wt_shared, bool restartable) {
-  B.E = E; B.n = n; B.kcap = kcap; B.ktot = ktot; B.mcap = mcap; B.nout = nout; B.s = s;
+  Ec = std::max(1, std::min(E, Ec));
+  B.E = Ec; B.n = n; B.kcap = kcap; B.ktot = ktot; B.mcap = mcap; B.nout = nout; B.s = s;
   B.vs_e = (long long)kcap * n;
   B.hs_e = (long long)kcap * kcap;
   B.zs_e = (long long)nout * kcap;
-  B.V = ar.take<double>(size_t(E) * kcap * n);
-  B.H = ar.take<double>(size_t(E) * kcap * kcap);
-  B.Z = ar.take<double>(size_t(E) * nout * kcap);
-  B.Gt = ar.take<double>(size_t(E) * mcap * mcap);
-  B.Wt = Wt_shared ? Wt_shared : ar.take<double>(size_t(E) * mcap * n);
-  B.Wt2 = ar.take<double>(size_t(E) * mcap * n);
-  B.n0p = ar.take<double>(size_t(E) * mcap);
-  B.T = ar.take<double>(size_t(E) * kcap * mcap);
-  B.G0 = ar.take<double>(size_t(E) * mcap * mcap);
-  B.G1 = ar.take<double>(size_t(E) * mcap * mcap);
-  B.Rinv = ar.take<double>(size_t(E) * mcap * mcap);
-  B.Rtmp = ar.take<double>(size_t(E) * mcap * mcap);
-  B.R0 = ar.take<double>(size_t(E) * mcap * mcap);
-  B.critc = ar.take<double>(size_t(E) * mcap);
-  B.horc = ar.take<int>(size_t(E) * mcap);
+  // ---- light, all evaluations
   B.res = ar.take<double>(E);
   B.gam = ar.take<double>(E);
   B.crit = ar.take<double>(E);
   B.beta = ar.take<double>(size_t(E) * mcap);
   B.coef = forced ? ar.take<double>(size_t(E) * (s - 1) * 4 * mcap) : nullptr;
-  B.live = ar.take<int>(size_t(E) * kcap);
   B.active = ar.take<int>(E);
   B.conv = ar.take<int>(E);
   B.kfin = ar.take<int>(E);
@@ -132,30 +133,53 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int n, int kcap, int ktot, i
   B.fidx = ar.take<int>(E);
   B.opidx = ar.take<int>(E);
   B.xcnt = ar.take<int>(E);
-  // bound on E'*nch(E') for every E' <= E (xty_chunks stops at <= 1184 CTAs or one chunk)
-  size_t ech = std::max<size_t>(size_t(E) * cdiv(n, xty_chunks(n, E)), 2 * 148 * 8 + size_t(E));
-  ech = std::min<size_t>(ech, size_t(E) * cdiv(n, 512));
-  B.part_cap = ech * std::max(kcap, s) * (forced ? std::max(mcap, s) : mcap);
-  // tall path (ny <= 32): E' * nch(E') <= E' + 2*148*6 chunks for any E' <= E
-  const int nyt = std::min(forced ? std::max(mcap, s) : mcap, 32);
-  size_t tall = (size_t(E) + 2 * 148 * 6) * size_t(std::max(kcap, s)) * nyt;
-  B.part_cap = std::max(B.part_cap, tall);
+  // ---- heavy, one chunk
+  B.V = ar.take<double>(size_t(Ec) * kcap * n);
+  B.H = ar.take<double>(size_t(Ec) * kcap * kcap);
+  B.Z = ar.take<double>(size_t(Ec) * nout * kcap);
+  B.Gt = ar.take<double>(size_t(Ec) * mcap * mcap);
+  B.Wt = Wt_shared ? Wt_shared : ar.take<double>(size_t(Ec) * mcap * n);
+  B.Wt2 = ar.take<double>(size_t(Ec) * mcap * n);
+  B.n0p = ar.take<double>(size_t(Ec) * mcap);
+  B.T = ar.take<double>(size_t(Ec) * kcap * mcap);
+  B.G0 = ar.take<double>(size_t(Ec) * mcap * mcap);
+  B.G1 = ar.take<double>(size_t(Ec) * mcap * mcap);
+  B.Rinv = ar.take<double>(size_t(Ec) * mcap * mcap);
+  B.Rtmp = ar.take<double>(size_t(Ec) * mcap * mcap);
+  B.R0 = ar.take<double>(size_t(Ec) * mcap * mcap);
+  B.critc = ar.take<double>(size_t(Ec) * mcap);
+  B.horc = ar.take<int>(size_t(Ec) * mcap);
+  B.live = ar.take<int>(size_t(Ec) * kcap);
+  // the SVD stage (all E, s x s products) shares the partial-sum buffer with the chunks
+  B.part_cap = std::max(part_need(Ec, n, std::max(kcap, s), forced ? std::max(mcap, s) : mcap),
+                        forced ? part_need(E, n, s, s) : size_t(0));
   B.part = ar.take<double>(B.part_cap);
   B.Nmax = ktot + (forced ? 4 * mcap : 0);
   B.work_slot = 10LL * B.Nmax * B.Nmax;
   B.iwork_slot = B.Nmax;
   // one workspace slot per resident cluster; large projected problems get one per SM
-  B.nslots = std::min(E, B.Nmax > 512 ? 148 : 512);
+  B.nslots = std::min(Ec, B.Nmax > 512 ? 148 : 512);
   B.work = ar.take<double>(size_t(B.nslots) * B.work_slot);
   B.iwork = ar.take<int>(size_t(B.nslots) * B.iwork_slot);
   if (restartable) {
-    B.NA = ar.take<double>(size_t(E) * ktot * ktot);
-    B.CPL = ar.take<double>(size_t(E) * mcap * kcap);
-    B.TX = ar.take<double>(size_t(E) * mcap * kcap);
-    B.Dn = ar.take<int>(E);
-    B.Kl = ar.take<int>(E);
-    B.kplast = ar.take<int>(E);
+    B.NA = ar.take<double>(size_t(Ec) * ktot * ktot);
+    B.CPL = ar.take<double>(size_t(Ec) * mcap * kcap);
+    B.TX = ar.take<double>(size_t(Ec) * mcap * kcap);
+    B.Dn = ar.take<int>(Ec);
+    B.Kl = ar.take<int>(Ec);
+    B.kplast = ar.take<int>(Ec);
   }
+}
+
+// View of evaluations [c0, c0 + Ec) of B for one EBK chunk (light arrays offset, heavy shared).
+static EbkBufs chunk_view(const EbkBufs& B, int c0, int Ec, int mb) {
+  EbkBufs C = B;
+  C.E = Ec;
+  C.res += c0; C.gam += c0; C.crit += c0; C.active += c0; C.conv += c0; C.kfin += c0;
+  C.npieces += c0; C.fidx += c0; C.opidx += c0; C.xcnt += c0;
+  C.beta += c0;  // kind-1 layout (forced chunks do not read beta)
+  if (C.coef) C.coef += size_t(c0) * (B.s - 1) * 4 * mb;
+  return C;
 }
 
 // Pivoted deflating Cholesky-QR of the m columns of V at column offset c0 (in place):
@@ -567,20 +591,23 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
   const int mb = std::max(mmax, 1);
   if (mb > B->mcap) fail(1, "retained rank exceeds capacity");
   launch_build_final(st, E, s, mb, S.off, S.Qs, S.sig, S.Cs, S.me, S.Msel, S.Cfin, S.fill);
-  launch_combine(st, E, n, U, gs_e, 0, s, S.Msel, (long long)s * mb, s, B->V, B->vs_e, 0, mb, 1.0, 0.0, nullptr);
-  launch_fill_random(st, E, n, mb, S.fill, B->V, B->vs_e, 12345u);
+  // final block U_j (mb columns, padded with the next singular vectors / random columns),
+  // CholQR2 -> S.U (stride s*n); the EBK copies each chunk's U_j into its basis block 0
+  launch_combine(st, E, n, U, gs_e, 0, s, S.Msel, (long long)s * mb, s, Fr, gs_e, 0, mb, 1.0, 0.0, nullptr);
+  launch_fill_random(st, E, n, mb, S.fill, Fr, gs_e, 12345u);
   for (int q = 0; q < 2; ++q) {
-    launch_xty(st, E, n, B->V, B->vs_e, 0, mb, B->V, B->vs_e, 0, mb, part, part_cap, S.Gs, (long long)mb * mb, mb, 0, 0,
+    double* X = q == 0 ? Fr : S.U;
+    launch_xty(st, E, n, X, gs_e, 0, mb, X, gs_e, 0, mb, part, part_cap, S.Gs, (long long)mb * mb, mb, 0, 0,
                false, nullptr, B->xcnt);
     launch_block_chol(st, E, mb, S.Gs, (long long)mb * mb, mb, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0,
                       0, nullptr, 0, nullptr, false);
-    if (mb <= 32) {
-      launch_combine(st, E, n, B->V, B->vs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, B->V, B->vs_e, 0, mb, 1.0, 0.0,
-                     nullptr);
+    if (q == 0) {
+      launch_combine(st, E, n, Fr, gs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, S.U, gs_e, 0, mb, 1.0, 0.0, nullptr);
+    } else if (mb <= 32) {
+      launch_combine(st, E, n, S.U, gs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, S.U, gs_e, 0, mb, 1.0, 0.0, nullptr);
     } else {
-      launch_combine(st, E, n, B->V, B->vs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, Fr, gs_e, 0, mb, 1.0, 0.0, nullptr);
-      PEXP_CUDA_TRY(cudaMemcpy2DAsync(B->V, B->vs_e * sizeof(double), Fr, gs_e * sizeof(double),
-                                      size_t(mb) * n * sizeof(double), E, cudaMemcpyDeviceToDevice, st));
+      launch_combine(st, E, n, S.U, gs_e, 0, mb, S.Rinv, (long long)mb * mb, mb, Fr, gs_e, 0, mb, 1.0, 0.0, nullptr);
+      PEXP_CUDA_TRY(cudaMemcpyAsync(S.U, Fr, size_t(E) * gs_e * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
   }
   std::vector<double> Ki = notaknot_inverse(s);
@@ -660,13 +687,13 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   L.Yend = ar.take<double>(size_t(E) * n);
   alloc_svd(ar, L.S, E, n, s);
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
-  alloc_ebk(ar, L.B, E, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable);
+  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable);
   if (P > 1) {
     const int mh = std::min(16, P - 1), G = cdiv(P - 1, mh), Eg = Bt * G;
     // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
     // 16 legs -> 288 columns); give it at least 24 block steps
     const int kcap_h = std::min(KSMALL_MAX - 64, std::max(o.kcap, 24 * mh));
-    alloc_ebk(ar, L.Bh, Eg, n, kcap_h, kcap_h, mh, P, s, false, nullptr, false);
+    alloc_ebk(ar, L.Bh, Eg, Eg, n, kcap_h, kcap_h, mh, P, s, false, nullptr, false);
     L.Bh.groups = G;
     L.Yh = ar.take<double>(size_t(Eg) * P * n);
   } else {
@@ -709,9 +736,9 @@ static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
   L.err = ar.take<int>(4);
   alloc_svd(ar, L.S, E, n, s);
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
-  alloc_ebk(ar, L.B, E, n, o.kcyc, o.kcap, s, s, s, true, L.S.R, restartable);
+  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, s, s, true, L.S.R, restartable);
   const int k1 = std::min(o.kcap, 512);  // scan: single vectors, short spaces, no restart
-  alloc_ebk(ar, L.B1, 1, n, k1, k1, 1, s, s, false, nullptr, false);
+  alloc_ebk(ar, L.B1, 1, 1, n, k1, k1, 1, s, s, false, nullptr, false);
 }
 
 static size_t lin_bytes(const pexp_ctx* c, int P) {
@@ -737,6 +764,35 @@ static void init_once() {
   }
 }
 
+// The forced EBK over E evaluations in chunks of B.E (eval_chunk): each chunk copies its
+// U_j from the SVD stage into basis block 0, runs the block Arnoldi, and writes its outputs
+// Y[e] (+)= V_e z_e at output o0 (restart accumulation, then the final cycle).
+static RunInfo ebk_forced_chunked(cudaStream_t st, EbkBufs& B, const SvdBufs& S, const Factors& F, const Ops& O,
+                                  bool periodic, int E, int mmax, double h, int s, int out_stride, int nout,
+                                  int o0, double* Y, long long ys_e, int stop_rule, int restart_blocks) {
+  RunInfo tot;
+  const int n = B.n, Ecap = B.E;
+  const int no = o0 == 0 ? nout : 1;
+  for (int c0 = 0; c0 < E; c0 += Ecap) {
+    const int ec = std::min(Ecap, E - c0);
+    EbkBufs Bc = chunk_view(B, c0, ec, mmax);
+    PEXP_CUDA_TRY(cudaMemcpy2DAsync(Bc.V, Bc.vs_e * sizeof(double), S.U + size_t(c0) * s * n,
+                                    size_t(s) * n * sizeof(double), size_t(mmax) * n * sizeof(double), ec,
+                                    cudaMemcpyDeviceToDevice, st));
+    double* Yc = Y + size_t(c0) * ys_e;
+    RunInfo r = ebk_run(st, Bc, F, O, periodic, mmax, 0, h, s - 1, out_stride, nout, stop_rule,
+                        Accum{Yc, ys_e, o0, no}, restart_blocks);
+    launch_combine(st, ec, n, Bc.V, Bc.vs_e, 0, std::max(r.max_k, 1), Bc.Z + size_t(o0) * Bc.kcap, Bc.zs_e, Bc.kcap,
+                   Yc, ys_e, 0, no, 1.0, r.restarts ? 1.0 : 0.0, nullptr, Bc.kfin);
+    tot.max_k = std::max(tot.max_k, r.max_k);
+    tot.max_ktot = std::max(tot.max_ktot, r.max_ktot);
+    tot.restarts += r.restarts;
+    tot.unconverged += r.unconverged;
+    tot.worst_res_ratio = std::max(tot.worst_res_ratio, r.worst_res_ratio);
+  }
+  return tot;
+}
+
 // ---------------------------------------------------------------- C ABI
 extern "C" {
 
@@ -759,7 +815,7 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
   if (o.node_rule != 0) return PEXP_EINVAL;
   if (o.k_max < 0 || o.k_max > KSMALL_MAX - 64) return PEXP_EINVAL;
   if (o.stop_rule < 0 || o.stop_rule > 1) return PEXP_EINVAL;
-  if (o.basis_cols < 0) return PEXP_EINVAL;
+  if (o.basis_cols < 0 || o.eval_chunk < 0) return PEXP_EINVAL;
   pexp_ctx* c = new pexp_ctx;
   c->n = n;
   c->bc = bc;
@@ -852,10 +908,8 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
     RunInfo ri{}, rh{};
     if (mmax > 0) {
-      ri = ebk_run(st, L.B, L.F, L.O, periodic, mmax, 0, h, s - 1, s - 1, 2, o.stop_rule, Accum{L.Yend, n, 1, 1},
-                   o.restart_blocks);
-      launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, ri.max_k, L.B.Z + L.B.kcap, L.B.zs_e, L.B.kcap, L.Yend, n, 0, 1,
-                     1.0, ri.restarts ? 1.0 : 0.0, nullptr, L.B.kfin);
+      ri = ebk_forced_chunked(st, L.B, L.S, L.F, L.O, periodic, E, mmax, h, s, s - 1, 2, 1, L.Yend, n, o.stop_rule,
+                              o.restart_blocks);
     } else {
       PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
     }
@@ -968,13 +1022,11 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
       max_m = std::max(max_m, mmax);
       if (mmax > 0) {
-        RunInfo ri = ebk_run(st, L.B, L.F, L.O, true, mmax, 0, h, s - 1, 1, s, o.stop_rule,
-                             Accum{L.Y, (long long)s * n, 0, s}, o.restart_blocks);
+        RunInfo ri = ebk_forced_chunked(st, L.B, L.S, L.F, L.O, true, E, mmax, h, s, 1, s, 0, L.Y, (long long)s * n,
+                                        o.stop_rule, o.restart_blocks);
         if (ri.unconverged) fail(PEXP_ENOCONV, "Krylov capacity reached (nonhomogeneous, WR iteration " + std::to_string(k + 1) + ")");
         max_k = std::max(max_k, ri.max_ktot);
         restarts += ri.restarts;
-        launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, ri.max_k, L.B.Z, L.B.zs_e, L.B.kcap, L.Y, (long long)s * n, 0, s,
-                       1.0, ri.restarts ? 1.0 : 0.0, nullptr, L.B.kfin);
       } else {
         PEXP_CUDA_TRY(cudaMemsetAsync(L.Y, 0, size_t(P) * s * n * sizeof(double), st));
       }
@@ -1084,8 +1136,8 @@ pexp_status pexp_source_svd(pexp_ctx* ctx, const double* G, int32_t E, double to
     int mmax = svd_stage(st, L.S, &L.B, E, n, s, G, tau, o.eta_f * tol, 1.0, m_host);
     PEXP_CUDA_TRY(cudaMemcpyAsync(sigma, L.S.sig, size_t(E) * s * sizeof(double), cudaMemcpyDeviceToDevice, st));
     int mb = std::max(mmax, 1);
-    launch_combine(st, E, n, L.B.V, L.B.vs_e, 0, mb, L.S.Cfin, (long long)mb * s, mb, proj, (long long)s * n, 0, s, 1.0,
-                   0.0, nullptr);
+    launch_combine(st, E, n, L.S.U, (long long)s * n, 0, mb, L.S.Cfin, (long long)mb * s, mb, proj, (long long)s * n, 0,
+                   s, 1.0, 0.0, nullptr);
     PEXP_CUDA_TRY(cudaStreamSynchronize(st));
   });
 }

@@ -96,6 +96,12 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
     Q[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
+  // rotation floor: the Gram carries absolute rounding ~eps*lambda_max, so pairs below
+  // 1e-18*max_i a_ii are decoupled as far as the data allows (relative accuracy is neither
+  // available nor needed: pass 2 and the final SVD of C = U^T G make the basis exact)
+  double dmax = 0.0;
+  for (int i = threadIdx.x; i < s; i += blockDim.x) dmax = fmax(dmax, A[i][i]);
+  const double afloor = fmax(1e-18 * block_max(dmax, red), 1e-300);
   __shared__ int s_rot;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) s_rot = 0;
@@ -106,7 +112,7 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
         jacobi_pair(Ne, r, threadIdx.x, p, q);
         double c = 1.0, sn = 0.0;
         // rotate only pairs that are not yet decoupled to working precision
-        if (fabs(A[p][q]) > 1e-16 * sqrt(fabs(A[p][p] * A[q][q])) && fabs(A[p][q]) > 1e-300) {
+        if (fabs(A[p][q]) > 1e-16 * sqrt(fabs(A[p][p] * A[q][q])) && fabs(A[p][q]) > afloor) {
           sym_schur2(A[p][p], A[q][q], A[p][q], c, sn);
           s_rot = 1;
         }
@@ -135,7 +141,6 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
     __syncthreads();  // every thread has read s_rot before thread 0 resets it
     if (!rotated) break;
   }
-  (void)red;
   if (threadIdx.x == 0) {
     for (int i = 0; i < s; ++i) perm[i] = i;
     for (int i = 0; i < s; ++i) {

@@ -33,7 +33,8 @@ PROFILE_CLASSES = ["sai_solve", "xty", "combine", "small_problem", "small_dense"
 class Options(C.Structure):
     _fields_ = [("s", C.c_int32), ("node_rule", C.c_int32), ("svd_tau_factor", C.c_double),
                 ("stop_factor", C.c_double), ("restart_blocks", C.c_int32), ("k_max", C.c_int32),
-                ("stream", C.c_void_p), ("stop_rule", C.c_int32), ("basis_cols", C.c_int32)]
+                ("stream", C.c_void_p), ("stop_rule", C.c_int32), ("basis_cols", C.c_int32),
+                ("eval_chunk", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -91,7 +92,8 @@ class Context:
 
     def __init__(self, n: int, bc: str = "periodic", nu=1e-2, a=0.0, *, s: int = 32, k_max: int = 256,
                  svd_tau_factor: float = 0.01, stop_factor: float = 0.1, restart_blocks: int = 20,
-                 stream: Optional[torch.cuda.Stream] = None, stop_rule: int = 0, basis_cols: int = 0):
+                 stream: Optional[torch.cuda.Stream] = None, stop_rule: int = 0, basis_cols: int = 0,
+                 eval_chunk: int = 0):
         self.n, self.bc, self.s = int(n), bc, int(s)
         self._stream = stream
         nu = [float(v) for v in (nu if hasattr(nu, "__len__") else [nu])]
@@ -101,7 +103,7 @@ class Context:
         self.batch = len(nu)
         handle = stream.cuda_stream if stream is not None else None  # None = legacy default stream
         self.opt = Options(self.s, 0, svd_tau_factor, stop_factor, restart_blocks, k_max, handle, stop_rule,
-                           basis_cols)
+                           basis_cols, eval_chunk)
         self._h = _P()
         arr = C.c_double * self.batch
         st = _lib.pexp_create_batched(C.byref(self._h), self.n, BC[bc], self.batch, arr(*nu), arr(*a),

@@ -16,7 +16,9 @@ else:
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     kmax = int(sys.argv[3]) if len(sys.argv) > 3 else 768
     bcols = int(sys.argv[4]) if len(sys.argv) > 4 else 256
-    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=kmax, basis_cols=bcols, restart_blocks=-1)
+    chunk = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=kmax, basis_cols=bcols, restart_blocks=-1,
+                     eval_chunk=chunk)
     print("workspace GiB", c.workspace_bytes(p.P, 1) / 2**30, flush=True)
     t0 = time.time(); out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, iters); torch.cuda.synchronize()
     print("C5", st, "wall %.2f" % (time.time() - t0), flush=True)

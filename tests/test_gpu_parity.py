@@ -185,6 +185,14 @@ def test_linear_config2_reduced_restarted():
     assert st["restarts"] >= 1, st
 
 
+def test_linear_config2_reduced_chunked():
+    """eval_chunk: the 16 subintervals run as EBK chunks 5, 5, 5, 1 sharing one basis buffer."""
+    p = synth.config2(n=1200, P=16, T=0.25, s=64)
+    out, st = _linear(p, k_max=384, eval_chunk=5)
+    ref = _oracle_linear(p)
+    assert rel(out, ref) < 1e-8, st
+
+
 def test_linear_P1_and_unforced_and_zero():
     n = 300
     x = synth.grid_x(n, "periodic")
@@ -240,3 +248,11 @@ def test_burgers_small_restarted():
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
     assert st["restarts"] >= 1, st
+
+
+def test_burgers_small_chunked():
+    p = synth.config3(n=256, P=4, s=12, T=0.2, nu=0.02)
+    out, st = _burgers(p, eval_chunk=3)
+    ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
+    assert st["wr_iters"] == info["iters"], (st, info["delta"])
+    assert rel(out, ref) < 1e-8, st
