@@ -58,9 +58,9 @@ def workload(name):
         return p, dict(kind="burgers", s=p.s, k_max=256)
     if name == "C5":
         p = synth.config5()
-        # 256 subintervals x 65536 points: the basis of one restart cycle is capped at 256
-        # columns per subinterval (34 GiB); total dimension up to 768 (exact nested restart)
-        return p, dict(kind="burgers", s=p.s, k_max=768, basis_cols=256)
+        # 256 subintervals x 65536 points: the EBK runs in chunks of 64 subintervals with
+        # 960-column bases (32 GiB of basis; 92 GiB workspace in total)
+        return p, dict(kind="burgers", s=p.s, k_max=960, basis_cols=960, eval_chunk=64)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -216,7 +216,7 @@ def main():
         out = torch.empty((p.batch, p.P, p.n), dtype=torch.float64, device=dev)
     else:
         ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"],
-                           basis_cols=cfg.get("basis_cols", 0))
+                           basis_cols=cfg.get("basis_cols", 0), eval_chunk=cfg.get("eval_chunk", 0))
         ctx.ensure_workspace(p.P, dev, kind=1)
         u0_h = torch.tensor(p.u0).pin_memory()
         src_h = None

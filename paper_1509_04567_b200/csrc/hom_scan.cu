@@ -1,0 +1,516 @@
+// hom_scan.cu — the Burgers homogeneous scan (Fig. 5 / Eq.
+// (updateSolution) P:331-335) as ONE persistent cooperative kernel.
+//
+// For subinterval i = 1..P-1 (sequential: the operator A_i changes per subinterval):
+//     u_hat(t) = exp((t - T_{i-1}) A_i) u_hat(T_{i-1}),   t = T_{i-1} + r h,  r = 0..s-1,
+// by single-vector shift-and-invert Arnoldi on B_i = (I - gamma_i A_i)^{-1}, projected
+// A_hat = (I - H^{-1}) / gamma_i, z(t) = exp(t A_hat) beta e_1, residual stop rule of DESIGN.md
+// §3 #6 (SaI residual |h_{K+1,K} e_K^T H^{-1} z(t)| / gamma <= eta beta / dT).  The waveform
+// update u_{k+1} = u0 + Y + u_hat and delta = max |u_{k+1} - u_k| (a7, a8) are fused in.
+//
+// Roles: CTAs 0..nw-1 are workers, each owning a contiguous segment of rows; CTA nw is the
+// checker that solves the projected problem on the newest available Krylov dimension while the
+// workers keep extending the basis (check latency overlaps the Arnoldi steps).  Worker 0 is the
+// leader: it turns the checker's result into a decision that every worker reads after the next
+// barrier, so all workers leave the Arnoldi loop at the same step.
+//
+// Per Arnoldi step (4 worker barriers):
+//   A: forward L-solve affine maps of own rows -> CTA total; SM dot partial      | barrier
+//   B: carry-in from lower segments, y; backward U-solve maps -> CTA total         | barrier
+//   C: carry-in from upper segments, x; SM correction; CGS pass-1 dot partials      | barrier
+//   D: reduce h; x -= V h; pass-2 dot partials and ||x||^2                          | barrier
+//   E: reduce h2; x -= V h2; ||x|| = sqrt(||x||^2 - ||h2||^2); v_{k+1}; H column; publish
+// Cross-CTA reductions sum the per-CTA partials in a fixed order (identical in every CTA).
+#include "kernels.cuh"
+#include "dense.cuh"
+#include "scan.cuh"
+
+namespace pexp {
+
+namespace {
+
+constexpr int RPT_MAX = 4;   // rows per thread
+constexpr int NT = PEXP_THREADS;
+
+enum { F_STEPS = 0, F_RESULT = 1, F_DECISION = 2, F_KMAX = 3, F_ERR = 4, F_BREAK = 5, F_NFLAGS = 8 };
+enum { B_WCNT = 0, B_WGEN = 1, B_ACNT = 2, B_AGEN = 3 };
+
+__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+// Sense-counting grid barrier over nb CTAs (co-residency guaranteed by the cooperative launch).
+__device__ inline void gbar(unsigned* cnt, unsigned* gen, unsigned nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vg = gen;
+    const unsigned g0 = *vg;
+    __threadfence();
+    if (atomicAdd(cnt, 1u) == nb - 1) {
+      atomicExch(cnt, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vg == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Sum over CTAs of part[c*pw + j] for j < nval, in a fixed order; result to out[j] (smem).
+// One warp per value, lanes stride over the CTAs, then a warp tree.
+__device__ inline void grid_reduce(const double* part, int pw, int ncta, int j0, int nval, double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j = w; j < nval; j += NT / 32) {
+    double a = 0.0;
+    for (int c = lane; c < ncta; c += 32) a += __ldcg(part + size_t(c) * pw + j0 + j);
+    a = warp_sum(a);
+    if (lane == 0) out[j] = a;
+  }
+  __syncthreads();
+}
+
+// Partial dots of the CTA's segment: out[j] = V_j[seg] . x[seg] (j < kk), out[pn] = ||x[seg]||^2.
+// x (rpt rows per thread, row l = threadIdx.x * rpt + q) is staged in shared memory; one warp
+// per column, lanes over consecutive rows (coalesced V reads).
+__device__ inline void seg_dots(const double* V, int n, int row0, int nrow, int kk, const double* xr, int rpt,
+                                double* xs, double* out, int pn) {
+  for (int q = 0; q < rpt; ++q) {
+    const int l = threadIdx.x * rpt + q;
+    if (l < nrow) xs[l] = xr[q];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j = w; j <= kk; j += NT / 32) {
+    double p = 0.0;
+    if (j < kk) {
+      const double* v = V + size_t(j) * n + row0;
+      for (int l = lane; l < nrow; l += 32) p = fma(v[l], xs[l], p);
+    } else {
+      for (int l = lane; l < nrow; l += 32) p = fma(xs[l], xs[l], p);
+    }
+    p = warp_sum(p);
+    if (lane == 0) out[j < kk ? j : pn] = p;
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+struct ScanArgs {
+  int P, s, n, nw, seg, rpt, kcap, periodic;
+  const double *fl, *fdinv, *fsup, *fz, *fw;  // factors, factor index = subinterval
+  const double* gam;                          // [P]
+  double h, eta, defl;
+  const double *u0, *Y, *Uold;  // u0 [n]; Y, Uold [P][s][n]
+  double* Unew;                 // [P][s][n]
+  double* delta;                // max |Unew - Uold| (atomic max)
+  double* V;                    // [kcap + 1][n]
+  double* H;                    // (kcap + 1) x kcap, ld kcap + 1
+  double* Zc;                   // [s][kcap]
+  double* partA;                // [nw][pw]
+  double* partB;                // [nw][pw]
+  double* maps;                 // [2][nw][2]
+  double* work;                 // checker: 10 kcap^2
+  int* iwork;                   // checker: kcap
+  unsigned* bar;                // [4]
+  int* flags;                   // [F_NFLAGS]
+};
+
+// Projected check on the checker CTA: returns max_r residual; writes Zc[r][0..K).
+__device__ static double hom_check(const ScanArgs& a, int K, double gam, double beta, double* z, double* zn,
+                                   double* red) {
+  const int ld = a.kcap, ldh = a.kcap + 1;
+  const size_t MM = size_t(ld) * ld;
+  double* S0 = a.work;
+  double* S1 = S0 + MM;
+  double* S2 = S1 + MM;
+  double* WK = S2 + MM;
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int i = t % K, j = t / K;
+    S0[i + size_t(j) * ld] = __ldcg(a.H + i + size_t(j) * ldh);
+  }
+  __syncthreads();
+  cta_identity(K, S1, ld, 1.0);
+  cta_lu(K, S0, ld, a.iwork, red);
+  cta_lu_solve(K, S0, ld, a.iwork, S1, ld, K);
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int i = t % K, j = t / K;
+    S2[i + size_t(j) * ld] = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
+  }
+  __syncthreads();
+  cta_expm_pade13(K, S2, ld, WK, ld, a.iwork, red);
+  const double htail = __ldcg(a.H + K + size_t(K - 1) * ldh);
+  for (int r = threadIdx.x; r < K; r += NT) z[r] = r == 0 ? beta : 0.0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < K; r += NT) a.Zc[r] = z[r];
+  double maxres = 0.0;
+  for (int q = 1; q < a.s; ++q) {
+    for (int r = threadIdx.x; r < K; r += NT) {
+      double v = 0.0;
+      for (int j = 0; j < K; ++j) v = fma(S2[r + size_t(j) * ld], z[j], v);
+      zn[r] = v;
+    }
+    __syncthreads();
+    double xp = 0.0;
+    for (int r = threadIdx.x; r < K; r += NT) {
+      z[r] = zn[r];
+      a.Zc[size_t(q) * a.kcap + r] = zn[r];
+      xp = fma(S1[(K - 1) + size_t(r) * ld], zn[r], xp);
+    }
+    const double x = block_sum(xp, red);
+    maxres = fmax(maxres, fabs(htail * x) / gam);
+  }
+  __syncthreads();
+  return maxres;
+}
+
+__global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
+  __shared__ double red[32];
+  __shared__ Aff wsm[NT / 32 + 1];
+  __shared__ int s_dec;
+  extern __shared__ double dyn[];  // hv, hv2: KSMALL_MAX + 8 each; xs: NT * RPT_MAX
+  double* hv = dyn;
+  double* hv2 = dyn + KSMALL_MAX + 8;
+  double* xs = hv2 + KSMALL_MAX + 8;
+  const int c = blockIdx.x;
+  const bool checker = c == a.nw;
+  const int n = a.n, s = a.s, rpt = a.rpt;
+  const int pw = a.kcap + 8;       // partial row width: [0, kcap] dots, +1 norm, +2 SM dot, +3 beta
+  const int PN = a.kcap + 1, PF = a.kcap + 2, PBETA = a.kcap + 3;
+  unsigned* bar = a.bar;
+  int* fl = a.flags;
+  // own rows: g = row0 + threadIdx.x * rpt + q
+  const int row0 = c * a.seg;
+  const int rend = min(n, row0 + a.seg);
+  double uh[RPT_MAX], xr[RPT_MAX], vr[RPT_MAX];
+
+  // ---- subinterval 0: no homogeneous part; u_{k+1} = u0 + Y, u_hat(T_1) = Y(T_1)
+  if (!checker) {
+    double mx = 0.0, b2 = 0.0;
+    for (int q = 0; q < rpt; ++q) {
+      const int g = row0 + threadIdx.x * rpt + q;
+      uh[q] = 0.0;
+      if (g >= rend) continue;
+      for (int r = 0; r < s; ++r) {
+        const size_t k = size_t(r) * n + g;
+        const double un = a.u0[g] + a.Y[k];
+        mx = fmax(mx, fabs(un - a.Uold[k]));
+        if (!isfinite(un)) mx = INFINITY;
+        a.Unew[k] = un;
+      }
+      uh[q] = a.Y[size_t(s - 1) * n + g];
+      b2 = fma(uh[q], uh[q], b2);
+    }
+    mx = block_max(mx, red);
+    if (threadIdx.x == 0) atomic_max_nonneg(a.delta, mx);
+    b2 = block_sum(b2, red);
+    if (threadIdx.x == 0) a.partA[size_t(c) * pw + PBETA] = b2;
+  }
+  gbar(bar + B_ACNT, bar + B_AGEN, a.nw + 1);
+
+  for (int i = 1; i < a.P; ++i) {
+    grid_reduce(a.partA, pw, a.nw, PBETA, 1, hv);
+    const double beta = sqrt(hv[0]);
+    const double gam = a.gam[i];
+    const size_t fo = size_t(i) * n;
+    gbar(bar + B_ACNT, bar + B_AGEN, a.nw + 1);  // everyone has read beta before partA is reused
+    if (checker) {
+      // ---------------------------------------------------------------- checker CTA
+      if (beta > 0.0) {
+        const double crit = a.eta * beta / ((s - 1) * a.h);
+        double* z = hv;
+        double* zn = hv2;
+        int target = min(4, a.kcap - 1), Kprev = -1;
+        double qprev = -1.0;
+        while (true) {
+          if (threadIdx.x == 0) {
+            int K;
+            while (true) {
+              K = vload(fl + F_STEPS);
+              const int bk = vload(fl + F_BREAK);
+              if (bk > 0) { K = bk; break; }
+              if (K >= target) break;
+              __nanosleep(64);
+            }
+            __threadfence();
+            s_dec = K;
+          }
+          __syncthreads();
+          const int K = s_dec;
+          const bool brk = vload(fl + F_BREAK) == K;
+          const double res = hom_check(a, K, gam, beta, z, zn, red);
+          if (threadIdx.x == 0) {
+            int result = 0;
+            if (brk || res <= crit) result = K;
+            else if (K >= a.kcap - 1) result = -1;
+            if (result != 0) {
+              __threadfence();
+              atomicExch(fl + F_RESULT, result);
+              atomicMax(fl + F_KMAX, K);
+            } else {
+              const double qv = res / crit;
+              int nt = K + 2;
+              if (Kprev >= 0 && qprev > 0.0 && qv > 0.0 && qv < qprev) {
+                const double slope = (log(qv) - log(qprev)) / double(K - Kprev);
+                nt = (int)ceil(K + log(0.5 / qv) / slope);
+              }
+              target = min(max(nt, K + 1), min(2 * K, a.kcap - 1));
+              Kprev = K;
+              qprev = qv;
+            }
+            s_dec = result;
+          }
+          __syncthreads();
+          if (s_dec != 0) break;
+        }
+      }
+    } else {
+      // ---------------------------------------------------------------- workers
+      const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
+      for (int q = 0; q < rpt; ++q) {
+        const int g = row0 + threadIdx.x * rpt + q;
+        vr[q] = uh[q] * inv;
+        if (g < rend) a.V[g] = vr[q];
+      }
+      int Kc = 0;  // converged dimension (0: beta == 0, no homogeneous part)
+      if (beta > 0.0) {
+        for (int k = 0;; ++k) {
+          // A: forward L-solve maps y_g = -l_g y_{g-1} + b_g over own rows
+          Aff m{1.0, 0.0};
+          double fdot = 0.0;
+          for (int q = 0; q < rpt; ++q) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) {
+              m = after(m, Aff{-a.fl[fo + g], vr[q]});
+              if (a.periodic) fdot = fma(a.fw[fo + g], vr[q], fdot);
+            }
+          }
+          Aff tot;
+          const Aff pre = block_excl_scan<false>(m, threadIdx.x, wsm, tot);
+          if (a.periodic) fdot = block_sum(fdot, red);
+          if (threadIdx.x == 0) {
+            a.maps[2 * c] = tot.A;
+            a.maps[2 * c + 1] = tot.B;
+            a.partA[size_t(c) * pw + PF] = fdot;
+            if (c == 0) {  // leader: decision for this step
+              int d = vload(fl + F_RESULT);
+              if (d == 0 && (k >= a.kcap - 1 || vload(fl + F_BREAK) > 0)) {  // no room / invariant space
+                while ((d = vload(fl + F_RESULT)) == 0) __nanosleep(64);
+              }
+              fl[F_DECISION] = d;
+            }
+          }
+          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
+          if (threadIdx.x == 0) s_dec = vload(fl + F_DECISION);
+          __syncthreads();
+          if (s_dec != 0) {
+            Kc = s_dec;
+            break;
+          }
+          // B: carry from lower segments; y; backward maps x_g = -di_g cs_g x_{g+1} + di_g y_g
+          if (threadIdx.x == 0) {
+            double cy = 0.0;
+            for (int cc = 0; cc < c; ++cc) cy = fma(__ldcg(a.maps + 2 * cc), cy, __ldcg(a.maps + 2 * cc + 1));
+            hv[0] = cy;
+          }
+          __syncthreads();
+          double y = fma(pre.A, hv[0], pre.B);
+          for (int q = 0; q < rpt; ++q) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) {
+              y = fma(-a.fl[fo + g], y, vr[q]);
+              xr[q] = y;
+            }
+          }
+          Aff mb{1.0, 0.0};
+          for (int q = rpt - 1; q >= 0; --q) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) {
+              const double dv = a.fdinv[fo + g];
+              mb = after(mb, Aff{-dv * a.fsup[fo + g], dv * xr[q]});
+            }
+          }
+          Aff totb;
+          const Aff preb = block_excl_scan<true>(mb, NT - 1 - threadIdx.x, wsm, totb);
+          if (threadIdx.x == 0) {
+            a.maps[2 * a.nw + 2 * c] = totb.A;
+            a.maps[2 * a.nw + 2 * c + 1] = totb.B;
+          }
+          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
+          // C: carry from upper segments; x; SM correction; pass-1 dots
+          if (threadIdx.x == 0) {
+            double cx = 0.0;
+            for (int cc = a.nw - 1; cc > c; --cc)
+              cx = fma(__ldcg(a.maps + 2 * a.nw + 2 * cc), cx, __ldcg(a.maps + 2 * a.nw + 2 * cc + 1));
+            hv[0] = cx;
+          }
+          if (a.periodic) grid_reduce(a.partA, pw, a.nw, PF, 1, hv2);
+          __syncthreads();
+          const double fsm = a.periodic ? hv2[0] : 0.0;
+          double x = fma(preb.A, hv[0], preb.B);
+          for (int q = rpt - 1; q >= 0; --q) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) {
+              const double dv = a.fdinv[fo + g];
+              x = fma(-dv * a.fsup[fo + g], x, dv * xr[q]);
+              xr[q] = a.periodic ? fma(-fsm, a.fz[fo + g], x) : x;
+            }
+          }
+          const int kk = k + 1;  // columns 0..k
+          seg_dots(a.V, n, row0, rend - row0, kk, xr, rpt, xs, a.partA + size_t(c) * pw, PN);
+          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
+          // D: h = V^T x; x -= V h; pass-2 dots
+          grid_reduce(a.partA, pw, a.nw, 0, kk, hv);
+          grid_reduce(a.partA, pw, a.nw, PN, 1, hv + kk);
+          const double nrm0 = sqrt(hv[kk]);
+          for (int q = 0; q < rpt; ++q) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) {
+              double v = xr[q];
+              for (int j = 0; j < kk; ++j) v = fma(-hv[j], a.V[size_t(j) * n + g], v);
+              xr[q] = v;
+            }
+          }
+          seg_dots(a.V, n, row0, rend - row0, kk, xr, rpt, xs, a.partB + size_t(c) * pw, PN);
+          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
+          // E: second pass, norm, new column
+          grid_reduce(a.partB, pw, a.nw, 0, kk, hv2);
+          grid_reduce(a.partB, pw, a.nw, PN, 1, hv2 + kk);
+          double h2n = 0.0;
+          for (int j = 0; j < kk; ++j) h2n = fma(hv2[j], hv2[j], h2n);
+          const double hn = sqrt(fmax(hv2[kk] - h2n, 0.0));
+          const bool brk = !(hn > a.defl * nrm0);
+          const double sc = brk ? 0.0 : 1.0 / hn;
+          for (int q = 0; q < rpt; ++q) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) {
+              double v = xr[q];
+              for (int j = 0; j < kk; ++j) v = fma(-hv2[j], a.V[size_t(j) * n + g], v);
+              vr[q] = v * sc;
+              a.V[size_t(kk) * n + g] = vr[q];
+            }
+          }
+          if (c == 0) {
+            const int ldh = a.kcap + 1;
+            for (int j = threadIdx.x; j <= kk; j += NT)
+              a.H[j + size_t(k) * ldh] = j < kk ? hv[j] + hv2[j] : (brk ? 0.0 : hn);
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+              if (brk) atomicCAS(fl + F_BREAK, 0, kk);
+              atomicExch(fl + F_STEPS, kk);
+            }
+          }
+        }
+      }
+      if (Kc < 0) {
+        if (c == 0 && threadIdx.x == 0) atomicExch(fl + F_ERR, 1);
+        Kc = 0;
+      }
+      // output: u_hat(t_r) = V Z[r] ; u_{k+1} = u0 + Y + u_hat ; delta ; next u_hat(T_i)
+      for (int t = threadIdx.x; t < s * Kc && Kc > 0 && s * Kc <= KSMALL_MAX; t += NT)
+        hv[t] = __ldcg(a.Zc + size_t(t / Kc) * a.kcap + t % Kc);
+      __syncthreads();
+      double mx = 0.0, b2 = 0.0;
+      const size_t yo = size_t(i) * s * n;
+      for (int q = 0; q < rpt; ++q) {
+        const int g = row0 + threadIdx.x * rpt + q;
+        uh[q] = 0.0;
+        if (g >= rend) continue;
+        for (int r = 0; r < s; ++r) {
+          double w = 0.0;
+          if (s * Kc <= KSMALL_MAX) {
+            for (int j = 0; j < Kc; ++j) w = fma(a.V[size_t(j) * n + g], hv[r * Kc + j], w);
+          } else {
+            for (int j = 0; j < Kc; ++j) w = fma(a.V[size_t(j) * n + g], __ldcg(a.Zc + size_t(r) * a.kcap + j), w);
+          }
+          const size_t kx = yo + size_t(r) * n + g;
+          const double uhr = a.Y[kx] + w;
+          const double un = a.u0[g] + uhr;
+          mx = fmax(mx, fabs(un - a.Uold[kx]));
+          if (!isfinite(un)) mx = INFINITY;
+          a.Unew[kx] = un;
+          if (r == s - 1) uh[q] = uhr;
+        }
+        b2 = fma(uh[q], uh[q], b2);
+      }
+      mx = block_max(mx, red);
+      b2 = block_sum(b2, red);
+      if (threadIdx.x == 0) {
+        atomic_max_nonneg(a.delta, mx);
+        a.partA[size_t(c) * pw + PBETA] = b2;
+      }
+    }
+    // reset the per-subinterval flags (nobody reads them until after the barrier)
+    if (c == 0 && threadIdx.x == 0) {
+      fl[F_STEPS] = 0;
+      fl[F_RESULT] = 0;
+      fl[F_DECISION] = 0;
+      fl[F_BREAK] = 0;
+      __threadfence();
+    }
+    gbar(bar + B_ACNT, bar + B_AGEN, a.nw + 1);
+    if (vload(fl + F_ERR)) return;
+  }
+}
+
+bool hom_scan_ok(int n, int kcap) { return kcap <= KSMALL_MAX && n <= 147 * NT * RPT_MAX; }
+
+size_t hom_scan_bytes(int n, int s, int kcap) {
+  const int nw = std::min(147, cdiv(n, NT));
+  const size_t pw = kcap + 8;
+  return sizeof(double) * (size_t(kcap + 1) * n + size_t(kcap + 1) * kcap + size_t(s) * kcap + 2 * nw * pw +
+                           4 * nw + 10 * size_t(kcap) * kcap) +
+         sizeof(int) * (kcap + F_NFLAGS) + 4 * sizeof(unsigned) + 16 * 256;  // + arena alignment
+}
+
+int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
+                    double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
+                    double* delta, char* ws, size_t ws_bytes) {
+  Arena ar{ws, ws_bytes, 0};
+  ScanArgs a{};
+  a.P = P; a.s = s; a.n = n; a.kcap = kcap; a.periodic = F.periodic;
+  a.nw = std::min(147, cdiv(n, NT));
+  a.seg = cdiv(n, a.nw);
+  a.rpt = cdiv(a.seg, NT);
+  if (a.rpt > RPT_MAX) fail(1, "hom_scan: n too large for the persistent scan");
+  a.fl = F.l; a.fdinv = F.dinv; a.fsup = F.sup; a.fz = F.z; a.fw = F.w;
+  a.gam = gam; a.h = h; a.eta = eta; a.defl = defl;
+  a.u0 = u0; a.Y = Y; a.Uold = Uold; a.Unew = Unew; a.delta = delta;
+  const size_t pw = kcap + 8;
+  a.V = ar.take<double>(size_t(kcap + 1) * n);
+  a.H = ar.take<double>(size_t(kcap + 1) * kcap);
+  a.Zc = ar.take<double>(size_t(s) * kcap);
+  a.partA = ar.take<double>(a.nw * pw);
+  a.partB = ar.take<double>(a.nw * pw);
+  a.maps = ar.take<double>(4 * a.nw);
+  a.work = ar.take<double>(10 * size_t(kcap) * kcap);
+  a.iwork = ar.take<int>(kcap);
+  a.flags = ar.take<int>(F_NFLAGS);
+  a.bar = ar.take<unsigned>(4);
+  if (ar.off > ws_bytes) fail(2, "hom_scan workspace too small");
+  PEXP_CUDA_TRY(cudaMemsetAsync(a.flags, 0, F_NFLAGS * sizeof(int), st));
+  PEXP_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), st));
+  PEXP_CUDA_TRY(cudaMemsetAsync(a.H, 0, size_t(kcap + 1) * kcap * sizeof(double), st));
+  {
+    // algorithmic bytes: the waveform pass (Y, Uold read; Unew write) per subinterval
+    ProfScope ps(PC_SCAN, st, double(P) * s * n * 24.0, 0.0);
+    void* args[] = {&a};
+    const size_t smem = sizeof(double) * (2 * (KSMALL_MAX + 8) + NT * RPT_MAX);
+    static bool attr = false;
+    if (!attr) {
+      PEXP_CUDA_TRY(cudaFuncSetAttribute(k_hom_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    PEXP_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hom_scan, dim3(a.nw + 1), dim3(NT), args, smem, st));
+  }
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+  int hf[F_NFLAGS];
+  PEXP_CUDA_TRY(cudaMemcpyAsync(hf, a.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+  PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hf[F_ERR]) fail(4 /* PEXP_ENOCONV */, "Krylov capacity reached (homogeneous scan)");
+  return hf[F_KMAX];
+}
+
+}  // namespace pexp

@@ -131,6 +131,12 @@ void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, 
 void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, const double* Cfin, double h,
                    double eta, double* coef, double* crit);
 void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax = 0);
+// hom_scan.cu: the Burgers homogeneous scan as one persistent cooperative kernel
+bool hom_scan_ok(int n, int kcap);
+size_t hom_scan_bytes(int n, int s, int kcap);
+int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
+                    double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
+                    double* delta, char* ws, size_t ws_bytes);
 void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double* R, const double* TX, double* CPL,
                            int* Dn, int* Kl, const int* kplast, double* H, long long hs_e, int* live,
                            const int* active);

@@ -707,6 +707,8 @@ struct BurPlan {
   Factors F;
   double *Uk, *Un, *ubar, *G, *Y, *Wh, *uhat, *delta;
   int *iota, *err;
+  char* scan_ws = nullptr;
+  size_t scan_bytes = 0;
   SvdBufs S;
   EbkBufs B, B1;
 };
@@ -739,6 +741,10 @@ static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
   alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, s, s, true, L.S.R, restartable);
   const int k1 = std::min(o.kcap, 512);  // scan: single vectors, short spaces, no restart
   alloc_ebk(ar, L.B1, 1, 1, n, k1, k1, 1, s, s, false, nullptr, false);
+  if (hom_scan_ok(n, k1)) {
+    L.scan_bytes = hom_scan_bytes(n, s, k1);
+    L.scan_ws = ar.take<char>(L.scan_bytes);
+  }
 }
 
 static size_t lin_bytes(const pexp_ctx* c, int P) {
@@ -1031,6 +1037,13 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
         PEXP_CUDA_TRY(cudaMemsetAsync(L.Y, 0, size_t(P) * s * n * sizeof(double), st));
       }
       PEXP_CUDA_TRY(cudaMemsetAsync(L.delta, 0, sizeof(double), st));
+      static const bool noscan = getenv("PEXP_NOSCAN") != nullptr;  // developer switch: host-driven scan
+      if (L.scan_ws && !noscan) {
+        const int k1 = std::min(o.kcap, 512);
+        static const double defl_s = getenv("PEXP_DEFL") ? atof(getenv("PEXP_DEFL")) : 1e-10;
+        max_k = std::max(max_k, launch_hom_scan(st, L.F, L.B.gam, P, s, n, k1, h, eta, defl_s, u0, L.Y, L.Uk, L.Un,
+                                                L.delta, L.scan_ws, L.scan_bytes));
+      } else
       for (int i = 0; i < P; ++i) {
         const size_t off = size_t(i) * s * n;
         if (i == 0) {
