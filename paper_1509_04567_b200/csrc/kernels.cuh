@@ -85,10 +85,11 @@ struct StepArgs {
   const int* active;
   double defl, piv_tol;
   int rc;
+  int cs;                         // CTAs per evaluation (thread-block cluster)
 };
 
 // arnoldi.cu
-bool arnoldi_fused_ok(int m, int kcap);
+bool arnoldi_fused_ok(int m, int nv);
 void launch_arnoldi_step(cudaStream_t st, StepArgs a);
 
 // tridiag.cu

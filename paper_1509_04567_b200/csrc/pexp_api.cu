@@ -257,7 +257,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   launch_fill_i32(st, B.conv, E, 0);
   PEXP_LAUNCH_CHECK();
   static const bool nofuse = getenv("PEXP_NOFUSE") != nullptr;  // developer switch
-  const bool fused = !nofuse && E >= 512 && n <= 16384 && arnoldi_fused_ok(m, kcap);
+  // fused cluster step (arnoldi.cu) whenever the step's panels fit shared memory
   int steps = 0, last_check = -1;
   int next_check = std::max(4, 2 * m);
   // deflation: a new column is dropped when BCGS leaves < 1e-10 of ||(I - gamma A)^{-1} v|| (well
@@ -433,7 +433,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     }
     const int b = steps, nv = (b + 1) * m;
     const long long ws_e = B.vs_e;
-    if (fused) {  // one CTA per evaluation does the whole step (arnoldi.cu)
+    if (!nofuse && arnoldi_fused_ok(m, nv)) {  // one cluster per evaluation does the whole step
       StepArgs sa{};
       sa.E = E; sa.n = n; sa.m = m; sa.b = b; sa.kcap = kcap; sa.periodic = F.periodic;
       sa.V = B.V; sa.vs_e = B.vs_e; sa.H = B.H; sa.hs_e = B.hs_e; sa.live = B.live; sa.fidx = B.fidx;

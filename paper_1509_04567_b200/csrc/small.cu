@@ -11,6 +11,7 @@
 //   * k_small_problem   : projected SaI problem: H^{-1}, A_hat = (I - H^{-1})/gamma, Pade-13
 //                         exponential of the augmented matrix, exact chaining over the cubic
 //                         pieces, residual norms at every node (subsystem 4)
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include "common.cuh"
 #include "dense.cuh"
@@ -19,6 +20,14 @@
 namespace pexp {
 
 constexpr int MAXS = 64;
+namespace cg = cooperative_groups;
+// k_small_problem dynamic shared memory: replicated state 2*KSMALL_MAX, row partials CH_PSUM,
+// own rows KSMALL_MAX, residual ring 2*MAXS, then the CTA's slice of F (FS_CAP doubles)
+constexpr int CH_PSUM = KSMALL_MAX + 32;
+constexpr size_t SP_DYN = 180 * 1024;
+constexpr size_t HOM_DYN = 160 * 1024;
+constexpr size_t HOM_FS_CAP = HOM_DYN / 8 - 2 * 256;
+constexpr size_t FS_CAP = SP_DYN / 8 - (2 * KSMALL_MAX + CH_PSUM + KSMALL_MAX + 2 * MAXS);
 double g_piv_tol = getenv("PEXP_PIVTOL") ? atof(getenv("PEXP_PIVTOL")) : 1e-14;  // developer override
 constexpr size_t SM2 = 2 * MAXS * (MAXS + 1) * sizeof(double);  // two padded 64x64 tiles
 
@@ -71,7 +80,11 @@ __device__ inline void sym_schur2(double app, double aqq, double apq, double& c,
 // G: [E][s][s] (col-major s x s).  Pass `pass` of the two-pass SVD: keep eigenpairs with
 // sigma_i = sqrt(lambda_i) > theta*sigma_max(pass) and > 0.5*tau*sigma1 (sigma1 from pass 0),
 // write Msel[:, off + c] = q_i / sigma_i (all other columns 0), off += kept.
-__global__ void __launch_bounds__(PEXP_THREADS)
+// Parallel cyclic Jacobi (round-robin pairing): per round the Ne/2 disjoint rotations are
+// computed by Ne/2 threads, then every thread applies both rotations to ONE 2x2 block
+// (rows {p_k,q_k} x columns {p_l,q_l}) of A and one column pair of Q — two barriers per round.
+constexpr int EIG_THREADS = 1024;
+__global__ void __launch_bounds__(EIG_THREADS)
 k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off, double* sigma1,
                  int pass, double tau, double theta, const int* active) {
   const int e = blockIdx.x;
@@ -82,13 +95,14 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
   __shared__ int rp[MAXS / 2], rq[MAXS / 2];
   __shared__ int perm[MAXS];
   __shared__ double red[32];
+  __shared__ int s_sel[2];
   double* M = Msel + size_t(e) * s * s;
 
   if (active && !active[e]) {
     for (int i = threadIdx.x; i < s * s; i += blockDim.x) M[i] = 0.0;
     return;
   }
-  const int Ne = s + (s & 1);
+  const int Ne = s + (s & 1), half = Ne / 2;
   const double* Ge = G + size_t(e) * s * s;
   for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
     int i = idx % Ne, j = idx / Ne;
@@ -96,18 +110,22 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
     Q[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  // rotation floor: the Gram carries absolute rounding ~eps*lambda_max, so pairs below
-  // 1e-18*max_i a_ii are decoupled as far as the data allows (relative accuracy is neither
-  // available nor needed: pass 2 and the final SVD of C = U^T G make the basis exact)
+  // rotation floor: a rotation itself perturbs every rotated entry by ~eps*max_i a_ii, so
+  // pairs below 1e-15*max_i a_ii (~4.5 eps) are decoupled as far as the rounding allows.
+  // (A floor below the rounding level never terminates: 40 sweeps instead of 7-8 on the
+  // rank-deficient, noisy C2 Grams.)  Relative accuracy of the tiny eigenpairs is neither
+  // available from a Gram nor needed: pass 2 and the final SVD of C = U^T G make the basis exact.
   double dmax = 0.0;
   for (int i = threadIdx.x; i < s; i += blockDim.x) dmax = fmax(dmax, A[i][i]);
-  const double afloor = fmax(1e-18 * block_max(dmax, red), 1e-300);
+  const double afloor = fmax(1e-15 * block_max(dmax, red), 1e-300);
   __shared__ int s_rot;
+  const int bk = threadIdx.x / half, bl = threadIdx.x % half;  // this thread's 2x2 block
+  const bool has_blk = threadIdx.x < half * half;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) s_rot = 0;
     __syncthreads();
     for (int r = 0; r < Ne - 1; ++r) {
-      if (threadIdx.x < Ne / 2) {
+      if (threadIdx.x < half) {
         int p, q;
         jacobi_pair(Ne, r, threadIdx.x, p, q);
         double c = 1.0, sn = 0.0;
@@ -119,19 +137,19 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
         rp[threadIdx.x] = p; rq[threadIdx.x] = q; rc[threadIdx.x] = c; rs[threadIdx.x] = sn;
       }
       __syncthreads();
-      for (int idx = threadIdx.x; idx < (Ne / 2) * Ne; idx += blockDim.x) {  // rows
-        int k = idx / Ne, j = idx % Ne, p = rp[k], q = rq[k];
-        double c = rc[k], sn = rs[k], ap = A[p][j], aq = A[q][j];
-        A[p][j] = c * ap - sn * aq;
-        A[q][j] = sn * ap + c * aq;
+      if (has_blk) {
+        const int pk = rp[bk], qk = rq[bk], pl = rp[bl], ql = rq[bl];
+        const double ck = rc[bk], sk = rs[bk], cl = rc[bl], sl = rs[bl];
+        const double a = A[pk][pl], b = A[pk][ql], c_ = A[qk][pl], d = A[qk][ql];
+        // rows: r_p' = c r_p - s r_q, r_q' = s r_p + c r_q ; then the same on the columns
+        const double a1 = ck * a - sk * c_, b1 = ck * b - sk * d, c1 = sk * a + ck * c_, d1 = sk * b + ck * d;
+        double a2 = cl * a1 - sl * b1, b2 = sl * a1 + cl * b1, c2 = cl * c1 - sl * d1, d2 = sl * c1 + cl * d1;
+        if (bk == bl && sk != 0.0) { b2 = 0.0; c2 = 0.0; }  // the annihilated pair (classical Jacobi)
+        A[pk][pl] = a2; A[pk][ql] = b2; A[qk][pl] = c2; A[qk][ql] = d2;
       }
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < (Ne / 2) * Ne; idx += blockDim.x) {  // columns
-        int k = idx / Ne, j = idx % Ne, p = rp[k], q = rq[k];
-        double c = rc[k], sn = rs[k], ap = A[j][p], aq = A[j][q];
-        A[j][p] = c * ap - sn * aq;
-        A[j][q] = sn * ap + c * aq;
-        double qp = Q[j][p], qq = Q[j][q];
+      for (int idx = threadIdx.x; idx < half * Ne; idx += blockDim.x) {  // Q <- Q J (column pairs)
+        const int l = idx / Ne, j = idx % Ne, p = rp[l], q = rq[l];
+        const double c = rc[l], sn = rs[l], qp = Q[j][p], qq = Q[j][q];
         Q[j][p] = c * qp - sn * qq;
         Q[j][q] = sn * qp + c * qq;
       }
@@ -141,14 +159,15 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
     __syncthreads();  // every thread has read s_rot before thread 0 resets it
     if (!rotated) break;
   }
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < s; ++i) perm[i] = i;
-    for (int i = 0; i < s; ++i) {
-      int b = i;
-      for (int j = i + 1; j < s; ++j)
-        if (A[perm[j]][perm[j]] > A[perm[b]][perm[b]]) b = j;
-      int t = perm[i]; perm[i] = perm[b]; perm[b] = t;
+  // descending order of the eigenvalues (stable rank sort, one thread per eigenvalue)
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    const double li = A[i][i];
+    int rank = 0;
+    for (int j = 0; j < s; ++j) {
+      const double lj = A[j][j];
+      rank += (lj > li) || (lj == li && j < i);
     }
+    perm[rank] = i;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < s; i += blockDim.x) lam_out[size_t(e) * s + i] = fmax(A[perm[i]][perm[i]], 0.0);
@@ -165,11 +184,11 @@ k_sym_eig_select(int s, const double* G, double* lam_out, double* Msel, int* off
       ++kept;
     }
     off[e] = o + kept;
-    rq[0] = o;
-    rq[1] = kept;
+    s_sel[0] = o;
+    s_sel[1] = kept;
   }
   __syncthreads();
-  const int o = rq[0], kept = rq[1];
+  const int o = s_sel[0], kept = s_sel[1];
   for (int idx = threadIdx.x; idx < kept * s; idx += blockDim.x) {
     int c = idx / s, i = idx % s;
     double sg = sqrt(fmax(A[perm[c]][perm[c]], 0.0));
@@ -536,10 +555,7 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
   __shared__ int tidx[MAXS], lpos[MAXS];
   __shared__ int s_K, s_mt, s_ml;
   __shared__ double red[32];
-  __shared__ double xs[MAXS], ts[MAXS];
-  extern __shared__ double zsm[];  // 2 * KSMALL_MAX doubles
-  double* z = zsm;
-  double* zn = zsm + KSMALL_MAX;
+  extern __shared__ double zsm[];  // SP_DYN bytes: chaining state, partials, F slice
   const Grp g = this_grp();
   const int slot = blockIdx.x / g.size, nslot = gridDim.x / g.size;
   double* S0 = a.work + slot * a.work_slot;
@@ -623,23 +639,34 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     if (a.kplast && g.rank == 0 && threadIdx.x == 0) a.kplast[e] = Kp;
     grp_sync(g);
     cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red, g);
-    if (g.rank == 0) {  // chaining and residuals: rank 0 of the cluster
-    const int np = a.npieces ? a.npieces[e] : a.npieces_const;
-    for (int r = threadIdx.x; r < Dz; r += blockDim.x) z[r] = (!forced && r == 0) ? a.beta[e] : 0.0;
-    double* Ze = a.Z + e * a.zs_e;
-    for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
-    __syncthreads();
-    for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[idx[r]] = z[D + r];
-    double maxres = 0.0;
-    const double* cf = forced ? a.coef + size_t(e) * (a.s - 1) * 4 * m : nullptr;
-    for (int i = 0; i < np; ++i) {
-      __syncthreads();
-      for (int r = threadIdx.x; r < Dz; r += blockDim.x) {
-        double v = 0.0;
-        for (int j = 0; j < Dz; ++j) v = fma(S2[r + size_t(j) * ld], z[j], v);
-        if (forced) {
+    // ---- exact chaining over the np pieces (rows split over the group, one group barrier per
+    // piece): z_{i+1} = F z_i + f_i with F = e^{h N}[0:Dz, 0:Dz] and the piece forcing
+    // f_i = sum_q h^q B_q c_{i,q}; the state is replicated in every CTA's shared memory (each CTA
+    // publishes its rows through DSMEM).  Residual at every node (DESIGN.md §3 #6): ts = R z[D:],
+    // R = H_tail H^{-1}[last block rows, :] (mt x Kp), reduced per piece from per-CTA partials.
+    {
+      cg::cluster_group cl = cg::this_cluster();
+      const int np = a.npieces ? a.npieces[e] : a.npieces_const;
+      const int rs = (Dz + g.size - 1) / g.size;
+      const int r0 = min(Dz, g.rank * rs), nr = min(Dz, r0 + rs) - r0;
+      const int nrt = (nr + 31) / 32, jp = max(1, (PEXP_THREADS / 32) / max(nrt, 1)), jper = (Dz + jp - 1) / jp;
+      double* zb0 = zsm;
+      double* zb1 = zsm + KSMALL_MAX;
+      double* psum = zsm + 2 * KSMALL_MAX;  // [jp][nrt*32]
+      double* zown = psum + CH_PSUM;        // [nr]
+      double* ring = zown + KSMALL_MAX;     // [2][MAXS] residual partials (read remotely by rank 0)
+      double* Fs = ring + 2 * MAXS;         // own rows of F, column-major (ld nr), if they fit
+      const bool fsm = size_t(nr) * Dz <= FS_CAP;
+      double* Fo = WK;                      // [np][Dz] forcing of every piece
+      double* Rg = WK + size_t(np) * Dz;    // [mt][Kp]
+      double* Ze = a.Z + e * a.zs_e;
+      const double* cf = forced ? a.coef + size_t(e) * (a.s - 1) * 4 * m : nullptr;
+      for (int t = threadIdx.x + g.rank * blockDim.x; t < a.nout * a.kcap; t += blockDim.x * g.size) Ze[t] = 0.0;
+      if (forced)
+        for (int t = threadIdx.x; t < nr * np; t += blockDim.x) {
+          const int r = r0 + t % nr, i = t / nr;
           const double* ci = cf + size_t(i) * 4 * m;
-          double hq = 1.0;
+          double v = 0.0, hq = 1.0;
           for (int q = 0; q < 4; ++q) {
             const double* B = S2 + size_t(Dz + q * m) * ld;
             double acc = 0.0;
@@ -647,50 +674,98 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
             v = fma(hq, acc, v);
             hq *= a.h;
           }
+          Fo[size_t(i) * Dz + r] = v;
         }
-        zn[r] = v;
+      for (int t = threadIdx.x; t < mt * nr; t += blockDim.x) {
+        const int r = r0 + t % nr, tc = t / nr;
+        if (r < D) continue;
+        const int j = r - D;
+        double v = 0.0;
+        for (int c = 0; c < ml; ++c)
+          v = fma(He[tidx[tc] + size_t(idx[lpos[c]]) * a.ldh], S1[lpos[c] + size_t(j) * ld], v);
+        Rg[size_t(tc) * Kp + j] = v;
       }
-      __syncthreads();
-      for (int r = threadIdx.x; r < Dz; r += blockDim.x) z[r] = zn[r];
-      __syncthreads();
-      const int node = i + 1;
-      if (node % a.out_stride == 0 && node / a.out_stride < a.nout)
-        for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[size_t(node / a.out_stride) * a.kcap + idx[r]] = z[D + r];
-      // residual ||r(t)|| = (1/gamma) || (I - gamma A) Vtail Htail x ||, x = (H^{-1} z)[last block]
-      if (mt > 0) {
-        for (int c = threadIdx.x; c < ml; c += blockDim.x) {
-          double v = 0.0;
-          const int row = lpos[c];
-          for (int j = 0; j < Kp; ++j) v = fma(S1[row + size_t(j) * ld], z[D + j], v);
-          xs[c] = v;
+      if (fsm)
+        for (int t = threadIdx.x; t < nr * Dz; t += blockDim.x) {
+          const int rl = t % nr, j = t / nr;
+          Fs[t] = S2[r0 + rl + size_t(j) * ld];
         }
-        __syncthreads();
-        for (int tc = threadIdx.x; tc < mt; tc += blockDim.x) {
-          double v = 0.0;
-          for (int c = 0; c < ml; ++c) v = fma(He[tidx[tc] + size_t(idx[lpos[c]]) * a.ldh], xs[c], v);
-          ts[tc] = v;
-        }
-        __syncthreads();
-        double part = 0.0;
-        if (a.stop_rule == 1) {  // ||(I - gamma A) Vtail t||^2 = t^T Gt t
-          const double* Gt = a.Gt + e * a.gts_e;
-          for (int p = threadIdx.x; p < mt * mt; p += blockDim.x) {
-            int i1 = p % mt, i2 = p / mt;
-            part += ts[i1] * Gt[(tidx[i1] - K) + size_t(tidx[i2] - K) * m] * ts[i2];
+      for (int r = threadIdx.x; r < Dz; r += blockDim.x) zb0[r] = (!forced && r == 0) ? a.beta[e] : 0.0;
+      grp_sync(g);
+      for (int rl = threadIdx.x; rl < nr; rl += blockDim.x)
+        if (r0 + rl >= D) Ze[idx[r0 + rl - D]] = zb0[r0 + rl];
+      const double* Fp = fsm ? Fs : S2 + r0;
+      const int ldf = fsm ? nr : ld;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      double maxres = 0.0;
+      __shared__ double tsum[MAXS];
+      for (int i = 0; i < np; ++i) {
+        const double* cur = (i & 1) ? zb1 : zb0;
+        double* nxt = (i & 1) ? zb0 : zb1;
+        for (int task = warp; task < nrt * jp; task += PEXP_THREADS / 32) {
+          const int rt = task % nrt, p = task / nrt, rl = rt * 32 + lane;
+          const int j0 = p * jper, j1 = min(Dz, j0 + jper);
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          if (rl < nr) {
+            const double* fr = Fp + rl;
+            int j = j0;
+            for (; j + 3 < j1; j += 4) {
+              s0 = fma(fr[size_t(j) * ldf], cur[j], s0);
+              s1 = fma(fr[size_t(j + 1) * ldf], cur[j + 1], s1);
+              s2 = fma(fr[size_t(j + 2) * ldf], cur[j + 2], s2);
+              s3 = fma(fr[size_t(j + 3) * ldf], cur[j + 3], s3);
+            }
+            for (; j < j1; ++j) s0 = fma(fr[size_t(j) * ldf], cur[j], s0);
           }
-        } else {                 // ||Vtail t||^2 = ||t||^2 (orthonormal tail)
-          for (int p = threadIdx.x; p < mt; p += blockDim.x) part += ts[p] * ts[p];
+          psum[p * nrt * 32 + rl] = (s0 + s1) + (s2 + s3);
         }
-        double r2 = block_sum(part, red);
-        maxres = fmax(maxres, sqrt(fmax(r2, 0.0)) / gam);
+        __syncthreads();
+        const int node = i + 1;
+        const bool out = node % a.out_stride == 0 && node / a.out_stride < a.nout;
+        for (int rl = threadIdx.x; rl < nr; rl += blockDim.x) {
+          double v = forced ? Fo[size_t(i) * Dz + r0 + rl] : 0.0;
+          for (int p = 0; p < jp; ++p) v += psum[p * nrt * 32 + rl];
+          zown[rl] = v;
+          for (int q = 0; q < g.size; ++q) (g.size > 1 ? cl.map_shared_rank(nxt, q) : nxt)[r0 + rl] = v;
+          if (out && r0 + rl >= D) Ze[size_t(node / a.out_stride) * a.kcap + idx[r0 + rl - D]] = v;
+        }
+        __syncthreads();
+        if (mt > 0)
+          for (int tc = warp; tc < mt; tc += PEXP_THREADS / 32) {
+            double sacc = 0.0;
+            for (int rl = lane; rl < nr; rl += 32)
+              if (r0 + rl >= D) sacc = fma(Rg[size_t(tc) * Kp + r0 + rl - D], zown[rl], sacc);
+            sacc = warp_sum(sacc);
+            if (lane == 0) ring[(i & 1) * MAXS + tc] = sacc;
+          }
+        grp_sync(g);
+        if (g.rank == 0 && mt > 0) {  // residual of node i+1 (partials stable until the next barrier)
+          for (int tc = threadIdx.x; tc < mt; tc += blockDim.x) {
+            double v = 0.0;
+            for (int q = 0; q < g.size; ++q) v += (g.size > 1 ? cl.map_shared_rank(ring, q) : ring)[(i & 1) * MAXS + tc];
+            tsum[tc] = v;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            double r2 = 0.0;
+            if (a.stop_rule == 1) {  // ||(I - gamma A) Vtail t||^2 = t^T Gt t
+              const double* Gt = a.Gt + e * a.gts_e;
+              for (int i1 = 0; i1 < mt; ++i1)
+                for (int i2 = 0; i2 < mt; ++i2)
+                  r2 += tsum[i1] * Gt[(tidx[i1] - K) + size_t(tidx[i2] - K) * m] * tsum[i2];
+            } else {                 // ||Vtail t||^2 = ||t||^2 (orthonormal tail)
+              for (int i1 = 0; i1 < mt; ++i1) r2 += tsum[i1] * tsum[i1];
+            }
+            maxres = fmax(maxres, sqrt(fmax(r2, 0.0)) / gam);
+          }
+        }
       }
-    }
-    if (threadIdx.x == 0) {
-      a.res[e] = maxres;
-      int cv = (mt == 0) || (maxres <= a.crit[e]);
-      a.conv[e] = cv;
-      if (cv && a.kfin) a.kfin[e] = K;
-    }
+      if (g.rank == 0 && threadIdx.x == 0) {
+        a.res[e] = maxres;
+        int cv = (mt == 0) || (maxres <= a.crit[e]);
+        a.conv[e] = cv;
+        if (cv && a.kfin) a.kfin[e] = K;
+      }
     }  // rank 0
     grp_sync(g);
   }
@@ -745,7 +820,6 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
   __shared__ int tidx[MAXS], lpos[MAXS];
   __shared__ int s_K, s_mt, s_ml;
   __shared__ double red[32];
-  __shared__ double xs[16 * 16], ts[16 * 16];  // (ml, mt <= m <= 16) x m
   const Grp g = this_grp();
   const int slot = blockIdx.x / g.size, nslot = gridDim.x / g.size;
   double* S0 = a.work + slot * a.work_slot;
@@ -791,59 +865,94 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
     }
     grp_sync(g);
     cta_expm_pade13(Kp, S2, ld, WK, ld, piv, red, g);
-    // Z (Kp x m) and Zn in the (now free) expm workspace
-    double* Z = WK;
-    double* Zn = WK + size_t(ld) * m;
+    // ---- propagation Z_q = F Z_{q-1} (Kp x m), rows split over the group, one group barrier
+    // per step.  The replicated state lives in the slot's global workspace (L2; read with
+    // __ldcg across CTAs), each CTA accumulates its own rows of every leg's outputs and a partial
+    // of the residual ts = R Z_q (R = H_tail H^{-1}[last block rows, :], mt x Kp) per leg.
+    cg::cluster_group cl = cg::this_cluster();
+    const int rs = (Kp + g.size - 1) / g.size;
+    const int r0 = min(Kp, g.rank * rs), nr = min(Kp, r0 + rs) - r0;
+    double* Zb0 = WK;                          // [m][Kp]
+    double* Zb1 = WK + size_t(Kp) * m;         // [m][Kp]
+    double* Rg = Zb1 + size_t(Kp) * m;         // [mt][Kp]
+    double* zown = Rg + size_t(mt) * Kp;       // [m][nr] per CTA (disjoint rows)
+    extern __shared__ double hsm[];            // HOM_DYN bytes: residual ring, then the F slice
+    double* ring = hsm;                        // [2][16*16]
+    double* Fs = hsm + 2 * 256;                // own rows of F, column-major (ld nr), if they fit
+    const bool fsm = size_t(nr) * Kp <= HOM_FS_CAP;
     const double* R0 = a.R0 + size_t(e) * m * m;
     double* Ze = a.Z + e * a.zs_e;
-    if (g.rank == 0) {
-      for (int t = threadIdx.x; t < Kp * m; t += blockDim.x) {
-        int r = t % Kp, c = t / Kp;
-        Z[r + size_t(c) * ld] = idx[r] < m ? R0[idx[r] + c * m] : 0.0;
-      }
-      for (int t = threadIdx.x; t < a.nout * a.kcap; t += blockDim.x) Ze[t] = 0.0;
+    for (int t = threadIdx.x; t < nr * m; t += blockDim.x) {
+      const int r = r0 + t % nr, c = t / nr;
+      Zb0[r + size_t(c) * Kp] = idx[r] < m ? R0[idx[r] + c * m] : 0.0;
     }
+    for (int t = threadIdx.x + g.rank * blockDim.x; t < a.nout * a.kcap; t += blockDim.x * g.size) Ze[t] = 0.0;
+    for (int t = threadIdx.x; t < mt * nr; t += blockDim.x) {
+      const int j = r0 + t % nr, tc = t / nr;
+      double v = 0.0;
+      for (int c = 0; c < ml; ++c)
+        v = fma(He[tidx[tc] + size_t(idx[lpos[c]]) * a.ldh], S1[lpos[c] + size_t(j) * ld], v);
+      Rg[size_t(tc) * Kp + j] = v;
+    }
+    if (fsm)
+      for (int t = threadIdx.x; t < nr * Kp; t += blockDim.x) Fs[t] = S2[r0 + t % nr + size_t(t / nr) * ld];
     grp_sync(g);
+    const double* Fp = fsm ? Fs : S2 + r0;
+    const int ldf = fsm ? nr : ld;
     const int j0 = (e % a.groups) * m;
     const double* cc = a.critc + size_t(e) * m;
     const int* hc = a.horc + size_t(e) * m;
     int qmax = 0;
     for (int c = 0; c < m; ++c) qmax = max(qmax, hc[c]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double worst = 0.0;
     for (int q = 1; q <= qmax; ++q) {
-      cta_gemm(Kp, m, Kp, 1.0, S2, ld, Z, ld, 0.0, Zn, ld, g);
-      double* tmp = Z; Z = Zn; Zn = tmp;
-      if (g.rank != 0) continue;  // residuals and accumulation on rank 0
-      if (mt > 0) {
-        for (int t = threadIdx.x; t < ml * m; t += blockDim.x) {
-          int cidx = t % ml, c = t / ml;
-          double v = 0.0;
-          for (int j = 0; j < Kp; ++j) v = fma(S1[lpos[cidx] + size_t(j) * ld], Z[j + size_t(c) * ld], v);
-          xs[cidx + c * 16] = v;
+      const double* cur = (q & 1) ? Zb0 : Zb1;
+      double* nxt = (q & 1) ? Zb1 : Zb0;
+      for (int t = threadIdx.x; t < nr * m; t += blockDim.x) {
+        const int rl = t % nr, c = t / nr;
+        const double* fr = Fp + rl;
+        const double* zc = cur + size_t(c) * Kp;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int j = 0;
+        for (; j + 3 < Kp; j += 4) {
+          s0 = fma(fr[size_t(j) * ldf], __ldcg(zc + j), s0);
+          s1 = fma(fr[size_t(j + 1) * ldf], __ldcg(zc + j + 1), s1);
+          s2 = fma(fr[size_t(j + 2) * ldf], __ldcg(zc + j + 2), s2);
+          s3 = fma(fr[size_t(j + 3) * ldf], __ldcg(zc + j + 3), s3);
         }
-        __syncthreads();
-        for (int t = threadIdx.x; t < mt * m; t += blockDim.x) {
-          int tc = t % mt, c = t / mt;
-          double v = 0.0;
-          for (int cidx = 0; cidx < ml; ++cidx)
-            v = fma(He[tidx[tc] + size_t(idx[lpos[cidx]]) * a.ldh], xs[cidx + c * 16], v);
-          ts[tc + c * 16] = v;
+        for (; j < Kp; ++j) s0 = fma(fr[size_t(j) * ldf], __ldcg(zc + j), s0);
+        const double v = (s0 + s1) + (s2 + s3);
+        __stcg(nxt + r0 + rl + size_t(c) * Kp, v);
+        zown[r0 + rl + size_t(c) * Kp] = v;
+        if (q <= hc[c]) Ze[size_t(j0 + c + q) * a.kcap + idx[r0 + rl]] += v;
+      }
+      __syncthreads();
+      if (mt > 0)
+        for (int pr = warp; pr < mt * m; pr += PEXP_THREADS / 32) {
+          const int tc = pr % mt, c = pr / mt;
+          double sacc = 0.0;
+          if (q <= hc[c])
+            for (int rl = lane; rl < nr; rl += 32)
+              sacc = fma(Rg[size_t(tc) * Kp + r0 + rl], zown[r0 + rl + size_t(c) * Kp], sacc);
+          sacc = warp_sum(sacc);
+          if (lane == 0) ring[(q & 1) * 256 + pr] = sacc;
         }
-        __syncthreads();
+      grp_sync(g);
+      if (g.rank == 0 && mt > 0) {  // per-leg residuals of step q (partials stable until the next barrier)
         double wq = 0.0;
         for (int c = threadIdx.x; c < m; c += blockDim.x) {
           if (q > hc[c]) continue;
           double s2 = 0.0;
-          for (int tc = 0; tc < mt; ++tc) s2 += ts[tc + c * 16] * ts[tc + c * 16];
+          for (int tc = 0; tc < mt; ++tc) {
+            double v = 0.0;
+            for (int qq = 0; qq < g.size; ++qq)
+              v += (g.size > 1 ? cl.map_shared_rank(ring, qq) : ring)[(q & 1) * 256 + tc + c * mt];
+            s2 += v * v;
+          }
           wq = fmax(wq, sqrt(s2) / gam / cc[c]);
         }
         worst = fmax(worst, block_max(wq, red));
-      }
-      for (int c = 0; c < m; ++c) {
-        if (q > hc[c]) continue;
-        const int i = j0 + c + q;
-        for (int r = threadIdx.x; r < Kp; r += blockDim.x) Ze[size_t(i) * a.kcap + idx[r]] += Z[r + size_t(c) * ld];
-        __syncthreads();
       }
     }
     if (g.rank == 0 && threadIdx.x == 0) {
@@ -861,7 +970,7 @@ void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
   if (a.m > 16) fail(1, "grouped legs: at most 16 legs per group");
   ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * a.K * a.K * a.K));
   const int ncl = std::min(a.E, nslots);
-  launch_clustered(k_small_hom, ncl, cluster_size_for(ncl), 0, st, a);
+  launch_clustered(k_small_hom, ncl, cluster_size_for(ncl), HOM_DYN, st, a);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }
@@ -885,7 +994,7 @@ k_expm_batched(int E, int N, const double* A, double* X, double* work, long long
 void launch_sym_eig_select(cudaStream_t st, int E, int s, const double* G, double* lam, double* Msel,
                            int* off, double* sigma1, int pass, double tau, double theta, const int* active) {
   ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
-  k_sym_eig_select<<<E, PEXP_THREADS, SM2, st>>>(s, G, lam, Msel, off, sigma1, pass, tau, theta, active);
+  k_sym_eig_select<<<E, EIG_THREADS, SM2, st>>>(s, G, lam, Msel, off, sigma1, pass, tau, theta, active);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }
@@ -931,7 +1040,7 @@ void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, 
 
 void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax) {
   if (Dmax + a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
-  size_t smem = 2 * KSMALL_MAX * sizeof(double);
+  size_t smem = SP_DYN;
   {
   const double N = Dmax + a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
   ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
@@ -954,7 +1063,8 @@ void small_init() {
   cudaFuncSetAttribute(k_sym_eig_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_block_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_onesided_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
-  cudaFuncSetAttribute(k_small_problem, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KSMALL_MAX * 8);
+  cudaFuncSetAttribute(k_small_problem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_DYN);
+  cudaFuncSetAttribute(k_small_hom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HOM_DYN);
   cudaFuncSetAttribute(k_spline, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * 64 * 8);
 }
 
