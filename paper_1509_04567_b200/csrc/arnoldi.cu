@@ -25,11 +25,15 @@ namespace cg = cooperative_groups;
 namespace pexp {
 
 struct SmemT {
-  double *Hs, *Pp, *Cx, *Cy, *G, *Gp, *Rinv, *Mc, *S, *Xw, *Lp, *d, *n0, *n0p, *xch;
-  int ldc;  // chunk leading dimension (rc + 1)
+  double *Hs, *Pp, *Cx, *Cy, *G, *Gp, *Rinv, *Mc, *S, *Xw, *Lp, *d, *n0, *n0p, *xch, *Ws;
+  int ldc;   // chunk leading dimension (rc + 1)
+  int gpar;  // which of the two Gram partial buffers the next cluster reduction uses
 };
 
 constexpr int RC = 256;  // rows per staged chunk of the projections (8 rows per lane)
+
+// rows of every column owned by one CTA of a cs-CTA cluster (multiple of 32)
+__host__ __device__ inline int step_rows(int n, int cs) { return ((n + cs - 1) / cs + 31) / 32 * 32; }
 
 __device__ inline void cl_sync(cg::cluster_group& cl, int cs) {
   if (cs > 1)
@@ -39,6 +43,9 @@ __device__ inline void cl_sync(cg::cluster_group& cl, int cs) {
 }
 
 // out[i] = sum over the cluster's CTAs (rank order) of part[i], i < cnt.  part and out distinct.
+// One cluster barrier: a CTA may overwrite `part` only after the NEXT cluster barrier (all remote
+// reads of this reduction happen before their reader arrives there), so consecutive reductions
+// alternate buffers (Gram partials) or are separated by other reductions (V^T W partials).
 __device__ inline void cl_allreduce(cg::cluster_group& cl, int cs, double* part, double* out, int cnt) {
   cl_sync(cl, cs);
   for (int i = threadIdx.x; i < cnt; i += PEXP_THREADS) {
@@ -46,15 +53,15 @@ __device__ inline void cl_allreduce(cg::cluster_group& cl, int cs, double* part,
     for (int q = 0; q < cs; ++q) s += (cs > 1 ? cl.map_shared_rank(part, q) : part)[i];
     out[i] = s;
   }
-  cl_sync(cl, cs);
+  __syncthreads();
 }
 
 // Partial Hp[a + c*nv] = sum over this CTA's rows of V[a][r] W[c][r]  (a < nv, c < m).
 // The W chunk (RC rows) is staged in shared memory; every warp streams two V columns at a time
 // (16 independent 256-B loads in flight per lane) and reduces with shuffles.
 template <int MB>
-__device__ inline void cta_vtw(int ld, int rows, const double* V, int nv, const double* W, int m, double* Hp,
-                               double* Cb, int ldc) {
+__device__ inline void cta_vtw(int ld, int ldw, int rows, const double* V, int nv, const double* W, int m,
+                               double* Hp, double* Cb, int ldc) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = PEXP_THREADS / 32;
   constexpr int U = RC / 32;
   for (int i = threadIdx.x; i < nv * m; i += PEXP_THREADS) Hp[i] = 0.0;
@@ -64,7 +71,7 @@ __device__ inline void cta_vtw(int ld, int rows, const double* V, int nv, const 
     __syncthreads();
     for (int i = threadIdx.x; i < m * RC; i += PEXP_THREADS) {
       int bb = i / RC, r = i % RC;
-      Cb[bb * ldc + r] = r < cnt ? W[size_t(bb) * ld + r0 + r] : 0.0;
+      Cb[bb * ldc + r] = r < cnt ? W[size_t(bb) * ldw + r0 + r] : 0.0;
     }
     __syncthreads();
     for (int a = CPW * warp; a < nv; a += CPW * nw) {
@@ -109,7 +116,8 @@ __device__ inline void cta_vtw(int ld, int rows, const double* V, int nv, const 
 
 // W[b][r] -= sum_a V[a][r] Hs[a + b*nv] on this CTA's rows
 template <int MB>
-__device__ inline void cta_update(int ld, int rows, const double* V, int nv, double* W, int m, const double* Hs) {
+__device__ inline void cta_update(int ld, int ldw, int rows, const double* V, int nv, double* W, int m,
+                                  const double* Hs) {
   constexpr int RR = 2, UA = 8;  // rows per thread x columns in flight
   for (int r0 = threadIdx.x; r0 < rows; r0 += PEXP_THREADS * RR) {
     double acc[RR][MB];
@@ -149,8 +157,8 @@ __device__ inline void cta_update(int ld, int rows, const double* V, int nv, dou
 #pragma unroll
     for (int bb = 0; bb < MB; ++bb)
       if (bb < m) {
-        W[size_t(bb) * ld + r0] -= acc[0][bb];
-        if (ok1) W[size_t(bb) * ld + r0 + PEXP_THREADS] -= acc[1][bb];
+        W[size_t(bb) * ldw + r0] -= acc[0][bb];
+        if (ok1) W[size_t(bb) * ldw + r0 + PEXP_THREADS] -= acc[1][bb];
       }
   }
   __syncthreads();
@@ -158,18 +166,18 @@ __device__ inline void cta_update(int ld, int rows, const double* V, int nv, dou
 
 // Partial G[a + b*MB] = sum over this CTA's rows of X[a][r] Y[b][r]  (Y may equal X)
 template <int MB>
-__device__ inline void cta_gram(int ld, int rows, const double* X, const double* Y, int m, double* G) {
+__device__ inline void cta_gram(int ldx, int ldy, int rows, const double* X, const double* Y, int m, double* G) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = PEXP_THREADS / 32;
   for (int a = warp; a < m; a += nw) {
-    const double* xa = X + size_t(a) * ld;
+    const double* xa = X + size_t(a) * ldx;
     double acc[MB];
 #pragma unroll
     for (int bb = 0; bb < MB; ++bb) acc[bb] = 0.0;
     for (int r = lane; r < rows; r += 32) {
-      const double xv = __ldcg(xa + r);
+      const double xv = xa[r];
 #pragma unroll
       for (int bb = 0; bb < MB; ++bb)
-        if (bb < m) acc[bb] = fma(xv, __ldcg(Y + size_t(bb) * ld + r), acc[bb]);
+        if (bb < m) acc[bb] = fma(xv, Y[size_t(bb) * ldy + r], acc[bb]);
     }
 #pragma unroll
     for (int bb = 0; bb < MB; ++bb)
@@ -183,12 +191,14 @@ __device__ inline void cta_gram(int ld, int rows, const double* X, const double*
 
 // Cluster-wide Gram: partial into s.Gp, summed into s.G
 template <int MB>
-__device__ inline void cl_gram(cg::cluster_group& cl, int cs, int ld, int rows, const double* X, const double* Y,
-                               int m, SmemT& s) {
-  for (int i = threadIdx.x; i < MB * MB; i += PEXP_THREADS) s.Gp[i] = 0.0;
+__device__ inline void cl_gram(cg::cluster_group& cl, int cs, int ldx, int ldy, int rows, const double* X,
+                               const double* Y, int m, SmemT& s) {
+  double* gp = s.Gp + s.gpar * MB * MB;
+  s.gpar ^= 1;
+  for (int i = threadIdx.x; i < MB * MB; i += PEXP_THREADS) gp[i] = 0.0;
   __syncthreads();
-  cta_gram<MB>(ld, rows, X, Y, m, s.Gp);
-  cl_allreduce(cl, cs, s.Gp, s.G, MB * MB);
+  cta_gram<MB>(ldx, ldy, rows, X, Y, m, gp);
+  cl_allreduce(cl, cs, gp, s.G, MB * MB);
 }
 
 // W <- beta*W + W*M  (M: m x m, ld MB) row by row
@@ -430,8 +440,8 @@ __device__ inline double seg_bwd(int g0, int cnt, const double* di, const double
 template <int MB>
 __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int ld, int g0, int cnt, int periodic,
                                     const double* l, const double* di, const double* sup, const double* fz,
-                                    const double* fw, const double* Vb, int m, double* W, double* W0, SmemT& s,
-                                    Aff* wsm, double* red) {
+                                    const double* fw, const double* Vb, int m, double* W, int ldw, double* W0,
+                                    SmemT& s, Aff* wsm, double* red) {
   double* xf = s.xch;
   double* xd = s.xch + 2 * MB;
   double* xb = s.xch + 3 * MB;
@@ -459,10 +469,10 @@ __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int l
     f_s[c] = f;
   }
   __syncthreads();
-  for (int c = 0; c < m; ++c) seg_fwd(g0, cnt, l, Vb + size_t(c) * ld, W + size_t(c) * ld, carry_s[c], s.Cx, s.Cy, wsm);
+  for (int c = 0; c < m; ++c) seg_fwd(g0, cnt, l, Vb + size_t(c) * ld, W + size_t(c) * ldw, carry_s[c], s.Cx, s.Cy, wsm);
   // ---- backward segment maps
   for (int c = 0; c < m; ++c) {
-    Aff Bm = (cs > 1 && cr > 0) ? seg_map_bwd(g0, cnt, di, sup, W + size_t(c) * ld, wsm) : Aff{1.0, 0.0};
+    Aff Bm = (cs > 1 && cr > 0) ? seg_map_bwd(g0, cnt, di, sup, W + size_t(c) * ldw, wsm) : Aff{1.0, 0.0};
     if (threadIdx.x == 0) { xb[2 * c] = Bm.A; xb[2 * c + 1] = Bm.B; }
   }
   cl_sync(cl, cs);
@@ -476,7 +486,7 @@ __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int l
   }
   __syncthreads();
   for (int c = 0; c < m; ++c) {
-    double nr = seg_bwd(g0, cnt, di, sup, periodic ? fz : nullptr, f_s[c], W + size_t(c) * ld, W0 + size_t(c) * ld,
+    double nr = seg_bwd(g0, cnt, di, sup, periodic ? fz : nullptr, f_s[c], W + size_t(c) * ldw, W0 + size_t(c) * ld,
                         carry_s[c], s.Cx, s.Cy, wsm, red);
     if (threadIdx.x == 0) xn[c] = nr;
   }
@@ -495,10 +505,11 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
   if (A.active && !A.active[e]) return;  // uniform over the cluster
   const int n = A.n, m = A.m, b = A.b, kcap = A.kcap, nv = (b + 1) * m;
   // this CTA's rows [g0, g0 + cnt) of every column (multiples of 32)
-  const int per = ((n + cs - 1) / cs + 31) / 32 * 32;
+  const int per = step_rows(n, cs);
   const int g0 = min(n, cr * per), cnt = min(n, g0 + per) - g0;
   SmemT s;
   s.ldc = RC + 1;
+  s.gpar = 0;
   const int cbuf = max(s.ldc * MB, PEXP_THREADS * SPAD);
   double* p = sm;
   s.Hs = p; p += size_t(nv) * MB;
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
   s.Cx = p; p += cbuf;
   s.Cy = p; p += cbuf;
   s.G = p; p += MB * MB;
-  s.Gp = p; p += MB * MB;
+  s.Gp = p; p += 2 * MB * MB;
   s.Rinv = p; p += MB * MB;
   s.Mc = p; p += MB * MB;
   s.S = p; p += MB * (MB + 1);
@@ -516,54 +527,62 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
   s.n0 = p; p += MB;
   s.n0p = p; p += MB;
   s.xch = p; p += 6 * MB;
+  s.Ws = A.ws_smem ? p : nullptr;
   double* V = A.V + e * A.vs_e + g0;
   double* H = A.H + e * A.hs_e;
   int* live = A.live + size_t(e) * kcap;
   double* W0 = A.W0 + e * A.w0s_e + g0;
-  double* W = V + size_t(nv) * n;
+  double* Wg = V + size_t(nv) * n;              // the new block in the basis (global)
+  double* W = A.ws_smem ? s.Ws : Wg;            // working copy of the CTA's rows
+  const int ldw = A.ws_smem ? per : n;
   const size_t fo = size_t(A.fidx ? A.fidx[e] : e) * n;
-  // ---- W0 = (I - gamma A)^{-1} V_b   (kept in W0; working copy in the new block)
+  // ---- W0 = (I - gamma A)^{-1} V_b   (kept in W0; working copy in W)
   cl_sai_solve<MB>(cl, cs, cr, n, g0, cnt, A.periodic, A.fl + fo, A.fdinv + fo, A.fsup + fo,
                    A.periodic ? A.fz + fo : nullptr, A.periodic ? A.fw + fo : nullptr, V + size_t(b * m) * n, m, W,
-                   W0, s, wsm, red);
+                   ldw, W0, s, wsm, red);
   // ---- BCGS pass 1
-  cta_vtw<MB>(n, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
+  cta_vtw<MB>(n, ldw, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
   cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
   if (cr == 0)
     for (int i = threadIdx.x; i < nv * m; i += PEXP_THREADS) {
       int a = i % nv, c = i / nv;
       H[a + size_t(b * m + c) * kcap] = s.Hs[i];
     }
-  cta_update<MB>(n, cnt, V, nv, W, m, s.Hs);
+  cta_update<MB>(n, ldw, cnt, V, nv, W, m, s.Hs);
   // ---- in-block QR, stage A (accept kappa <= 1e4, defer the rest, drop below defl*|W0|)
-  cl_gram<MB>(cl, cs, n, cnt, W, W, m, s);
+  cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
   cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 1e-8, A.piv_tol, s, cls, perm, used, dead);
-  cta_apply<MB>(n, cnt, W, m, s.Rinv, 0.0);
+  cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
   // ---- stage B: explicit CGS2 of deferred columns against accepted ones
   for (int rep = 0; rep < 2; ++rep) {
-    cl_gram<MB>(cl, cs, n, cnt, W, W, m, s);
+    cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
     for (int idx = threadIdx.x; idx < MB * MB; idx += PEXP_THREADS) {
       int a = idx % MB, k = idx / MB;
       s.Mc[idx] = (a < m && k < m && cls[a] == 1 && cls[k] == 2) ? -s.G[a + k * MB] : 0.0;
     }
     __syncthreads();
-    cta_apply<MB>(n, cnt, W, m, s.Mc, 1.0);
+    cta_apply<MB>(ldw, cnt, W, m, s.Mc, 1.0);
   }
   // ---- stage C: final pivoted CholQR with deflation relative to |W0|
-  cl_gram<MB>(cl, cs, n, cnt, W, W, m, s);
+  cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
   for (int k = threadIdx.x; k < m; k += PEXP_THREADS) s.n0[k] = s.n0p[k];
   __syncthreads();
   cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 0.0, A.piv_tol, s, cls, perm, used, dead);
-  cta_apply<MB>(n, cnt, W, m, s.Rinv, 0.0);
+  cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
   // ---- BCGS pass 2 + CholQR
-  cta_vtw<MB>(n, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
+  cta_vtw<MB>(n, ldw, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
   cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
-  cta_update<MB>(n, cnt, V, nv, W, m, s.Hs);
-  cl_gram<MB>(cl, cs, n, cnt, W, W, m, s);
+  cta_update<MB>(n, ldw, cnt, V, nv, W, m, s.Hs);
+  cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
   cta_chol_piv<MB>(m, s.G, nullptr, A.defl, 0.0, A.piv_tol, s, cls, perm, used, dead);
-  cta_apply<MB>(n, cnt, W, m, s.Rinv, 0.0);
-  // ---- subdiagonal block H[nv + a, b*m + c] = Q_a^T W0_c ; live flags
-  cl_gram<MB>(cl, cs, n, cnt, W, W0, m, s);
+  cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
+  // ---- the new basis block to global memory; subdiagonal block H[nv + a, b*m + c] = Q_a^T W0_c
+  if (A.ws_smem)
+    for (int idx = threadIdx.x; idx < m * cnt; idx += PEXP_THREADS) {
+      const int c = idx / cnt, r = idx % cnt;
+      Wg[size_t(c) * n + r] = W[size_t(c) * ldw + r];
+    }
+  cl_gram<MB>(cl, cs, ldw, n, cnt, W, W0, m, s);
   if (cr == 0) {
     for (int i = threadIdx.x; i < m * m; i += PEXP_THREADS) {
       int a = i % m, c = i / m;
@@ -571,19 +590,21 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
     }
     for (int k = threadIdx.x; k < m; k += PEXP_THREADS) live[nv + k] = cls[k] ? 1 : 0;
   }
+  cl_sync(cl, cs);  // no CTA leaves while its shared memory may still be read remotely
 }
 
-static size_t step_smem(int MB, int nv) {
+static size_t step_smem(int MB, int nv, int wrows) {
   const int ldc = RC + 1;
   size_t cbuf = std::max(size_t(ldc) * MB, size_t(PEXP_THREADS) * SPAD);
-  return sizeof(double) * (2 * size_t(nv) * MB + 2 * cbuf + 4 * MB * MB + 3 * MB * (MB + 1) + 3 * MB + 6 * MB);
+  return sizeof(double) * (2 * size_t(nv) * MB + 2 * cbuf + 5 * MB * MB + 3 * MB * (MB + 1) + 3 * MB + 6 * MB +
+                           size_t(wrows) * MB);
 }
 
 static int mb_for(int m) { return m <= 8 ? 8 : (m <= 16 ? 16 : 32); }
 
 bool arnoldi_fused_ok(int m, int nv) {
   if (m > 32) return false;
-  return step_smem(mb_for(m), nv) <= 200 * 1024;
+  return step_smem(mb_for(m), nv, 0) <= 200 * 1024;
 }
 
 // cluster size: enough CTAs for ~2 waves over the 148 SMs, >= 512 rows per CTA, portable max 8
@@ -622,7 +643,10 @@ void launch_arnoldi_step(cudaStream_t st, StepArgs a) {
   a.piv_tol = g_piv_tol;
   a.cs = step_cluster(a.E, a.n);
   const int nv = (a.b + 1) * a.m;
-  size_t smem = step_smem(MB, nv);
+  const int per = step_rows(a.n, a.cs);
+  size_t smem = step_smem(MB, nv, per);
+  a.ws_smem = smem <= 200 * 1024 ? 1 : 0;  // the CTA's rows of the new block stay on chip
+  if (!a.ws_smem) smem = step_smem(MB, nv, 0);
   ProfScope ps(PC_ARNOLDI, st, double(a.E) * a.n * 8.0 * (4.0 * nv + 12.0 * a.m),
                double(a.E) * a.n * (8.0 * nv * a.m + 10.0 * a.m * a.m));
   if (MB == 8)

@@ -161,82 +161,138 @@ __device__ inline double cta_norm1(int N, const double* A, int lda, double* red)
   return block_max(mx, red);
 }
 
+// Triangular solve with a kb x kb (kb <= 32) diagonal block T (ld ldt) staged in shared memory:
+// X (kb x ncols, ld ldx) <- T^{-1} X, unit lower (LOWER) or non-unit upper (!LOWER).  One thread
+// per column keeps its kb values in registers.  Columns [c0, c1) of X; all CTA threads call it.
+template <bool LOWER>
+__device__ inline void cta_trsm_small(int kb, const double* T, int ldt, double* X, int ldx, int c0, int c1) {
+  double (*Ts)[33] = reinterpret_cast<double (*)[33]>(gemm_smem());
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+    const int i = idx % kb, j = idx / kb;
+    Ts[i][j] = T[i + size_t(j) * ldt];
+  }
+  __syncthreads();
+  for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
+    double x[32];
+    double* col = X + size_t(j) * ldx;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = i < kb ? col[i] : 0.0;
+    if (LOWER) {
+#pragma unroll
+      for (int i = 1; i < 32; ++i) {
+        double v = x[i];
+#pragma unroll
+        for (int p = 0; p < i; ++p) v = fma(-Ts[i][p], x[p], v);
+        x[i] = v;
+      }
+    } else {
+#pragma unroll
+      for (int i = 31; i >= 0; --i) {
+        if (i < kb) {
+          double v = x[i];
+#pragma unroll
+          for (int p = i + 1; p < 32; ++p)
+            if (p < kb) v = fma(-Ts[i][p], x[p], v);
+          x[i] = v / Ts[i][i];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < kb) col[i] = x[i];
+  }
+  __syncthreads();
+}
+
 // Blocked right-looking LU with partial pivoting, in place.  piv[k] = row swapped with k.
-// Returns false if a zero pivot was met.
-__device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red, Grp g = kSolo) {
+// Returns false if a zero pivot was met.  The N x NBL panel is factored in shared memory (psm,
+// psm_cap doubles; NBL = 32, halved until the panel fits) by rank 0 of the group; its row
+// interchanges are then applied to the other columns by the whole group; U12 = L11^{-1} A12 by
+// register triangular solves, A22 -= L21 U12 by the CTA-level GEMM.
+__device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red, Grp g, double* psm, int psm_cap) {
   __shared__ int s_ip;
-  __shared__ double s_pv;
   __shared__ int s_bad;
   __shared__ int s_idx[32];
   if (threadIdx.x == 0) s_bad = 0;
-  constexpr int NBL = 32;
+  int NBL = 32;
+  while (NBL > 1 && size_t(N) * NBL > size_t(psm_cap)) NBL /= 2;
   for (int k0 = 0; k0 < N; k0 += NBL) {
-    const int kb = min(NBL, N - k0);
-    // --- unblocked panel factorisation of columns k0..k0+kb-1 (rows k0..N-1), rank 0 only
-    if (g.rank == 0)
-    for (int k = k0; k < k0 + kb; ++k) {
-      // pivot search
-      double best = -1.0;
-      int bi = k;
-      for (int i = k + threadIdx.x; i < N; i += blockDim.x) {
-        double v = fabs(A[i + size_t(k) * lda]);
-        if (v > best) { best = v; bi = i; }
-      }
-      // reduce (value, index) over block via warps
-      for (int o = 16; o > 0; o >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    const int kb = min(NBL, N - k0), h = N - k0;
+    if (g.rank == 0) {
+      double* P = psm;  // panel rows k0..N-1, columns k0..k0+kb-1, column-major ld h
+      for (int idx = threadIdx.x; idx < h * kb; idx += blockDim.x) {
+        const int i = idx % h, c = idx / h;
+        P[idx] = A[k0 + i + size_t(k0 + c) * lda];
       }
       __syncthreads();
-      if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = best; s_idx[threadIdx.x >> 5] = bi; }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int nw = (blockDim.x + 31) >> 5;
-        double b = red[0];
-        int ii = s_idx[0];
-        for (int w = 1; w < nw; ++w) {
-          double ob = red[w];
-          int oi = s_idx[w];
-          if (ob > b || (ob == b && oi < ii)) { b = ob; ii = oi; }
+      for (int k = 0; k < kb; ++k) {
+        double best = -1.0;
+        int bi = k;
+        for (int i = k + threadIdx.x; i < h; i += blockDim.x) {
+          const double v = fabs(P[i + size_t(k) * h]);
+          if (v > best) { best = v; bi = i; }
         }
-        s_ip = ii;
-        piv[k] = ii;
-        if (!(b > 0.0)) s_bad = 1;
-      }
-      __syncthreads();
-      const int ip = s_ip;
-      if (ip != k)
-        for (int j = threadIdx.x; j < N; j += blockDim.x) {
-          double tmp = A[k + size_t(j) * lda];
-          A[k + size_t(j) * lda] = A[ip + size_t(j) * lda];
-          A[ip + size_t(j) * lda] = tmp;
+        for (int o = 16; o > 0; o >>= 1) {
+          double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
         }
-      __syncthreads();
-      if (threadIdx.x == 0) s_pv = A[k + size_t(k) * lda];
-      __syncthreads();
-      const double pv = s_pv;
-      const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
-      for (int i = k + 1 + threadIdx.x; i < N; i += blockDim.x) A[i + size_t(k) * lda] *= inv;
-      __syncthreads();
-      // update the rest of the panel
-      const int w = k0 + kb - (k + 1), h = N - (k + 1);
-      for (int idx = threadIdx.x; idx < w * h; idx += blockDim.x) {
-        int i = k + 1 + idx % h, j = k + 1 + idx / h;
-        A[i + size_t(j) * lda] = fma(-A[i + size_t(k) * lda], A[k + size_t(j) * lda], A[i + size_t(j) * lda]);
+        if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = best; s_idx[threadIdx.x >> 5] = bi; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const int nw = (blockDim.x + 31) >> 5;
+          double b = red[0];
+          int ii = s_idx[0];
+          for (int w = 1; w < nw; ++w) {
+            if (red[w] > b || (red[w] == b && s_idx[w] < ii)) { b = red[w]; ii = s_idx[w]; }
+          }
+          s_ip = ii;
+          piv[k0 + k] = k0 + ii;
+          if (!(b > 0.0)) s_bad = 1;
+        }
+        __syncthreads();
+        const int ip = s_ip;
+        if (ip != k)
+          for (int c = threadIdx.x; c < kb; c += blockDim.x) {
+            const double t = P[k + size_t(c) * h];
+            P[k + size_t(c) * h] = P[ip + size_t(c) * h];
+            P[ip + size_t(c) * h] = t;
+          }
+        __syncthreads();
+        const double pv = P[k + size_t(k) * h];
+        const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
+        for (int i = k + 1 + threadIdx.x; i < h; i += blockDim.x) P[i + size_t(k) * h] *= inv;
+        __syncthreads();
+        const int w = kb - (k + 1), hh = h - (k + 1);
+        for (int idx = threadIdx.x; idx < w * hh; idx += blockDim.x) {
+          const int i = k + 1 + idx % hh, c = k + 1 + idx / hh;
+          P[i + size_t(c) * h] = fma(-P[i + size_t(k) * h], P[k + size_t(c) * h], P[i + size_t(c) * h]);
+        }
+        __syncthreads();
       }
-      __syncthreads();
+      for (int idx = threadIdx.x; idx < h * kb; idx += blockDim.x) {
+        const int i = idx % h, c = idx / h;
+        A[k0 + i + size_t(k0 + c) * lda] = P[idx];
+      }
+    }
+    grp_sync(g);
+    // the panel's interchanges on all other columns (one thread per column, group-split)
+    for (int j = threadIdx.x + g.rank * blockDim.x; j < N; j += blockDim.x * g.size) {
+      if (j >= k0 && j < k0 + kb) continue;
+      double* col = A + size_t(j) * lda;
+      for (int k = k0; k < k0 + kb; ++k) {
+        const int ip = piv[k];
+        if (ip != k) { const double t = col[k]; col[k] = col[ip]; col[ip] = t; }
+      }
     }
     grp_sync(g);
     const int rest = N - (k0 + kb);
     if (rest > 0) {
-      // U12 = L11^{-1} A12 (unit lower), one thread per column (columns split over the group)
-      for (int j = k0 + kb + threadIdx.x + g.rank * blockDim.x; j < N; j += blockDim.x * g.size)
-        for (int i = k0; i < k0 + kb; ++i) {
-          double s = A[i + size_t(j) * lda];
-          for (int p = k0; p < i; ++p) s = fma(-A[i + size_t(p) * lda], A[p + size_t(j) * lda], s);
-          A[i + size_t(j) * lda] = s;
-        }
+      // U12 = L11^{-1} A12 (unit lower), columns split over the group
+      const int per = (rest + g.size - 1) / g.size;
+      const int c0 = k0 + kb + g.rank * per, c1 = min(N, c0 + per);
+      cta_trsm_small<true>(kb, A + k0 + size_t(k0) * lda, lda, A + k0, lda, c0, c1);
       grp_sync(g);
       // A22 -= L21 U12
       cta_gemm(rest, rest, kb, -1.0, A + (k0 + kb) + size_t(k0) * lda, lda,
@@ -249,57 +305,75 @@ __device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red, 
 
 // Solve (LU) X = P B in place on B (N x nrhs), blocked; uses cta_gemm for off-diagonal blocks.
 __device__ inline void cta_lu_solve_local(int N, const double* LU, int lda, const int* piv, double* B,
-                                          int ldb, int nrhs);
+                                          int ldb, int nrhs, double* psm, int psm_cap, bool identity_rhs,
+                                          int cbase);
 
-// RHS columns are split into contiguous ranges, one per CTA of the group
+// RHS columns are split into contiguous ranges, one per CTA of the group.  identity_rhs: B is
+// the identity on entry (H^{-1}): P B is then written directly instead of permuted.
 __device__ inline void cta_lu_solve(int N, const double* LU, int lda, const int* piv, double* B, int ldb, int nrhs,
-                                    Grp g = kSolo) {
+                                    Grp g, double* psm, int psm_cap, bool identity_rhs = false) {
   const int per = (nrhs + g.size - 1) / g.size;
   const int c0 = g.rank * per, c1 = min(nrhs, c0 + per);
-  if (c1 > c0) cta_lu_solve_local(N, LU, lda, piv, B + size_t(c0) * ldb, ldb, c1 - c0);
+  cta_lu_solve_local(N, LU, lda, piv, B + size_t(c0) * ldb, ldb, max(0, c1 - c0), psm, psm_cap, identity_rhs, c0);
   grp_sync(g);
 }
 
 __device__ inline void cta_lu_solve_local(int N, const double* LU, int lda, const int* piv, double* B,
-                                          int ldb, int nrhs) {
-  // row interchanges
-  for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
+                                          int ldb, int nrhs, double* psm, int psm_cap, bool identity_rhs,
+                                          int cbase) {
+  // row order of P B: perm = the interchanges applied to 0..N-1 (thread 0, shared memory)
+  int* perm = reinterpret_cast<int*>(psm);
+  const int pint = (N + 1) / 2 + 1;  // doubles occupied by perm
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < N; ++i) perm[i] = i;
     for (int k = 0; k < N; ++k) {
-      int ip = piv[k];
-      if (ip != k) {
-        double tmp = B[k + size_t(j) * ldb];
-        B[k + size_t(j) * ldb] = B[ip + size_t(j) * ldb];
-        B[ip + size_t(j) * ldb] = tmp;
+      const int ip = piv[k];
+      if (ip != k) { const int t = perm[k]; perm[k] = perm[ip]; perm[ip] = t; }
+    }
+  }
+  __syncthreads();
+  if (nrhs > 0) {
+    if (identity_rhs) {
+      // B holds columns cbase.. of I: (P I)[i][j] = (perm[i] == cbase + j)
+      const int c0 = cbase;
+      for (int idx = threadIdx.x; idx < N * nrhs; idx += blockDim.x) {
+        const int i = idx % N, j = idx / N;
+        B[i + size_t(j) * ldb] = perm[i] == c0 + j ? 1.0 : 0.0;
+      }
+    } else {
+      double* buf = psm + pint;
+      const int cb = max(1, (psm_cap - pint) / max(N, 1));
+      for (int j0 = 0; j0 < nrhs; j0 += cb) {
+        const int nc = min(cb, nrhs - j0);
+        for (int idx = threadIdx.x; idx < N * nc; idx += blockDim.x) {
+          const int i = idx % N, j = idx / N;
+          buf[idx] = B[perm[i] + size_t(j0 + j) * ldb];
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < N * nc; idx += blockDim.x) {
+          const int i = idx % N, j = idx / N;
+          B[i + size_t(j0 + j) * ldb] = buf[idx];
+        }
+        __syncthreads();
       }
     }
+  }
   __syncthreads();
   constexpr int NBL = 32;
   // forward: unit lower
   for (int k0 = 0; k0 < N; k0 += NBL) {
     const int kb = min(NBL, N - k0);
-    for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
-      for (int i = k0; i < k0 + kb; ++i) {
-        double s = B[i + size_t(j) * ldb];
-        for (int p = k0; p < i; ++p) s = fma(-LU[i + size_t(p) * lda], B[p + size_t(j) * ldb], s);
-        B[i + size_t(j) * ldb] = s;
-      }
-    __syncthreads();
+    cta_trsm_small<true>(kb, LU + k0 + size_t(k0) * lda, lda, B + k0, ldb, 0, nrhs);
     const int rest = N - (k0 + kb);
-    if (rest > 0)
+    if (rest > 0 && nrhs > 0)
       cta_gemm(rest, nrhs, kb, -1.0, LU + (k0 + kb) + size_t(k0) * lda, lda, B + k0, ldb, 1.0,
                B + k0 + kb, ldb);
   }
   // backward: upper
   for (int k1 = N; k1 > 0; k1 -= NBL) {
     const int k0 = max(0, k1 - NBL), kb = k1 - k0;
-    for (int j = threadIdx.x; j < nrhs; j += blockDim.x)
-      for (int i = k1 - 1; i >= k0; --i) {
-        double s = B[i + size_t(j) * ldb];
-        for (int p = i + 1; p < k1; ++p) s = fma(-LU[i + size_t(p) * lda], B[p + size_t(j) * ldb], s);
-        B[i + size_t(j) * ldb] = s / LU[i + size_t(i) * lda];
-      }
-    __syncthreads();
-    if (k0 > 0)
+    cta_trsm_small<false>(kb, LU + k0 + size_t(k0) * lda, lda, B + k0, ldb, 0, nrhs);
+    if (k0 > 0 && nrhs > 0)
       cta_gemm(k0, nrhs, kb, -1.0, LU + size_t(k0) * lda, lda, B + k0, ldb, 1.0, B, ldb);
   }
 }
@@ -307,7 +381,7 @@ __device__ inline void cta_lu_solve_local(int N, const double* LU, int lda, cons
 // Pade-13 scaling-and-squaring exponential (Higham 2005), in place on X (N x N, ld = ldx).
 // work: 7 matrices of ld x N.  Returns the number of squarings.
 __device__ inline int cta_expm_pade13(int N, double* X, int ldx, double* work, int ldw, int* piv,
-                                      double* red, Grp g = kSolo) {
+                                      double* red, Grp g, double* psm, int psm_cap) {
   const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                         1187353796428800.0,  129060195264000.0,   10559470521600.0,
                         670442572800.0,      33522128640.0,       1323241920.0,
@@ -352,8 +426,8 @@ __device__ inline int cta_expm_pade13(int N, double* X, int ldx, double* work, i
     T2[o] = V[o] + U[o];
   }
   grp_sync(g);
-  cta_lu(N, T1, ldw, piv, red, g);
-  cta_lu_solve(N, T1, ldw, piv, T2, ldw, N, g);
+  cta_lu(N, T1, ldw, piv, red, g, psm, psm_cap);
+  cta_lu_solve(N, T1, ldw, piv, T2, ldw, N, g, psm, psm_cap);
   // squarings, ping-pong T2 <-> T1
   double *cur = T2, *nxt = T1;
   for (int q = 0; q < s; ++q) {

@@ -31,6 +31,7 @@ namespace {
 
 constexpr int RPT_MAX = 4;   // rows per thread
 constexpr int NT = PEXP_THREADS;
+constexpr int HS_PSM = 12288;  // checker's shared scratch (doubles) for the LU panel / permutation
 
 enum { F_STEPS = 0, F_RESULT = 1, F_DECISION = 2, F_KMAX = 3, F_ERR = 4, F_BREAK = 5, F_NFLAGS = 8 };
 enum { B_WCNT = 0, B_WGEN = 1, B_ACNT = 2, B_AGEN = 3 };
@@ -118,7 +119,7 @@ struct ScanArgs {
 
 // Projected check on the checker CTA: returns max_r residual; writes Zc[r][0..K).
 __device__ static double hom_check(const ScanArgs& a, int K, double gam, double beta, double* z, double* zn,
-                                   double* red) {
+                                   double* red, double* psm) {
   const int ld = a.kcap, ldh = a.kcap + 1;
   const size_t MM = size_t(ld) * ld;
   double* S0 = a.work;
@@ -131,14 +132,14 @@ __device__ static double hom_check(const ScanArgs& a, int K, double gam, double 
   }
   __syncthreads();
   cta_identity(K, S1, ld, 1.0);
-  cta_lu(K, S0, ld, a.iwork, red);
-  cta_lu_solve(K, S0, ld, a.iwork, S1, ld, K);
+  cta_lu(K, S0, ld, a.iwork, red, kSolo, psm, HS_PSM);
+  cta_lu_solve(K, S0, ld, a.iwork, S1, ld, K, kSolo, psm, HS_PSM, true);
   for (int t = threadIdx.x; t < K * K; t += NT) {
     const int i = t % K, j = t / K;
     S2[i + size_t(j) * ld] = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
   }
   __syncthreads();
-  cta_expm_pade13(K, S2, ld, WK, ld, a.iwork, red);
+  cta_expm_pade13(K, S2, ld, WK, ld, a.iwork, red, kSolo, psm, HS_PSM);
   const double htail = __ldcg(a.H + K + size_t(K - 1) * ldh);
   for (int r = threadIdx.x; r < K; r += NT) z[r] = r == 0 ? beta : 0.0;
   __syncthreads();
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   __shared__ double red[32];
   __shared__ Aff wsm[NT / 32 + 1];
   __shared__ int s_dec;
-  extern __shared__ double dyn[];  // hv, hv2: KSMALL_MAX + 8 each; xs: NT * RPT_MAX
+  extern __shared__ double dyn[];  // hv, hv2: KSMALL_MAX + 8 each; xs: NT * RPT_MAX; LU scratch HS_PSM
   double* hv = dyn;
   double* hv2 = dyn + KSMALL_MAX + 8;
   double* xs = hv2 + KSMALL_MAX + 8;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           __syncthreads();
           const int K = s_dec;
           const bool brk = vload(fl + F_BREAK) == K;
-          const double res = hom_check(a, K, gam, beta, z, zn, red);
+          const double res = hom_check(a, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
           if (threadIdx.x == 0) {
             int result = 0;
             if (brk || res <= crit) result = K;
@@ -496,7 +497,7 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
     // algorithmic bytes: the waveform pass (Y, Uold read; Unew write) per subinterval
     ProfScope ps(PC_SCAN, st, double(P) * s * n * 24.0, 0.0);
     void* args[] = {&a};
-    const size_t smem = sizeof(double) * (2 * (KSMALL_MAX + 8) + NT * RPT_MAX);
+    const size_t smem = sizeof(double) * (2 * (KSMALL_MAX + 8) + NT * RPT_MAX + HS_PSM);
     static bool attr = false;
     if (!attr) {
       PEXP_CUDA_TRY(cudaFuncSetAttribute(k_hom_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -86,6 +86,7 @@ struct StepArgs {
   double defl, piv_tol;
   int rc;
   int cs;                         // CTAs per evaluation (thread-block cluster)
+  int ws_smem;                    // 1: the CTA's rows of the new block live in shared memory
 };
 
 // arnoldi.cu

@@ -633,6 +633,36 @@ struct pexp_ctx {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   std::string err;
+  // side stream + events: the shift-and-invert factorisation runs concurrently with the source
+  // SVD stage (they are independent until the block Arnoldi starts)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~pexp_ctx() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
+};
+
+// Launch the factorisation on the context's side stream after everything queued on st so far;
+// join() makes st wait for it.
+struct SideFactor {
+  pexp_ctx* c;
+  cudaStream_t st;
+  SideFactor(pexp_ctx* c_, cudaStream_t st_) : c(c_), st(st_) {
+    if (!c->side) {
+      PEXP_CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      PEXP_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      PEXP_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    PEXP_CUDA_TRY(cudaEventRecord(c->ev_fork, st));
+    PEXP_CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  }
+  cudaStream_t stream() const { return c->side; }
+  void join() {
+    PEXP_CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
+    PEXP_CUDA_TRY(cudaStreamWaitEvent(st, c->ev_join, 0));
+  }
 };
 
 static pexp_status set_err(pexp_ctx* c, int code, const std::string& m) {
@@ -651,6 +681,13 @@ static pexp_status guarded(pexp_ctx* c, F&& f) {
   } catch (const std::exception& e) {
     return set_err(c, PEXP_EINVAL, e.what());
   }
+}
+
+// Homogeneous legs per group (one shared block Krylov space per group; <= 16, KSMALL limits)
+static int hom_group_width(int P) {
+  static const int force = getenv("PEXP_MH") ? atoi(getenv("PEXP_MH")) : 0;  // developer override
+  const int w = force > 0 ? std::min(force, 16) : 16;
+  return std::max(1, std::min(w, P - 1));
 }
 
 // ---------------------------------------------------------------- workspace plans
@@ -689,7 +726,7 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
   alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable);
   if (P > 1) {
-    const int mh = std::min(16, P - 1), G = cdiv(P - 1, mh), Eg = Bt * G;
+    const int mh = hom_group_width(P), G = cdiv(P - 1, mh), Eg = Bt * G;
     // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
     // 16 legs -> 288 columns); give it at least 24 block steps
     const int kcap_h = std::min(KSMALL_MAX - 64, std::max(o.kcap, 24 * mh));
@@ -896,7 +933,8 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     h2d(st, L.opidx_f, of);
     h2d(st, L.iota, iota);
     PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
-    launch_factor(st, L.F, 2 * Bt, L.opidx_f, L.gam_f, L.O, L.err);
+    SideFactor sf(ctx, st);
+    launch_factor(sf.stream(), L.F, 2 * Bt, L.opidx_f, L.gam_f, L.O, L.err);
     // shifted source G = A u0 + g at the nodes
     launch_apply_A(st, L.O, L.iota, Bt, 1, u0, n, 0, L.Au0, n, 0, periodic);
     launch_lin_source(st, Bt, P, s, n, L.Au0, src, L.G);
@@ -908,6 +946,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     h2d(st, L.B.opidx, fe);
     h2d(st, L.B.gam, ge);
     int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, nullptr);
+    sf.join();
     int herr = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
     PEXP_CUDA_TRY(cudaStreamSynchronize(st));
@@ -924,7 +963,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
       // homogeneous legs, grouped: up to 16 consecutive legs share one block Krylov space
       // (EBK for the homogeneous part too); group eh = b*G + g holds legs
       // j = g*mh .. g*mh+mh-1 of problem b
-      const int mh = std::min(16, P - 1);
+      const int mh = hom_group_width(P);
       G = cdiv(P - 1, mh);
       const int Eg = Bt * G;
       EbkBufs& Bh = L.Bh;
@@ -1019,9 +1058,11 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       launch_ubar_gamma(st, P, s, n, L.Uk, dT, L.ubar, L.B.gam);
       launch_burgers_rows(st, P, n, nu, L.ubar, L.O.sub, L.O.diag, L.O.sup);
       PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
-      launch_factor(st, L.F, P, L.iota, L.B.gam, L.O, L.err);
+      SideFactor sf(ctx, st);
+      launch_factor(sf.stream(), L.F, P, L.iota, L.B.gam, L.O, L.err);
       launch_burgers_source(st, P, s, n, nu, u0, L.Uk, L.ubar, L.G);
       int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, nullptr);
+      sf.join();
       int herr = 0;
       PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
       PEXP_CUDA_TRY(cudaStreamSynchronize(st));

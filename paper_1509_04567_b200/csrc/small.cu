@@ -601,8 +601,8 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     }
     grp_sync(g);
     cta_identity(Kp, S1, ld, 1.0, g);
-    cta_lu(Kp, S0, ld, piv, red, g);
-    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g);
+    cta_lu(Kp, S0, ld, piv, red, g, zsm, int(SP_DYN / 8));
+    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g, zsm, int(SP_DYN / 8), true);
     // augmented matrix (times h) in S2; on a restart check the new cycle is appended to NA
     const bool wr = a.restart_write && NAe;
     for (int t = threadIdx.x + g.rank * blockDim.x; t < Nn * Nn; t += blockDim.x * g.size) {
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
     }
     if (a.kplast && g.rank == 0 && threadIdx.x == 0) a.kplast[e] = Kp;
     grp_sync(g);
-    cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red, g);
+    cta_expm_pade13(Nn, S2, ld, WK, ld, piv, red, g, zsm, int(SP_DYN / 8));
     // ---- exact chaining over the np pieces (rows split over the group, one group barrier per
     // piece): z_{i+1} = F z_i + f_i with F = e^{h N}[0:Dz, 0:Dz] and the piece forcing
     // f_i = sum_q h^q B_q c_{i,q}; the state is replicated in every CTA's shared memory (each CTA
@@ -816,6 +816,7 @@ void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double
 // sum_{j<i} exp((T_{i+1} - T_{j+1}) A) v_j(T_{j+1}) (Eq.(superposition)).
 // Residual per leg and step (SaI form) against crit_c; convergence when every leg passes.
 __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
+  extern __shared__ double hsm[];  // HOM_DYN bytes: LU scratch; later residual ring + F slice
   __shared__ int idx[KSMALL_MAX];
   __shared__ int tidx[MAXS], lpos[MAXS];
   __shared__ int s_K, s_mt, s_ml;
@@ -857,14 +858,14 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
     }
     grp_sync(g);
     cta_identity(Kp, S1, ld, 1.0, g);
-    cta_lu(Kp, S0, ld, piv, red, g);
-    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g);
+    cta_lu(Kp, S0, ld, piv, red, g, hsm, int(HOM_DYN / 8));
+    cta_lu_solve(Kp, S0, ld, piv, S1, ld, Kp, g, hsm, int(HOM_DYN / 8), true);
     for (int t = threadIdx.x + g.rank * blockDim.x; t < Kp * Kp; t += blockDim.x * g.size) {
       int i = t % Kp, j = t / Kp;
       S2[i + size_t(j) * ld] = a.h * ((i == j ? 1.0 : 0.0) - S1[i + size_t(j) * ld]) / gam;
     }
     grp_sync(g);
-    cta_expm_pade13(Kp, S2, ld, WK, ld, piv, red, g);
+    cta_expm_pade13(Kp, S2, ld, WK, ld, piv, red, g, hsm, int(HOM_DYN / 8));
     // ---- propagation Z_q = F Z_{q-1} (Kp x m), rows split over the group, one group barrier
     // per step.  The replicated state lives in the slot's global workspace (L2; read with
     // __ldcg across CTAs), each CTA accumulates its own rows of every leg's outputs and a partial
@@ -876,7 +877,6 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
     double* Zb1 = WK + size_t(Kp) * m;         // [m][Kp]
     double* Rg = Zb1 + size_t(Kp) * m;         // [mt][Kp]
     double* zown = Rg + size_t(mt) * Kp;       // [m][nr] per CTA (disjoint rows)
-    extern __shared__ double hsm[];            // HOM_DYN bytes: residual ring, then the F slice
     double* ring = hsm;                        // [2][16*16]
     double* Fs = hsm + 2 * 256;                // own rows of F, column-major (ld nr), if they fit
     const bool fsm = size_t(nr) * Kp <= HOM_FS_CAP;
@@ -979,6 +979,7 @@ void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
 __global__ void __launch_bounds__(PEXP_THREADS)
 k_expm_batched(int E, int N, const double* A, double* X, double* work, long long work_slot, int* iwork) {
   __shared__ double red[32];
+  extern __shared__ double xsm[];  // HOM_DYN bytes: LU panel / permutation scratch
   const Grp g = this_grp();
   const int slot = blockIdx.x / g.size, nslot = gridDim.x / g.size;
   for (int e = slot; e < E; e += nslot) {
@@ -986,7 +987,7 @@ k_expm_batched(int E, int N, const double* A, double* X, double* work, long long
     const double* Ae = A + size_t(e) * N * N;
     for (int t = threadIdx.x + g.rank * blockDim.x; t < N * N; t += blockDim.x * g.size) Xe[t] = Ae[t];
     grp_sync(g);
-    cta_expm_pade13(N, Xe, N, work + slot * work_slot, N, iwork + slot * N, red, g);
+    cta_expm_pade13(N, Xe, N, work + slot * work_slot, N, iwork + slot * N, red, g, xsm, int(HOM_DYN / 8));
   }
 }
 
@@ -1054,7 +1055,7 @@ void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax
 void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
                          long long work_slot, int* iwork, int nslots) {
   const int ncl = std::min(E, nslots);
-  launch_clustered(k_expm_batched, ncl, cluster_size_for(ncl), 0, st, E, N, A, X, work, work_slot, iwork);
+  launch_clustered(k_expm_batched, ncl, cluster_size_for(ncl), HOM_DYN, st, E, N, A, X, work, work_slot, iwork);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }
@@ -1065,6 +1066,7 @@ void small_init() {
   cudaFuncSetAttribute(k_onesided_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_small_problem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_DYN);
   cudaFuncSetAttribute(k_small_hom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HOM_DYN);
+  cudaFuncSetAttribute(k_expm_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HOM_DYN);
   cudaFuncSetAttribute(k_spline, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * 64 * 8);
 }
 

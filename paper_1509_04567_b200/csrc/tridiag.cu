@@ -54,9 +54,14 @@ __global__ void k_burgers_rows(int nops, int n, double nu, const double* ubar, d
 // One thread per factor f: M = I - gamma_f A_{op_f}.  Writes l (multipliers), dinv (1/pivot),
 // msup (super-diagonal of M), and for periodic z = T^{-1}u, w' = T^{-T}v/(1+v^T z)
 // with the Numerical-Recipes splitting u = (gs,0..,0,alpha), v = (1,0..,0,beta/gs), gs = -M_00.
-__global__ void k_factor(int nf, int n, int periodic, const int* opidx, const double* gam,
-                         const double* sub, const double* diag, const double* sup, double* fl,
-                         double* fdinv, double* fsup, double* fz, double* fw, int* err) {
+// The recurrences are sequential; every pass reads its operands in register blocks of FCH rows
+// (independent loads in flight) so that only the arithmetic dependence chain is serial.
+constexpr int FCH = 16;
+__global__ void k_factor(int nf, int n, int periodic, const int* __restrict__ opidx, const double* __restrict__ gam,
+                         const double* __restrict__ sub, const double* __restrict__ diag,
+                         const double* __restrict__ sup, double* __restrict__ fl, double* __restrict__ fdinv,
+                         double* __restrict__ fsup, double* __restrict__ fz, double* __restrict__ fw,
+                         int* __restrict__ err) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const double g = gam[f];
@@ -76,30 +81,101 @@ __global__ void k_factor(int nf, int n, int periodic, const int* opidx, const do
   bool bad = !(fabs(dprev) > 1e-13 * fabs(d0)) || !isfinite(dprev);
   l[0] = 0.0;
   di[0] = 1.0 / dprev;
-  for (int i = 0; i < n - 1; ++i) cs[i] = -g * C[i];
-  cs[n - 1] = 0.0;
-  for (int i = 1; i < n; ++i) {
-    double Ti = 1.0 - g * B[i];
-    if (periodic && i == n - 1) Ti -= alpha * beta / gs;
-    double li = (-g * A[i]) / dprev;
-    double d = Ti - li * cs[i - 1];
-    if (!(fabs(d) > 1e-13 * (fabs(Ti) + fabs(li * cs[i - 1]))) || !isfinite(d)) bad = true;
-    l[i] = li;
-    di[i] = 1.0 / d;
-    dprev = d;
+  double cprev = -g * C[0];
+  cs[0] = cprev;
+  for (int i0 = 1; i0 < n; i0 += FCH) {
+    double a[FCH], bb[FCH], cc[FCH];
+#pragma unroll
+    for (int k = 0; k < FCH; ++k) {
+      const int i = i0 + k;
+      a[k] = i < n ? A[i] : 0.0;
+      bb[k] = i < n ? B[i] : 0.0;
+      cc[k] = i < n - 1 ? C[i] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < FCH; ++k) {
+      const int i = i0 + k;
+      if (i < n) {
+        double Ti = 1.0 - g * bb[k];
+        if (periodic && i == n - 1) Ti -= alpha * beta / gs;
+        const double li = (-g * a[k]) / dprev;
+        const double d = Ti - li * cprev;
+        if (!(fabs(d) > 1e-13 * (fabs(Ti) + fabs(li * cprev))) || !isfinite(d)) bad = true;
+        l[i] = li;
+        di[i] = 1.0 / d;
+        cprev = -g * cc[k];
+        cs[i] = i < n - 1 ? cprev : 0.0;
+        dprev = d;
+      }
+    }
   }
   if (periodic) {
     double *z = fz + fo, *w = fw + fo;
-    // z = T^{-1} u
+    // z = T^{-1} u : forward L-solve, backward U-solve
+    double zp = gs;
     z[0] = gs;
-    for (int i = 1; i < n; ++i) z[i] = ((i == n - 1) ? alpha : 0.0) - l[i] * z[i - 1];
-    z[n - 1] = z[n - 1] * di[n - 1];
-    for (int i = n - 2; i >= 0; --i) z[i] = (z[i] - cs[i] * z[i + 1]) * di[i];
+    for (int i0 = 1; i0 < n; i0 += FCH) {
+      double lv[FCH];
+#pragma unroll
+      for (int k = 0; k < FCH; ++k) lv[k] = i0 + k < n ? l[i0 + k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < FCH; ++k)
+        if (i0 + k < n) {
+          zp = ((i0 + k == n - 1) ? alpha : 0.0) - lv[k] * zp;
+          z[i0 + k] = zp;
+        }
+    }
+    zp = z[n - 1] * di[n - 1];
+    z[n - 1] = zp;
+    for (int i1 = n - 2; i1 >= 0; i1 -= FCH) {
+      double zv[FCH], cv[FCH], dv[FCH];
+#pragma unroll
+      for (int k = 0; k < FCH; ++k) {
+        const int i = i1 - k;
+        zv[k] = i >= 0 ? z[i] : 0.0;
+        cv[k] = i >= 0 ? cs[i] : 0.0;
+        dv[k] = i >= 0 ? di[i] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < FCH; ++k)
+        if (i1 - k >= 0) {
+          zp = (zv[k] - cv[k] * zp) * dv[k];
+          z[i1 - k] = zp;
+        }
+    }
     // w = T^{-T} v :  U^T q = v, then L^T w = q
     const double vl = beta / gs;
-    w[0] = 1.0 * di[0];
-    for (int i = 1; i < n; ++i) w[i] = (((i == n - 1) ? vl : 0.0) - cs[i - 1] * w[i - 1]) * di[i];
-    for (int i = n - 2; i >= 0; --i) w[i] = w[i] - l[i + 1] * w[i + 1];
+    double wp = 1.0 * di[0];
+    w[0] = wp;
+    for (int i0 = 1; i0 < n; i0 += FCH) {
+      double cv[FCH], dv[FCH];
+#pragma unroll
+      for (int k = 0; k < FCH; ++k) {
+        cv[k] = i0 + k < n ? cs[i0 + k - 1] : 0.0;
+        dv[k] = i0 + k < n ? di[i0 + k] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < FCH; ++k)
+        if (i0 + k < n) {
+          wp = (((i0 + k == n - 1) ? vl : 0.0) - cv[k] * wp) * dv[k];
+          w[i0 + k] = wp;
+        }
+    }
+    for (int i1 = n - 2; i1 >= 0; i1 -= FCH) {
+      double wv[FCH], lv[FCH];
+#pragma unroll
+      for (int k = 0; k < FCH; ++k) {
+        const int i = i1 - k;
+        wv[k] = i >= 0 ? w[i] : 0.0;
+        lv[k] = i >= 0 ? l[i + 1] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < FCH; ++k)
+        if (i1 - k >= 0) {
+          wp = wv[k] - lv[k] * wp;
+          w[i1 - k] = wp;
+        }
+    }
     const double denom = 1.0 + z[0] + vl * z[n - 1];
     if (!(fabs(denom) > 0.0) || !isfinite(denom)) bad = true;
     const double inv = 1.0 / denom;

@@ -199,37 +199,53 @@ __global__ void k_reduce(int nx, int ny, int nch, const double* part, double* D,
 // Square-ish X^T Y for 32 < nx, ny <= 64 (the s x s Grams and cross products of the two-pass
 // source SVD, s = 64): a stage of SQ_TR rows of X and Y sits in shared memory row-major; the
 // 256 threads form 4 row groups x (8 x 8) threads, each thread owning an 8 x 8 output tile
-// (4 FMA per shared load, double2 loads), the 4 row-group partials are summed at the end.
-constexpr int SQ_TR = 16;
+// (4 FMA per shared load, double2 loads); the next stage is prefetched into registers while the
+// current one is consumed; the 4 row-group partials are summed at the end (stage buffers reused).
+constexpr int SQ_TR = 32;
 __global__ void __launch_bounds__(PEXP_THREADS)
 k_xty_sq(int n, int rch, const double* X, long long xs_e, int x0, int nx, const double* Y, long long ys_e, int y0,
          int ny, double* part) {
-  __shared__ __align__(16) double Xs[SQ_TR][64];
-  __shared__ __align__(16) double Ys[SQ_TR][64];
-  __shared__ double red[3][64 * 64 / 4];  // row-group partials 1..3, reduced in quarters
+  __shared__ __align__(16) double stg[2 * SQ_TR * 64];  // Xs | Ys, later the row-group partials
+  double (*Xs)[64] = reinterpret_cast<double (*)[64]>(stg);
+  double (*Ys)[64] = reinterpret_cast<double (*)[64]>(stg + SQ_TR * 64);
   const int e = blockIdx.y, ch = blockIdx.x, nch = gridDim.x;
   const int t = threadIdx.x, grp = t >> 6, tx = t & 7, ty = (t >> 3) & 7;
   const double* Xe = X + e * xs_e + size_t(x0) * n;
   const double* Ye = Y + e * ys_e + size_t(y0) * n;
+  const bool same = (Xe == Ye) && nx == ny;
+  constexpr int LPT = SQ_TR * 64 / PEXP_THREADS;  // elements per thread per operand and stage
   double acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
   const int r0 = ch * rch, r1 = min(n, r0 + rch);
+  double px[LPT], py[LPT];
+  auto fetch = [&](int rb) {
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int idx = t + q * PEXP_THREADS, a = idx / SQ_TR, r = idx % SQ_TR, row = rb + r;  // rows fastest
+      px[q] = (a < nx && row < r1) ? __ldcg(Xe + size_t(a) * n + row) : 0.0;
+      py[q] = (!same && a < ny && row < r1) ? __ldcg(Ye + size_t(a) * n + row) : 0.0;
+    }
+  };
+  if (r0 < r1) fetch(r0);
   for (int rb = r0; rb < r1; rb += SQ_TR) {
     __syncthreads();
-    for (int idx = t; idx < SQ_TR * 64; idx += PEXP_THREADS) {
-      const int a = idx / SQ_TR, r = idx % SQ_TR, row = rb + r;  // coalesced along rows
-      Xs[r][a] = (a < nx && row < r1) ? Xe[size_t(a) * n + row] : 0.0;
-      Ys[r][a] = (a < ny && row < r1) ? Ye[size_t(a) * n + row] : 0.0;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int idx = t + q * PEXP_THREADS, a = idx / SQ_TR, r = idx % SQ_TR;
+      Xs[r][a] = px[q];
+      if (!same) Ys[r][a] = py[q];
     }
     __syncthreads();
-#pragma unroll 4
+    if (rb + SQ_TR < r1) fetch(rb + SQ_TR);
+    const double (*Yr)[64] = same ? Xs : Ys;
+#pragma unroll 2
     for (int r = grp; r < SQ_TR; r += 4) {
       double xv[8], yv[8];
       const double2* xp = reinterpret_cast<const double2*>(&Xs[r][ty * 8]);
-      const double2* yp = reinterpret_cast<const double2*>(&Ys[r][tx * 8]);
+      const double2* yp = reinterpret_cast<const double2*>(&Yr[r][tx * 8]);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         double2 a2 = xp[q], b2 = yp[q];
@@ -242,16 +258,17 @@ k_xty_sq(int n, int rch, const double* X, long long xs_e, int x0, int nx, const 
         for (int j = 0; j < 8; ++j) acc[i][j] = fma(xv[i], yv[j], acc[i][j]);
     }
   }
-  // sum the 4 row-group partials, one quarter of the 64 x 64 tile at a time (static smem budget)
+  // sum the 4 row-group partials, a quarter of every thread tile at a time (3 x 1024 doubles)
+  double* red = stg;
   double* P = part + (size_t(e) * nch + ch) * size_t(nx) * ny;
 #pragma unroll
-  for (int qt = 0; qt < 4; ++qt) {  // quarter qt: rows i in [2qt, 2qt+2) of every thread tile
+  for (int qt = 0; qt < 4; ++qt) {  // rows i in [2qt, 2qt+2) of every thread tile
     __syncthreads();
     if (grp > 0)
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) red[grp - 1][((ty * 2 + i) * 8 + tx) * 8 + j] = acc[2 * qt + i][j];
+        for (int j = 0; j < 8; ++j) red[(grp - 1) * 1024 + ((ty * 2 + i) * 8 + tx) * 8 + j] = acc[2 * qt + i][j];
     __syncthreads();
     if (grp == 0)
 #pragma unroll
@@ -259,7 +276,7 @@ k_xty_sq(int n, int rch, const double* X, long long xs_e, int x0, int nx, const 
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int k = ((ty * 2 + i) * 8 + tx) * 8 + j;
-          const double v = acc[2 * qt + i][j] + red[0][k] + red[1][k] + red[2][k];
+          const double v = acc[2 * qt + i][j] + red[k] + red[1024 + k] + red[2048 + k];
           const int a = ty * 8 + 2 * qt + i, b = tx * 8 + j;
           if (a < nx && b < ny) P[a + size_t(b) * nx] = v;
         }

@@ -256,3 +256,28 @@ def test_burgers_small_chunked():
     ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
+
+
+def test_burgers_config5_full_size_first_iterate():
+    """C5 at its full size (n = 65536, P = 256, s = 64) in the bench's launch configuration, one
+    WR iteration: u_0 ≡ u0 makes the first iterate the closed form u_1(t) = u0 + t φ1(tB) c with
+    B = νD2 + J(u0), c = νD2 u0 - u0∘D1 u0 (SURVEY §8(c).4 'WR iteration 1', pinned by
+    test_wr_first_iterate_closed_form).  The reference evaluates it at all T_i with the oracle's
+    SaI Krylov routine (η = 1e-12) on the constant rank-1 source."""
+    from oracle.ebk import ebk_krylov
+    from oracle.operators import burgers_J, d1_matrix, d2_matrix
+    p = synth.config5()
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=960, basis_cols=960, eval_chunk=64)
+    out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, 1)
+    out = out.cpu().numpy()
+    assert st["wr_iters"] == 1
+    B = (p.nu * d2_matrix(p.n) + burgers_J(p.u0, p.n)).tocsr()
+    cv = p.nu * (d2_matrix(p.n) @ p.u0) - p.u0 * (d1_matrix(p.n) @ p.u0)
+    beta = np.linalg.norm(cv)
+    coef = np.zeros((p.P, 4, 1))
+    coef[:, 0, 0] = beta
+    Y = ebk_krylov(B, (cv / beta)[:, None], coef, p.T / p.P, p.P, gamma=0.1, eta=1e-12)
+    ref = Y[1:] + p.u0[None, :]
+    assert rel(out, ref) < 1e-8, st
+    # mass is conserved by every WR iterate (periodic central differences)
+    assert np.abs(out.sum(axis=1) - p.u0.sum()).max() < 1e-9 * np.abs(p.u0).sum()
