@@ -224,238 +224,348 @@ __device__ inline void cta_apply(int ld, int rows, double* W, int m, const doubl
 
 // Pivoted, diagonally scaled, deflating Cholesky of the Gram G (m x m, ld MB) -> Rinv (ld MB),
 // classes cls (1 accepted, 2 deferred, 0 dead), optional re-ordered norm0 (see k_block_chol).
+// m <= 32: the whole factorisation runs in warp 0 (lane i owns row i; warp argmax for the pivot,
+// __syncwarp between phases, no CTA barriers); one __syncthreads publishes the results.
 template <int MB>
 __device__ inline void cta_chol_piv(int m, const double* G, const double* norm0, double defl, double dtol,
                                     double piv_tol, SmemT& s, int* cls, int* perm, int* used, int* dead) {
   constexpr int LD = MB + 1;
-  __shared__ int s_np, s_j, s_nd;
-  __shared__ double s_piv;
-  for (int k = threadIdx.x; k < m; k += PEXP_THREADS) {
-    double g = G[k + k * MB];
-    bool dk = !(g > 0.0);
-    if (norm0 && !(g > defl * defl * norm0[k])) dk = true;
-    dead[k] = dk;
-    used[k] = 0;
-    s.d[k] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < m * m; idx += PEXP_THREADS) {
-    int i = idx % m, j = idx / m;
-    s.S[i * LD + j] = s.d[i] * s.d[j] * 0.5 * (G[i + j * MB] + G[j + i * MB]);
-    s.Lp[i * LD + j] = 0.0;
-  }
-  if (threadIdx.x == 0) s_np = 0;
-  __syncthreads();
-  for (int t = 0; t < m; ++t) {
-    if (threadIdx.x == 0) {
-      int jb = -1;
-      double best = dtol > 0.0 ? dtol : piv_tol;
-      for (int j = 0; j < m; ++j)
-        if (!used[j] && !dead[j] && s.S[j * LD + j] > best) { best = s.S[j * LD + j]; jb = j; }
-      s_j = jb;
-      if (jb >= 0) {
-        used[jb] = 1;
-        perm[t] = jb;
-        s_piv = sqrt(best);
-        s_np = t + 1;
-      }
+  if (threadIdx.x < 32) {
+    const int i = threadIdx.x;
+    const unsigned full = 0xffffffffu;
+    if (i < m) {
+      const double g = G[i + i * MB];
+      bool di = !(g > 0.0);
+      if (norm0 && !(g > defl * defl * norm0[i])) di = true;
+      dead[i] = di;
+      used[i] = 0;
+      s.d[i] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
     }
-    __syncthreads();
-    const int jb = s_j;
-    if (jb < 0) break;
-    const double pv = s_piv;
-    for (int i = threadIdx.x; i < m; i += PEXP_THREADS)
-      s.Xw[i * LD] = (i == jb) ? pv : (used[i] ? 0.0 : s.S[i * LD + jb] / pv);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < m * m; idx += PEXP_THREADS) {
-      int i = idx % m, k = idx / m;
-      if (!used[i] && !used[k]) s.S[i * LD + k] -= s.Xw[i * LD] * s.Xw[k * LD];
-    }
-    for (int i = threadIdx.x; i < m; i += PEXP_THREADS) s.Lp[i * LD + t] = s.Xw[i * LD];
-    __syncthreads();
-  }
-  const int np = s_np;
-  if (threadIdx.x == 0) {
-    int q = np, nd = 0;
-    if (dtol > 0.0)
-      for (int j = 0; j < m; ++j)
-        if (!used[j] && !dead[j]) { perm[q++] = j; ++nd; }
-    for (int j = 0; j < m; ++j)
-      if (!used[j] && (dtol <= 0.0 || dead[j])) perm[q++] = j;
-    s_nd = nd;
-  }
-  __syncthreads();
-  const int nd = s_nd;
-  // X = Rp^{-1} (leading np x np), Rp[t][a] = Lp[perm[a]][t]
-  for (int j = threadIdx.x; j < m; j += PEXP_THREADS) {
-    for (int k = 0; k < m; ++k) s.Xw[k * LD + j] = 0.0;
-    if (j < np)
-      for (int k = j; k >= 0; --k) {
-        double sum = (k == j) ? 1.0 : 0.0;
-        for (int q = k + 1; q <= j; ++q) sum -= s.Lp[perm[q] * LD + k] * s.Xw[q * LD + j];
-        s.Xw[k * LD + j] = sum / s.Lp[perm[k] * LD + k];
+    __syncwarp();
+    if (i < m)
+      for (int j = 0; j < m; ++j) {
+        s.S[i * LD + j] = s.d[i] * s.d[j] * 0.5 * (G[i + j * MB] + G[j + i * MB]);
+        s.Lp[i * LD + j] = 0.0;
       }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < MB * MB; idx += PEXP_THREADS) s.Rinv[idx] = 0.0;
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < m * m; idx += PEXP_THREADS) {
-    int a = idx % m, t = idx / m;
-    s.Rinv[perm[a] + t * MB] = s.d[perm[a]] * s.Xw[a * LD + t];
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < nd; q += PEXP_THREADS) s.Rinv[perm[np + q] + (np + q) * MB] = 1.0;
-  for (int k = threadIdx.x; k < m; k += PEXP_THREADS) {
-    cls[k] = k < np ? 1 : (k < np + nd ? 2 : 0);
-    if (norm0) s.n0p[k] = norm0[perm[k]];
+    __syncwarp();
+    const double best0 = dtol > 0.0 ? dtol : piv_tol;
+    int np = 0;
+    for (int t = 0; t < m; ++t) {
+      // argmax of the remaining scaled pivots (strictly above best0; ties -> lowest index)
+      double cv = -1.0;
+      if (i < m && !used[i] && !dead[i] && s.S[i * LD + i] > best0) cv = s.S[i * LD + i];
+      int ci = i;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(full, cv, o);
+        const int oi = __shfl_xor_sync(full, ci, o);
+        if (ov > cv || (ov == cv && oi < ci)) { cv = ov; ci = oi; }
+      }
+      if (cv < 0.0) break;  // uniform over the warp
+      const int jb = ci;
+      const double pv = sqrt(cv);
+      double xw = 0.0;
+      if (i < m) xw = (i == jb) ? pv : (used[i] ? 0.0 : s.S[i * LD + jb] / pv);
+      __syncwarp();
+      if (i == 0) { used[jb] = 1; perm[t] = jb; }
+      __syncwarp();
+      if (i < m) {
+        s.Xw[i * LD] = xw;
+        s.Lp[i * LD + t] = xw;
+      }
+      __syncwarp();
+      if (i < m && !used[i])
+        for (int k = 0; k < m; ++k)
+          if (!used[k]) s.S[i * LD + k] -= xw * s.Xw[k * LD];
+      __syncwarp();
+      np = t + 1;
+    }
+    int nd = 0;
+    if (i == 0) {
+      int q = np;
+      if (dtol > 0.0)
+        for (int j = 0; j < m; ++j)
+          if (!used[j] && !dead[j]) { perm[q++] = j; ++nd; }
+      for (int j = 0; j < m; ++j)
+        if (!used[j] && (dtol <= 0.0 || dead[j])) perm[q++] = j;
+    }
+    nd = __shfl_sync(full, nd, 0);
+    __syncwarp();
+    // X = Rp^{-1} (leading np x np), Rp[t][a] = Lp[perm[a]][t]; lane j owns column j
+    if (i < m) {
+      for (int k = 0; k < m; ++k) s.Xw[k * LD + i] = 0.0;
+      if (i < np)
+        for (int k = i; k >= 0; --k) {
+          double sum = (k == i) ? 1.0 : 0.0;
+          for (int q = k + 1; q <= i; ++q) sum -= s.Lp[perm[q] * LD + k] * s.Xw[q * LD + i];
+          s.Xw[k * LD + i] = sum / s.Lp[perm[k] * LD + k];
+        }
+    }
+    __syncwarp();
+    for (int idx = i; idx < MB * MB; idx += 32) s.Rinv[idx] = 0.0;
+    __syncwarp();
+    for (int idx = i; idx < m * m; idx += 32) {
+      const int a = idx % m, t = idx / m;
+      s.Rinv[perm[a] + t * MB] = s.d[perm[a]] * s.Xw[a * LD + t];
+    }
+    __syncwarp();
+    if (i < nd) s.Rinv[perm[np + i] + (np + i) * MB] = 1.0;
+    if (i < m) {
+      cls[i] = i < np ? 1 : (i < np + nd ? 2 : 0);
+      if (norm0) s.n0p[i] = norm0[perm[i]];
+    }
   }
   __syncthreads();
 }
 
 // ---------------------------------------------------------------- cluster-split SaI solve
 // Forward L-solve y_g = -l_g y_{g-1} + b_g and backward U-solve x_g = -d_g c_g x_{g+1} + d_g y_g
-// as affine maps (scan.cuh).  Rows [g0, g0 + cnt) belong to this CTA; each thread composes EPT
-// consecutive rows of a CHUNK, a block scan composes the threads.
-__device__ inline Aff seg_map_fwd(int g0, int cnt, const double* l, const double* b, Aff* wsm) {
+// as affine maps (scan.cuh), for a group of up to CB columns at once: the maps of all columns of
+// a row share their multiplier (-l_g, resp. -d_g c_g) and differ only in the offset, so one block
+// scan carries 1 + CB values.  Rows [g0, g0 + cnt) belong to this CTA; thread t composes the EPT
+// consecutive rows t*EPT.. of each CHUNK; chunks are chained through the running carry.
+constexpr int CB = 8;
+
+// Exclusive block scan of (A, B[CB]) maps ordered by rank (REV: rank = 255 - threadIdx.x).
+// Returns the exclusive prefix in (pA, pB) and the block total in (tA, tB).
+template <bool REV>
+__device__ inline void block_scan_multi(double A, const double (&B)[CB], double* wsmM, double& pA, double (&pB)[CB],
+                                        double& tA, double (&tB)[CB]) {
+  const int rank = REV ? PEXP_THREADS - 1 - threadIdx.x : threadIdx.x;
+  const int lane = rank & 31, w = rank >> 5;
+  double iA = A, iB[CB];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) iB[c] = B[c];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double qa = REV ? __shfl_down_sync(0xffffffffu, iA, o) : __shfl_up_sync(0xffffffffu, iA, o);
+    double qb[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+      qb[c] = REV ? __shfl_down_sync(0xffffffffu, iB[c], o) : __shfl_up_sync(0xffffffffu, iB[c], o);
+    if (lane >= o) {  // (q then i): A = iA*qa, B = iA*qb + iB
+#pragma unroll
+      for (int c = 0; c < CB; ++c) iB[c] = fma(iA, qb[c], iB[c]);
+      iA *= qa;
+    }
+  }
+  double eA = REV ? __shfl_down_sync(0xffffffffu, iA, 1) : __shfl_up_sync(0xffffffffu, iA, 1);
+  double eB[CB];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) eB[c] = REV ? __shfl_down_sync(0xffffffffu, iB[c], 1) : __shfl_up_sync(0xffffffffu, iB[c], 1);
+  if (lane == 0) {
+    eA = 1.0;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) eB[c] = 0.0;
+  }
+  constexpr int NW = PEXP_THREADS / 32, ST = CB + 1;
+  __syncthreads();
+  if (lane == 31) {
+    wsmM[w * ST] = iA;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) wsmM[w * ST + 1 + c] = iB[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < ST) {  // thread c' composes component c' over the warps (A first, then the B's)
+    const int c = threadIdx.x;
+    double accA = 1.0, accB = 0.0;
+    for (int k = 0; k < NW; ++k) {
+      const double ta = wsmM[k * ST], tb = c == 0 ? 0.0 : wsmM[k * ST + c];
+      // store the exclusive prefix of warp k in slot (NW + k)
+      wsmM[(NW + k) * ST + c] = c == 0 ? accA : accB;
+      if (c > 0) accB = fma(ta, accB, tb);
+      accA *= ta;
+    }
+    wsmM[2 * NW * ST + c] = c == 0 ? accA : accB;
+  }
+  __syncthreads();
+  const double wA = wsmM[(NW + w) * ST];
+  // prefix = (warp prefix) then (exclusive within the warp)
+  pA = eA * wA;
+#pragma unroll
+  for (int c = 0; c < CB; ++c) pB[c] = fma(eA, wsmM[(NW + w) * ST + 1 + c], eB[c]);
+  tA = wsmM[2 * NW * ST];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) tB[c] = wsmM[2 * NW * ST + 1 + c];
+  __syncthreads();
+}
+
+// Forward segment maps (no writes) of columns [c0, c0 + nc) of b (ld ldb): total map per column.
+__device__ inline void seg_maps_fwd(int g0, int cnt, const double* l, const double* b, int ldb, int nc, double* wsmM,
+                                    double& TA, double (&TB)[CB]) {
   const int t = threadIdx.x;
-  Aff acc{1.0, 0.0};
+  TA = 1.0;
+#pragma unroll
+  for (int c = 0; c < CB; ++c) TB[c] = 0.0;
   for (int base = 0; base < cnt; base += CHUNK) {
-    Aff mp{1.0, 0.0};
+    double A = 1.0, B[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) B[c] = 0.0;
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const int i = base + t * EPT + k;
-      if (i < cnt) mp = after(mp, Aff{-l[g0 + i], b[i]});
+      if (i < cnt) {
+        const double a = -l[g0 + i];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) B[c] = fma(a, B[c], c < nc ? b[size_t(c) * ldb + i] : 0.0);
+        A *= a;
+      }
     }
-    Aff tot;
-    block_excl_scan<false>(mp, t, wsm, tot);
-    acc = after(acc, tot);
+    double pA, pB[CB], tA, tB[CB];
+    block_scan_multi<false>(A, B, wsmM, pA, pB, tA, tB);
+#pragma unroll
+    for (int c = 0; c < CB; ++c) TB[c] = fma(tA, TB[c], tB[c]);
+    TA *= tA;
   }
-  return acc;
 }
 
-__device__ inline Aff seg_map_bwd(int g0, int cnt, const double* di, const double* cs, const double* y, Aff* wsm) {
+// Forward pass with carry-in: y (ld ldy) from b (ld ldb); thread t solves its EPT rows in registers.
+__device__ inline void seg_fwd_multi(int g0, int cnt, const double* l, const double* b, int ldb, double* y, int ldy,
+                                     int nc, const double (&carry0)[CB], double* wsmM) {
   const int t = threadIdx.x;
-  Aff acc{1.0, 0.0};
+  double carry[CB];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) carry[c] = carry0[c];
+  for (int base = 0; base < cnt; base += CHUNK) {
+    double av[EPT], A = 1.0, B[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) B[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int i = base + t * EPT + k;
+      av[k] = i < cnt ? -l[g0 + i] : 1.0;
+      if (i < cnt) {
+#pragma unroll
+        for (int c = 0; c < CB; ++c) B[c] = fma(av[k], B[c], c < nc ? b[size_t(c) * ldb + i] : 0.0);
+        A *= av[k];
+      }
+    }
+    double pA, pB[CB], tA, tB[CB];
+    block_scan_multi<false>(A, B, wsmM, pA, pB, tA, tB);
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      if (c < nc) {
+        double v = fma(pA, carry[c], pB[c]);
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          const int i = base + t * EPT + k;
+          if (i < cnt) {
+            v = fma(av[k], v, b[size_t(c) * ldb + i]);
+            y[size_t(c) * ldy + i] = v;
+          }
+        }
+      }
+      carry[c] = fma(tA, carry[c], tB[c]);
+    }
+  }
+}
+
+// Backward segment maps of y (ld ldy): total map per column (rows in descending order).
+__device__ inline void seg_maps_bwd(int g0, int cnt, const double* di, const double* cs, const double* y, int ldy,
+                                    int nc, double* wsmM, double& TA, double (&TB)[CB]) {
+  const int t = threadIdx.x;
+  TA = 1.0;
+#pragma unroll
+  for (int c = 0; c < CB; ++c) TB[c] = 0.0;
   for (int base = ((cnt - 1) / CHUNK) * CHUNK; base >= 0 && cnt > 0; base -= CHUNK) {
-    Aff mp{1.0, 0.0};
+    double A = 1.0, B[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) B[c] = 0.0;
 #pragma unroll
     for (int k = EPT - 1; k >= 0; --k) {
       const int i = base + t * EPT + k;
       if (i < cnt) {
-        const double dv = di[g0 + i];
-        mp = after(mp, Aff{-dv * cs[g0 + i], dv * y[i]});
+        const double dv = di[g0 + i], a = -dv * cs[g0 + i];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) B[c] = fma(a, B[c], c < nc ? dv * y[size_t(c) * ldy + i] : 0.0);
+        A *= a;
       }
     }
-    Aff tot;
-    block_excl_scan<true>(mp, PEXP_THREADS - 1 - t, wsm, tot);
-    acc = after(acc, tot);
-  }
-  return acc;
-}
-
-// Forward pass with carry-in: y[i] (own rows) from b[i]; returns nothing (y written to out).
-__device__ inline void seg_fwd(int g0, int cnt, const double* l, const double* b, double* y, double carry, double* s0,
-                               double* s1, Aff* wsm) {
-  const int t = threadIdx.x;
-  for (int base = 0; base < cnt; base += CHUNK) {
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      const int g = base + i;
-      const int si = (i / EPT) * SPAD + (i % EPT);
-      s0[si] = g < cnt ? b[g] : 0.0;
-      s1[si] = g < cnt ? -l[g0 + g] : 1.0;
-    }
-    __syncthreads();
-    Aff mp{1.0, 0.0};
+    double pA, pB[CB], tA, tB[CB];
+    block_scan_multi<true>(A, B, wsmM, pA, pB, tA, tB);
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) mp = after(mp, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
-    Aff tot;
-    Aff pre = block_excl_scan<false>(mp, t, wsm, tot);
-    double v = fma(pre.A, carry, pre.B);
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      v = fma(s1[t * SPAD + k], v, s0[t * SPAD + k]);
-      s0[t * SPAD + k] = v;
-    }
-    carry = fma(tot.A, carry, tot.B);
-    __syncthreads();
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      const int g = base + i;
-      if (g < cnt) y[g] = s0[(i / EPT) * SPAD + (i % EPT)];
-    }
-    __syncthreads();
+    for (int c = 0; c < CB; ++c) TB[c] = fma(tA, TB[c], tB[c]);
+    TA *= tA;
   }
 }
 
-// Backward pass with carry-in (from the rows above this segment), periodic correction -f*z;
-// writes x into x and x2; returns this CTA's partial ||x||^2 (block-reduced).
-__device__ inline double seg_bwd(int g0, int cnt, const double* di, const double* cs, const double* fz, double f,
-                                 double* x, double* x2, double carry, double* s0, double* s1, Aff* wsm, double* red) {
+// Backward pass with carry-in (from the rows above this segment), periodic correction -f_c z;
+// x overwrites y (ld ldy) and is copied to x2 (ld ldx2); per-column ||x||^2 partials into nrm.
+__device__ inline void seg_bwd_multi(int g0, int cnt, const double* di, const double* cs, const double* fz,
+                                     const double (&f)[CB], double* y, int ldy, double* x2, int ldx2, int nc,
+                                     const double (&carry0)[CB], double* wsmM, double (&nrm)[CB]) {
   const int t = threadIdx.x;
-  double nrm2 = 0.0;
+  double carry[CB];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) { carry[c] = carry0[c]; nrm[c] = 0.0; }
   for (int base = ((cnt - 1) / CHUNK) * CHUNK; base >= 0 && cnt > 0; base -= CHUNK) {
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      const int g = base + i;
-      const int si = (i / EPT) * SPAD + (i % EPT);
-      if (g < cnt) {
-        const double dv = di[g0 + g];
-        s0[si] = dv * x[g];
-        s1[si] = -dv * cs[g0 + g];
-      } else {
-        s0[si] = 0.0;
-        s1[si] = 1.0;
-      }
-    }
-    __syncthreads();
-    Aff mp{1.0, 0.0};
+    double av[EPT], dvv[EPT], A = 1.0, B[CB];
 #pragma unroll
-    for (int k = EPT - 1; k >= 0; --k) mp = after(mp, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
-    Aff tot;
-    Aff pre = block_excl_scan<true>(mp, PEXP_THREADS - 1 - t, wsm, tot);
-    double v = fma(pre.A, carry, pre.B);
+    for (int c = 0; c < CB; ++c) B[c] = 0.0;
 #pragma unroll
     for (int k = EPT - 1; k >= 0; --k) {
-      v = fma(s1[t * SPAD + k], v, s0[t * SPAD + k]);
-      s0[t * SPAD + k] = v;
-    }
-    carry = fma(tot.A, carry, tot.B);
-    __syncthreads();
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      const int g = base + i;
-      if (g < cnt) {
-        double w = s0[(i / EPT) * SPAD + (i % EPT)];
-        if (fz) w = fma(-f, fz[g0 + g], w);
-        x[g] = w;
-        x2[g] = w;
-        nrm2 = fma(w, w, nrm2);
+      const int i = base + t * EPT + k;
+      dvv[k] = i < cnt ? di[g0 + i] : 0.0;
+      av[k] = i < cnt ? -dvv[k] * cs[g0 + i] : 1.0;
+      if (i < cnt) {
+#pragma unroll
+        for (int c = 0; c < CB; ++c) B[c] = fma(av[k], B[c], c < nc ? dvv[k] * y[size_t(c) * ldy + i] : 0.0);
+        A *= av[k];
       }
     }
-    __syncthreads();
+    double pA, pB[CB], tA, tB[CB];
+    block_scan_multi<true>(A, B, wsmM, pA, pB, tA, tB);
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      if (c < nc) {
+        double v = fma(pA, carry[c], pB[c]);
+#pragma unroll
+        for (int k = EPT - 1; k >= 0; --k) {
+          const int i = base + t * EPT + k;
+          if (i < cnt) {
+            v = fma(av[k], v, dvv[k] * y[size_t(c) * ldy + i]);
+            const double w = fz ? fma(-f[c], fz[g0 + i], v) : v;
+            y[size_t(c) * ldy + i] = w;
+            x2[size_t(c) * ldx2 + i] = w;
+            nrm[c] = fma(w, w, nrm[c]);
+          }
+        }
+      }
+      carry[c] = fma(tA, carry[c], tB[c]);
+    }
   }
-  return block_sum(nrm2, red);
 }
 
 // m columns W_c = (I - gamma A)^{-1} Vb_c on the cluster-split rows; W0 gets a copy; s.n0[c] =
-// ||W_c||^2 (cluster-reduced).  xch layout: [0,2MB) forward maps, [2MB,3MB) periodic dots,
-// [3MB,5MB) backward maps, [5MB,6MB) norm partials; s.Gp scratch for the reduced norms.
+// ||W_c||^2 (cluster-reduced).  xch layout (per column c < MB): [0,2MB) forward maps, [2MB,3MB)
+// periodic dots, [3MB,5MB) backward maps, [5MB,6MB) norm partials.
 template <int MB>
 __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int ld, int g0, int cnt, int periodic,
                                     const double* l, const double* di, const double* sup, const double* fz,
                                     const double* fw, const double* Vb, int m, double* W, int ldw, double* W0,
-                                    SmemT& s, Aff* wsm, double* red) {
+                                    SmemT& s, double* wsmM, double* red) {
   double* xf = s.xch;
   double* xd = s.xch + 2 * MB;
   double* xb = s.xch + 3 * MB;
   double* xn = s.xch + 5 * MB;
   // ---- forward segment maps (+ the periodic Sherman-Morrison dots w'^T b)
-  for (int c = 0; c < m; ++c) {
-    const double* b = Vb + size_t(c) * ld;
-    Aff F = (cs > 1 && cr < cs - 1) ? seg_map_fwd(g0, cnt, l, b, wsm) : Aff{1.0, 0.0};
-    double dot = 0.0;
-    if (periodic)
-      for (int i = threadIdx.x; i < cnt; i += PEXP_THREADS) dot = fma(fw[g0 + i], b[i], dot);
-    dot = periodic ? block_sum(dot, red) : 0.0;
-    if (threadIdx.x == 0) { xf[2 * c] = F.A; xf[2 * c + 1] = F.B; xd[c] = dot; }
+  for (int c0 = 0; c0 < m; c0 += CB) {
+    const int nc = min(CB, m - c0);
+    double TA = 1.0, TB[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) TB[c] = 0.0;
+    if (cs > 1 && cr < cs - 1) seg_maps_fwd(g0, cnt, l, Vb + size_t(c0) * ld, ld, nc, wsmM, TA, TB);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < nc; ++c) { xf[2 * (c0 + c)] = TA; xf[2 * (c0 + c) + 1] = TB[c]; }
   }
+  if (periodic)
+    for (int c = 0; c < m; ++c) {
+      double dot = 0.0;
+      for (int i = threadIdx.x; i < cnt; i += PEXP_THREADS) dot = fma(fw[g0 + i], Vb[size_t(c) * ld + i], dot);
+      dot = block_sum(dot, red);
+      if (threadIdx.x == 0) xd[c] = dot;
+    }
+  else if (threadIdx.x < m)
+    xd[threadIdx.x] = 0.0;
   cl_sync(cl, cs);
   __shared__ double carry_s[MB], f_s[MB];
   for (int c = threadIdx.x; c < m; c += PEXP_THREADS) {
@@ -469,11 +579,23 @@ __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int l
     f_s[c] = f;
   }
   __syncthreads();
-  for (int c = 0; c < m; ++c) seg_fwd(g0, cnt, l, Vb + size_t(c) * ld, W + size_t(c) * ldw, carry_s[c], s.Cx, s.Cy, wsm);
+  for (int c0 = 0; c0 < m; c0 += CB) {
+    const int nc = min(CB, m - c0);
+    double cin[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) cin[c] = c < nc ? carry_s[c0 + c] : 0.0;
+    seg_fwd_multi(g0, cnt, l, Vb + size_t(c0) * ld, ld, W + size_t(c0) * ldw, ldw, nc, cin, wsmM);
+  }
+  __syncthreads();
   // ---- backward segment maps
-  for (int c = 0; c < m; ++c) {
-    Aff Bm = (cs > 1 && cr > 0) ? seg_map_bwd(g0, cnt, di, sup, W + size_t(c) * ldw, wsm) : Aff{1.0, 0.0};
-    if (threadIdx.x == 0) { xb[2 * c] = Bm.A; xb[2 * c + 1] = Bm.B; }
+  for (int c0 = 0; c0 < m; c0 += CB) {
+    const int nc = min(CB, m - c0);
+    double TA = 1.0, TB[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) TB[c] = 0.0;
+    if (cs > 1 && cr > 0) seg_maps_bwd(g0, cnt, di, sup, W + size_t(c0) * ldw, ldw, nc, wsmM, TA, TB);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < nc; ++c) { xb[2 * (c0 + c)] = TA; xb[2 * (c0 + c) + 1] = TB[c]; }
   }
   cl_sync(cl, cs);
   for (int c = threadIdx.x; c < m; c += PEXP_THREADS) {
@@ -485,18 +607,25 @@ __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int l
     carry_s[c] = carry;
   }
   __syncthreads();
-  for (int c = 0; c < m; ++c) {
-    double nr = seg_bwd(g0, cnt, di, sup, periodic ? fz : nullptr, f_s[c], W + size_t(c) * ldw, W0 + size_t(c) * ld,
-                        carry_s[c], s.Cx, s.Cy, wsm, red);
-    if (threadIdx.x == 0) xn[c] = nr;
+  for (int c0 = 0; c0 < m; c0 += CB) {
+    const int nc = min(CB, m - c0);
+    double cin[CB], fc[CB], nrm[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) { cin[c] = c < nc ? carry_s[c0 + c] : 0.0; fc[c] = c < nc ? f_s[c0 + c] : 0.0; }
+    seg_bwd_multi(g0, cnt, di, sup, periodic ? fz : nullptr, fc, W + size_t(c0) * ldw, ldw, W0 + size_t(c0) * ld,
+                  ld, nc, cin, wsmM, nrm);
+    for (int c = 0; c < nc; ++c) {
+      const double nr = block_sum(nrm[c], red);
+      if (threadIdx.x == 0) xn[c0 + c] = nr;
+    }
   }
   cl_allreduce(cl, cs, xn, s.n0, m);
 }
 
 template <int MB>
-__global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
+__global__ void __launch_bounds__(PEXP_THREADS, MB <= 8 ? 2 : 1) k_arnoldi_step(StepArgs A) {
   extern __shared__ double sm[];
-  __shared__ Aff wsm[PEXP_THREADS / 32 + 1];
+  __shared__ double wsmM[(2 * (PEXP_THREADS / 32) + 1) * (CB + 1)];
   __shared__ double red[32];
   __shared__ int cls[MB], perm[MB], used[MB], dead[MB];
   cg::cluster_group cl = cg::this_cluster();
@@ -539,7 +668,7 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
   // ---- W0 = (I - gamma A)^{-1} V_b   (kept in W0; working copy in W)
   cl_sai_solve<MB>(cl, cs, cr, n, g0, cnt, A.periodic, A.fl + fo, A.fdinv + fo, A.fsup + fo,
                    A.periodic ? A.fz + fo : nullptr, A.periodic ? A.fw + fo : nullptr, V + size_t(b * m) * n, m, W,
-                   ldw, W0, s, wsm, red);
+                   ldw, W0, s, wsmM, red);
   // ---- BCGS pass 1
   cta_vtw<MB>(n, ldw, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
   cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
@@ -553,8 +682,16 @@ __global__ void __launch_bounds__(PEXP_THREADS) k_arnoldi_step(StepArgs A) {
   cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
   cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 1e-8, A.piv_tol, s, cls, perm, used, dead);
   cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
-  // ---- stage B: explicit CGS2 of deferred columns against accepted ones
-  for (int rep = 0; rep < 2; ++rep) {
+  // ---- stage B: explicit CGS2 of deferred columns against accepted ones (skipped when the
+  // stage-A factorisation deferred nothing; cls is identical in every CTA of the cluster)
+  __shared__ int s_ndef;
+  if (threadIdx.x == 0) {
+    int nd = 0;
+    for (int k = 0; k < m; ++k) nd += cls[k] == 2;
+    s_ndef = nd;
+  }
+  __syncthreads();
+  for (int rep = 0; rep < (s_ndef > 0 ? 2 : 0); ++rep) {
     cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
     for (int idx = threadIdx.x; idx < MB * MB; idx += PEXP_THREADS) {
       int a = idx % MB, k = idx / MB;

@@ -35,12 +35,98 @@ constexpr Grp kSolo{0, 1};
 // C = alpha*A*B + beta*C ; A: M x K (lda), B: K x N (ldb), C: M x N (ldc); C must not alias.
 // Tiles TM x TM (TM = 128 or 64) with K-steps of 16 staged in shared memory; 256 threads as a
 // 16 x 16 grid, each owning (TM/16)^2 outputs strided by 16 (conflict-free shared reads, 4 FMA
-// per shared load at TM = 128); the next K-step is prefetched into registers while the current
+// per shared load at TM = 128; the thread's row index runs fastest across a warp so the epilogue's
+// C reads/writes are coalesced); the next K-step is prefetched into registers while the current
 // one is consumed (hides the L2 latency of these L2-resident operands).
 // one shared staging buffer per kernel, shared by both tile instantiations
 __device__ inline double* gemm_smem() {
-  __shared__ double buf[2 * 16 * (128 + 1)];
+  __shared__ __align__(16) double buf[2 * 16 * (128 + 8)];
   return buf;
+}
+
+// fp64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row) B(4x8, col); per lane: A[lane/4][lane%4],
+// B[lane%4][lane/4], D[lane/4][2(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Same contract as cta_gemm_t, on the fp64 tensor cores: TM x TM CTA tiles, 8 warps as 4 (rows) x 2
+// (columns), warp tile (TM/4) x (TM/2) of m8n8 accumulators, K-steps of 16 staged in shared memory
+// (rows padded to TM + 8 doubles: the 4 k-rows of a fragment load fall in disjoint banks), the next
+// K-step prefetched into registers.
+template <int TM>
+__device__ inline void cta_gemm_dmma(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
+                                     int ldb, double beta, double* C, int ldc, Grp g) {
+  constexpr int LDS = TM + 8;
+  constexpr int WM = TM / 4, WN = TM / 2, MI = WM / 8, NI = WN / 8;
+  constexpr int LA = TM * 16 / 256;
+  double (*As)[LDS] = reinterpret_cast<double (*)[LDS]>(gemm_smem());
+  double (*Bs)[LDS] = reinterpret_cast<double (*)[LDS]>(gemm_smem() + 16 * LDS);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, wm = warp & 3, wn = warp >> 2;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int nti = (M + TM - 1) / TM, ntj = (N + TM - 1) / TM;
+  for (int tile = g.rank; tile < nti * ntj; tile += g.size) {
+    const int i0 = (tile % nti) * TM, j0 = (tile / nti) * TM;
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int b = 0; b < NI; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+    double pa[LA], pb[LA];
+    auto load = [&](int k0) {
+#pragma unroll
+      for (int q = 0; q < LA; ++q) {
+        int idx = t + q * 256;
+        int r = idx % TM, kk = idx / TM;        // A: rows fastest (coalesced)
+        int gi = i0 + r, gk = k0 + kk;
+        pa[q] = (gi < M && gk < K) ? A[gi + size_t(gk) * lda] : 0.0;
+        int kb = idx % 16, c = idx / 16;        // B: k fastest within a column
+        int gkb = k0 + kb, gj = j0 + c;
+        pb[q] = (gkb < K && gj < N) ? B[gkb + size_t(gj) * ldb] : 0.0;
+      }
+    };
+    load(0);
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < LA; ++q) {
+        int idx = t + q * 256;
+        As[idx / TM][idx % TM] = pa[q];
+        Bs[idx % 16][idx / 16] = pb[q];
+      }
+      __syncthreads();
+      if (k0 + 16 < K) load(k0 + 16);
+#pragma unroll
+      for (int kq = 0; kq < 4; ++kq) {
+        double af[MI], bf[NI];
+#pragma unroll
+        for (int a = 0; a < MI; ++a) af[a] = As[kq * 4 + fc][wm * WM + a * 8 + fr];
+#pragma unroll
+        for (int b = 0; b < NI; ++b) bf[b] = Bs[kq * 4 + fc][wn * WN + b * 8 + fr];
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int b = 0; b < NI; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gi = i0 + wm * WM + a * 8 + fr, gj = j0 + wn * WN + b * 8 + 2 * fc + h;
+          if (gi < M && gj < N) {
+            double* c = C + gi + size_t(gj) * ldc;
+            double v = alpha * acc[a][b][h];
+            if (beta != 0.0) v = fma(beta, *c, v);
+            *c = v;
+          }
+        }
+  }
+  grp_sync(g);
 }
 
 template <int TM>
@@ -88,9 +174,9 @@ __device__ inline void cta_gemm_t(int M, int N, int K, double alpha, const doubl
         for (int kk = 0; kk < 16; ++kk) {
           double av[R], bv[R];
 #pragma unroll
-          for (int a = 0; a < R; ++a) av[a] = As[kk][ty + 16 * a];
+          for (int a = 0; a < R; ++a) av[a] = As[kk][tx + 16 * a];
 #pragma unroll
-          for (int b = 0; b < R; ++b) bv[b] = Bs[kk][tx + 16 * b];
+          for (int b = 0; b < R; ++b) bv[b] = Bs[kk][ty + 16 * b];
 #pragma unroll
           for (int a = 0; a < R; ++a)
 #pragma unroll
@@ -101,7 +187,7 @@ __device__ inline void cta_gemm_t(int M, int N, int K, double alpha, const doubl
       for (int a = 0; a < R; ++a)
 #pragma unroll
         for (int b = 0; b < R; ++b) {
-          int gi = i0 + ty + 16 * a, gj = j0 + tx + 16 * b;
+          int gi = i0 + tx + 16 * a, gj = j0 + ty + 16 * b;  // consecutive threads: consecutive rows
           if (gi < M && gj < N) {
             double* c = C + gi + size_t(gj) * ldc;
             double v = alpha * acc[a][b];
@@ -114,8 +200,19 @@ __device__ inline void cta_gemm_t(int M, int N, int K, double alpha, const doubl
   grp_sync(g);
 }
 
+// 1: the fp64 tensor-core path (default); 0: SIMT FMA tiles (per translation unit; small.cu sets
+// its copy from the developer switch PEXP_NODMMA)
+static __device__ int g_gemm_dmma = 1;
+
 __device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
                                 int ldb, double beta, double* C, int ldc, Grp g = kSolo) {
+  if (g_gemm_dmma) {
+    if (M > 64 && N > 64)
+      cta_gemm_dmma<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
+    else
+      cta_gemm_dmma<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
+    return;
+  }
   if (M > 64 && N > 64)
     cta_gemm_t<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
   else

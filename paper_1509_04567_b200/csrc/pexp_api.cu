@@ -552,34 +552,48 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
   double* part = B->part;
   size_t part_cap = B->part_cap;
   PEXP_CUDA_TRY(cudaMemsetAsync(B->xcnt, 0, E * sizeof(int), st));
-  PEXP_CUDA_TRY(cudaMemsetAsync(S.U, 0, size_t(E) * s * n * sizeof(double), st));
   launch_fill_i32(st, S.off, E, 0);
-  double* U = S.U;   // current orthonormal basis (zero columns beyond off[e])
+  double* U = S.U;   // current orthonormal basis: columns [0, ko) valid (zero beyond off[e])
   double* Fr = S.R;  // free buffer
+  int ko = 0;        // max over evaluations of off[e] (host copy, read back after each selection)
+  std::vector<int> offh(E);
   for (int p = 0; p < npass; ++p) {
     const double* X = G;
-    if (p > 0) {
+    if (p > 0 && ko > 0) {
       // residual R = G - U (U^T G), explicit (pass p resolves what pass p-1 could not)
-      launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
+      launch_xty(st, E, n, U, gs_e, 0, ko, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, ko, 0, 0, false,
+                 nullptr, B->xcnt);
       PEXP_CUDA_TRY(cudaMemcpyAsync(Fr, G, size_t(E) * s * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      launch_combine(st, E, n, U, gs_e, 0, s, S.Cb, (long long)s * s, s, Fr, gs_e, 0, s, -1.0, 1.0, nullptr);
+      launch_combine(st, E, n, U, gs_e, 0, ko, S.Cb, (long long)s * s, ko, Fr, gs_e, 0, s, -1.0, 1.0, nullptr);
       X = Fr;
     }
     launch_xty(st, E, n, X, gs_e, 0, s, X, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
     launch_sym_eig_select(st, E, s, S.Gs, S.lam, S.Msel, S.off, S.sigma1, p, tau, theta, nullptr);
-    launch_combine(st, E, n, X, gs_e, 0, s, S.Msel, (long long)s * s, s, U, gs_e, 0, s, 1.0, 1.0, nullptr);
-    // CholQR2 of U (masked: zero columns stay zero); ping-pong U <-> Fr
+    PEXP_CUDA_TRY(cudaMemcpyAsync(offh.data(), S.off, E * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    int kn = 0;
+    for (int e = 0; e < E; ++e) kn = std::max(kn, offh[e]);
+    if (kn == 0) break;  // all-zero samples: nothing selected
+    // U[:, 0:ko] += X Msel[:, 0:ko];  U[:, ko:kn] = X Msel[:, ko:kn]
+    if (ko > 0) launch_combine(st, E, n, X, gs_e, 0, s, S.Msel, (long long)s * s, s, U, gs_e, 0, ko, 1.0, 1.0, nullptr);
+    if (kn > ko)
+      launch_combine(st, E, n, X, gs_e, 0, s, S.Msel + size_t(ko) * s, (long long)s * s, s, U, gs_e, ko, kn - ko, 1.0,
+                     0.0, nullptr);
+    ko = kn;
+    // CholQR2 of U[:, 0:ko] (masked: zero columns stay zero); ping-pong U <-> Fr
     for (int q = 0; q < 2; ++q) {
-      launch_xty(st, E, n, U, gs_e, 0, s, U, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false,
+      launch_xty(st, E, n, U, gs_e, 0, ko, U, gs_e, 0, ko, part, part_cap, S.Gs, (long long)ko * ko, ko, 0, 0, false,
                  nullptr, B->xcnt);
-      launch_block_chol(st, E, s, S.Gs, (long long)s * s, s, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0, 0,
+      launch_block_chol(st, E, ko, S.Gs, (long long)ko * ko, ko, nullptr, 0, 0, 0.0, S.Rinv, nullptr, 0, 0, nullptr, 0, 0,
                         nullptr, 0, nullptr, false);
-      launch_combine(st, E, n, U, gs_e, 0, s, S.Rinv, (long long)s * s, s, Fr, gs_e, 0, s, 1.0, 0.0, nullptr);
+      launch_combine(st, E, n, U, gs_e, 0, ko, S.Rinv, (long long)ko * ko, ko, Fr, gs_e, 0, ko, 1.0, 0.0, nullptr);
       std::swap(U, Fr);
     }
   }
-  // C = U^T G, one-sided Jacobi SVD, truncation
-  launch_xty(st, E, n, U, gs_e, 0, s, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
+  // C = U^T G (rows 0..ko-1 of the s x s matrix Cb), one-sided Jacobi SVD, truncation
+  if (ko > 0)
+    launch_xty(st, E, n, U, gs_e, 0, ko, G, gs_e, 0, s, part, part_cap, S.Cb, (long long)s * s, s, 0, 0, false, nullptr,
+               B->xcnt);
   launch_onesided_svd(st, E, s, S.Cb, S.off, tau, S.Qs, S.sig, S.Cs, S.me, nullptr);
   std::vector<int> mh(E);
   PEXP_CUDA_TRY(cudaMemcpyAsync(mh.data(), S.me, E * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -593,7 +607,10 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
   launch_build_final(st, E, s, mb, S.off, S.Qs, S.sig, S.Cs, S.me, S.Msel, S.Cfin, S.fill);
   // final block U_j (mb columns, padded with the next singular vectors / random columns),
   // CholQR2 -> S.U (stride s*n); the EBK copies each chunk's U_j into its basis block 0
-  launch_combine(st, E, n, U, gs_e, 0, s, S.Msel, (long long)s * mb, s, Fr, gs_e, 0, mb, 1.0, 0.0, nullptr);
+  if (ko > 0)
+    launch_combine(st, E, n, U, gs_e, 0, ko, S.Msel, (long long)s * mb, s, Fr, gs_e, 0, mb, 1.0, 0.0, nullptr);
+  else
+    PEXP_CUDA_TRY(cudaMemsetAsync(Fr, 0, size_t(E) * s * n * sizeof(double), st));
   launch_fill_random(st, E, n, mb, S.fill, Fr, gs_e, 12345u);
   for (int q = 0; q < 2; ++q) {
     double* X = q == 0 ? Fr : S.U;
@@ -686,7 +703,7 @@ static pexp_status guarded(pexp_ctx* c, F&& f) {
 // Homogeneous legs per group (one shared block Krylov space per group; <= 16, KSMALL limits)
 static int hom_group_width(int P) {
   static const int force = getenv("PEXP_MH") ? atoi(getenv("PEXP_MH")) : 0;  // developer override
-  const int w = force > 0 ? std::min(force, 16) : 16;
+  const int w = force > 0 ? std::min(force, 16) : 8;  // measured on C2: 8 legs per group beat 16 (48 vs 58 ms)
   return std::max(1, std::min(w, P - 1));
 }
 

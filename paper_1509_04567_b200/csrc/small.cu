@@ -1061,6 +1061,10 @@ void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double*
 }
 
 void small_init() {
+  if (getenv("PEXP_NODMMA")) {
+    const int zero = 0;
+    cudaMemcpyToSymbol(g_gemm_dmma, &zero, sizeof(int));
+  }
   cudaFuncSetAttribute(k_sym_eig_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_block_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_onesided_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
