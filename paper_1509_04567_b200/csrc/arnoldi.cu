@@ -42,6 +42,18 @@ __device__ inline void cl_sync(cg::cluster_group& cl, int cs) {
     __syncthreads();
 }
 
+// Cluster sum of per-CTA partials kept in GLOBAL memory: rank q's partial at part0 + q * stride.
+__device__ inline void cl_allreduce_g(cg::cluster_group& cl, int cs, const double* part0, long long stride,
+                                      double* out, int cnt) {
+  cl_sync(cl, cs);
+  for (int i = threadIdx.x; i < cnt; i += PEXP_THREADS) {
+    double s = 0.0;
+    for (int q = 0; q < cs; ++q) s += __ldcg(part0 + q * stride + i);
+    out[i] = s;
+  }
+  __syncthreads();
+}
+
 // out[i] = sum over the cluster's CTAs (rank order) of part[i], i < cnt.  part and out distinct.
 // One cluster barrier: a CTA may overwrite `part` only after the NEXT cluster barrier (all remote
 // reads of this reduction happen before their reader arrives there), so consecutive reductions
@@ -641,8 +653,16 @@ __global__ void __launch_bounds__(PEXP_THREADS, MB <= 8 ? 2 : 1) k_arnoldi_step(
   s.gpar = 0;
   const int cbuf = max(s.ldc * MB, PEXP_THREADS * SPAD);
   double* p = sm;
-  s.Hs = p; p += size_t(nv) * MB;
-  s.Pp = p; p += size_t(nv) * MB;
+  const long long hst = (long long)nv * MB;   // V^T W partial / sum size
+  double* Pp0 = nullptr;                      // rank-0 partial (global variant)
+  if (A.hs_glob) {                            // [e][rank][2][nv*MB] in global memory
+    s.Hs = A.hs_g + (size_t(e) * cs + cr) * 2 * hst;
+    s.Pp = s.Hs + hst;
+    Pp0 = A.hs_g + size_t(e) * cs * 2 * hst + hst;
+  } else {
+    s.Hs = p; p += hst;
+    s.Pp = p; p += hst;
+  }
   s.Cx = p; p += cbuf;
   s.Cy = p; p += cbuf;
   s.G = p; p += MB * MB;
@@ -671,7 +691,10 @@ __global__ void __launch_bounds__(PEXP_THREADS, MB <= 8 ? 2 : 1) k_arnoldi_step(
                    ldw, W0, s, wsmM, red);
   // ---- BCGS pass 1
   cta_vtw<MB>(n, ldw, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
-  cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
+  if (A.hs_glob)
+    cl_allreduce_g(cl, cs, Pp0, 2 * hst, s.Hs, nv * m);
+  else
+    cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
   if (cr == 0)
     for (int i = threadIdx.x; i < nv * m; i += PEXP_THREADS) {
       int a = i % nv, c = i / nv;
@@ -708,7 +731,10 @@ __global__ void __launch_bounds__(PEXP_THREADS, MB <= 8 ? 2 : 1) k_arnoldi_step(
   cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
   // ---- BCGS pass 2 + CholQR
   cta_vtw<MB>(n, ldw, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
-  cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
+  if (A.hs_glob)
+    cl_allreduce_g(cl, cs, Pp0, 2 * hst, s.Hs, nv * m);
+  else
+    cl_allreduce(cl, cs, s.Pp, s.Hs, nv * m);
   cta_update<MB>(n, ldw, cnt, V, nv, W, m, s.Hs);
   cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
   cta_chol_piv<MB>(m, s.G, nullptr, A.defl, 0.0, A.piv_tol, s, cls, perm, used, dead);
@@ -739,15 +765,29 @@ static size_t step_smem(int MB, int nv, int wrows) {
 
 static int mb_for(int m) { return m <= 8 ? 8 : (m <= 16 ? 16 : 32); }
 
-bool arnoldi_fused_ok(int m, int nv) {
+static int step_cluster(int E, int n);
+
+// The fused step is used when the CTA's rows of the new block fit shared memory (the V^T W
+// partials may live in global scratch).  Otherwise (very long columns, e.g. C5's 8192 rows per
+// CTA) the multi-kernel route streams V with full-grid launches, which measured 2x faster there.
+bool arnoldi_fused_ok(int m, int nv, int n, int E, bool have_global_scratch) {
   if (m > 32) return false;
-  return step_smem(mb_for(m), nv, 0) <= 200 * 1024;
+  const int MB = mb_for(m), per = step_rows(n, step_cluster(E, n));
+  if (step_smem(MB, nv, per) <= 200 * 1024) return true;
+  return have_global_scratch && step_smem(MB, 0, per) <= 200 * 1024;
+}
+
+// global scratch of the fused step for E evaluations (clusters of <= 8 CTAs, nv <= kcap)
+size_t arnoldi_scratch_doubles(int E, int kcap, int mcap) {
+  const int MB = mb_for(std::min(mcap, 32));
+  if (step_smem(MB, kcap, 0) <= 200 * 1024) return 0;  // every step fits shared memory
+  return size_t(E) * 8 * 2 * size_t(kcap) * MB;
 }
 
 // cluster size: enough CTAs for ~2 waves over the 148 SMs, >= 512 rows per CTA, portable max 8
 static int step_cluster(int E, int n) {
   static const int force = getenv("PEXP_ACL") ? atoi(getenv("PEXP_ACL")) : 0;  // developer override
-  if (force > 0) return force;
+  if (force > 0) return std::min(force, 8);
   int cs = 1;
   while (cs < 8 && long(E) * cs < 2 * 148 && n / (2 * cs) >= 512) cs *= 2;
   return cs;
@@ -782,8 +822,14 @@ void launch_arnoldi_step(cudaStream_t st, StepArgs a) {
   const int nv = (a.b + 1) * a.m;
   const int per = step_rows(a.n, a.cs);
   size_t smem = step_smem(MB, nv, per);
-  a.ws_smem = smem <= 200 * 1024 ? 1 : 0;  // the CTA's rows of the new block stay on chip
-  if (!a.ws_smem) smem = step_smem(MB, nv, 0);
+  a.ws_smem = 1;  // the CTA's rows of the new block stay on chip
+  a.hs_glob = 0;
+  if (smem > 200 * 1024) {  // V^T W partials and sums to global memory (large Krylov dimensions)
+    if (!a.hs_g) fail(1, "fused Arnoldi step: no global scratch for a large basis");
+    a.hs_glob = 1;
+    smem = step_smem(MB, 0, per);
+  }
+  if (smem > 200 * 1024) fail(1, "fused Arnoldi step: block rows exceed shared memory");
   ProfScope ps(PC_ARNOLDI, st, double(a.E) * a.n * 8.0 * (4.0 * nv + 12.0 * a.m),
                double(a.E) * a.n * (8.0 * nv * a.m + 10.0 * a.m * a.m));
   if (MB == 8)

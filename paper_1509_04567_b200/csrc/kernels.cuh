@@ -87,10 +87,13 @@ struct StepArgs {
   int rc;
   int cs;                         // CTAs per evaluation (thread-block cluster)
   int ws_smem;                    // 1: the CTA's rows of the new block live in shared memory
+  double* hs_g;                   // global scratch for the V^T W partials/sums when they exceed shared memory
+  int hs_glob;                    // 1: use hs_g (2 * nv * MB doubles per CTA)
 };
 
 // arnoldi.cu
-bool arnoldi_fused_ok(int m, int nv);
+bool arnoldi_fused_ok(int m, int nv, int n, int E, bool have_global_scratch);
+size_t arnoldi_scratch_doubles(int E, int kcap, int mcap);
 void launch_arnoldi_step(cudaStream_t st, StepArgs a);
 
 // tridiag.cu

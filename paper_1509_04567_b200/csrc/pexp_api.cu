@@ -87,6 +87,7 @@ struct EbkBufs {
   int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc;
   double* part;
   size_t part_cap;
+  double* stepws = nullptr;  // fused Arnoldi step: global V^T W partials (large bases)
   double* work;
   int* iwork;
   int nslots, Nmax;
@@ -154,6 +155,10 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   B.part_cap = std::max(part_need(Ec, n, std::max(kcap, s), forced ? std::max(mcap, s) : mcap),
                         forced ? part_need(E, n, s, s) : size_t(0));
   B.part = ar.take<double>(B.part_cap);
+  {
+    const size_t sw = arnoldi_scratch_doubles(Ec, kcap, mcap);
+    B.stepws = sw ? ar.take<double>(sw) : nullptr;
+  }
   B.Nmax = ktot + (forced ? 4 * mcap : 0);
   B.work_slot = 10LL * B.Nmax * B.Nmax;
   B.iwork_slot = B.Nmax;
@@ -433,12 +438,13 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     }
     const int b = steps, nv = (b + 1) * m;
     const long long ws_e = B.vs_e;
-    if (!nofuse && arnoldi_fused_ok(m, nv)) {  // one cluster per evaluation does the whole step
+    if (!nofuse && arnoldi_fused_ok(m, nv, n, E, B.stepws != nullptr)) {  // one cluster per evaluation: whole step
       StepArgs sa{};
       sa.E = E; sa.n = n; sa.m = m; sa.b = b; sa.kcap = kcap; sa.periodic = F.periodic;
       sa.V = B.V; sa.vs_e = B.vs_e; sa.H = B.H; sa.hs_e = B.hs_e; sa.live = B.live; sa.fidx = B.fidx;
       sa.fl = F.l; sa.fdinv = F.dinv; sa.fsup = F.sup; sa.fz = F.z; sa.fw = F.w;
       sa.W0 = B.Wt; sa.w0s_e = (long long)m * n; sa.active = B.active; sa.defl = defl;
+      sa.hs_g = B.stepws;
       launch_arnoldi_step(st, sa);
     } else {
     // W = (I - gamma A)^{-1} V_b  -> columns [nv, nv+m)

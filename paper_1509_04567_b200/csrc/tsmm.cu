@@ -8,12 +8,21 @@
 //              row so that Out may alias X (in-place right-multiplication, ny <= 32).
 // Loads are coalesced along rows (each warp reads 32 consecutive rows of a column);
 // per-thread 4x4 register tiles accumulate the small products from shared memory.
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace pexp {
 
 constexpr int TR = 16;  // rows per shared-memory stage
+
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) B(4x8, col); per lane A[lane/4][lane%4],
+// B[lane%4][lane/4], D[lane/4][2(lane%4) + {0,1}]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 constexpr int RA = 4, RB = 4;
 
 template <int NT>
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(PEXP_THREADS)
 k_combine(int n, const double* X, long long xs_e, int x0, int nx, const double* M, long long ms_e,
           int ldm, double* O, long long os_e, int o0, int ny, double alpha, double beta,
           const int* active, const int* nxe) {
-  extern __shared__ double Ms[];  // [nx][NBT]
+  extern __shared__ __align__(16) double Ms[];  // [nx][NBT]
   const int e = blockIdx.y;
   if (active && !active[e]) return;
   const double* Me = M + e * ms_e;
@@ -299,39 +308,125 @@ k_combine(int n, const double* X, long long xs_e, int x0, int nx, const double* 
     Ms[idx] = b < ny ? Me[a + size_t(b) * ldm] : 0.0;
   }
   __syncthreads();
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  // two rows per thread (r, r + 256): every shared-memory value feeds two FMAs, read as double2
+  const int row = blockIdx.x * (2 * PEXP_THREADS) + threadIdx.x;
   if (row >= n) return;
+  const bool two = row + PEXP_THREADS < n;
   const double* Xe = X + e * xs_e + size_t(x0) * n + row;
   const int nxl = nxe ? min(nx, nxe[e]) : nx;
-  double acc[NBT];
+  double acc0[NBT], acc1[NBT];
 #pragma unroll
-  for (int b = 0; b < NBT; ++b) acc[b] = 0.0;
+  for (int b = 0; b < NBT; ++b) { acc0[b] = 0.0; acc1[b] = 0.0; }
   int a = 0;
-  for (; a + 3 < nxl; a += 4) {  // 4 independent column loads in flight
-    double x0v = Xe[size_t(a) * n], x1v = Xe[size_t(a + 1) * n], x2v = Xe[size_t(a + 2) * n],
-           x3v = Xe[size_t(a + 3) * n];
-    const double* mr = Ms + a * NBT;
+  for (; a + 3 < nxl; a += 4) {  // 4 columns x 2 rows of independent loads in flight
+    double x0v[4], x1v[4];
 #pragma unroll
-    for (int b = 0; b < NBT; ++b) {
-      acc[b] = fma(x0v, mr[b], acc[b]);
-      acc[b] = fma(x1v, mr[NBT + b], acc[b]);
-      acc[b] = fma(x2v, mr[2 * NBT + b], acc[b]);
-      acc[b] = fma(x3v, mr[3 * NBT + b], acc[b]);
+    for (int u = 0; u < 4; ++u) {
+      x0v[u] = __ldcg(Xe + size_t(a + u) * n);
+      x1v[u] = two ? __ldcg(Xe + size_t(a + u) * n + PEXP_THREADS) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2* mr = reinterpret_cast<const double2*>(Ms + (a + u) * NBT);
+#pragma unroll
+      for (int b = 0; b < NBT / 2; ++b) {
+        const double2 mv = mr[b];
+        acc0[2 * b] = fma(x0v[u], mv.x, acc0[2 * b]);
+        acc0[2 * b + 1] = fma(x0v[u], mv.y, acc0[2 * b + 1]);
+        acc1[2 * b] = fma(x1v[u], mv.x, acc1[2 * b]);
+        acc1[2 * b + 1] = fma(x1v[u], mv.y, acc1[2 * b + 1]);
+      }
     }
   }
   for (; a < nxl; ++a) {
-    double xv = Xe[size_t(a) * n];
+    const double xv = Xe[size_t(a) * n], xw = two ? Xe[size_t(a) * n + PEXP_THREADS] : 0.0;
     const double* mr = Ms + a * NBT;
 #pragma unroll
-    for (int b = 0; b < NBT; ++b) acc[b] = fma(xv, mr[b], acc[b]);
+    for (int b = 0; b < NBT; ++b) {
+      acc0[b] = fma(xv, mr[b], acc0[b]);
+      acc1[b] = fma(xw, mr[b], acc1[b]);
+    }
   }
   double* Oe = O + e * os_e + size_t(o0) * n + row;
 #pragma unroll
   for (int b = 0; b < NBT; ++b)
     if (b < ny) {
-      double v = alpha * acc[b];
+      double v = alpha * acc0[b];
       if (beta != 0.0) v = fma(beta, Oe[size_t(b) * n], v);
       Oe[size_t(b) * n] = v;
+      if (two) {
+        double w = alpha * acc1[b];
+        if (beta != 0.0) w = fma(beta, Oe[size_t(b) * n + PEXP_THREADS], w);
+        Oe[size_t(b) * n + PEXP_THREADS] = w;
+      }
+    }
+}
+
+// Tall-skinny X^T Y on the fp64 tensor cores for the large projections (nx >= 32, 8 < ny <= 32):
+// grid (row chunks, 64-column blocks of X, E).  Per 16-row step the CTA stages X (16 x 64) and
+// Y (16 x NYT) in shared memory (next step prefetched into registers); warp w owns the m8 tile w
+// of the 64 X columns and all NYT/8 n8 tiles (DMMA m8n8k4).  Partials per chunk, reduced by k_reduce.
+template <int NYT>
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_xty_mma(int n, int rch, const double* X, long long xs_e, int x0, int nx, const double* Y, long long ys_e, int y0,
+          int ny, double* part, const int* active) {
+  constexpr int XC = 64, LDX = XC + 8, LDY = NYT + 8, NJ = NYT / 8;
+  constexpr int LX = 16 * XC / PEXP_THREADS, LY = (16 * NYT + PEXP_THREADS - 1) / PEXP_THREADS;
+  __shared__ __align__(16) double Xs[16][LDX];
+  __shared__ __align__(16) double Ys[16][LDY];
+  const int ch = blockIdx.x, cb = blockIdx.y, e = blockIdx.z, nch = gridDim.x;
+  if (active && !active[e]) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, fr = lane >> 2, fc = lane & 3;
+  const int a0 = cb * XC;
+  const double* Xe = X + e * xs_e + size_t(x0 + a0) * n;
+  const double* Ye = Y + e * ys_e + size_t(y0) * n;
+  const int r0 = ch * rch, r1 = min(n, r0 + rch);
+  double acc[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) { acc[j][0] = 0.0; acc[j][1] = 0.0; }
+  double px[LX], py[LY];
+  auto fetch = [&](int rb) {
+#pragma unroll
+    for (int q = 0; q < LX; ++q) {
+      const int idx = t + q * PEXP_THREADS, c = idx / 16, k = idx % 16, row = rb + k;
+      px[q] = (a0 + c < nx && row < r1) ? __ldcg(Xe + size_t(c) * n + row) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < LY; ++q) {
+      const int idx = t + q * PEXP_THREADS, c = idx / 16, k = idx % 16, row = rb + k;
+      py[q] = (idx < 16 * NYT && c < ny && row < r1) ? __ldcg(Ye + size_t(c) * n + row) : 0.0;
+    }
+  };
+  if (r0 < r1) fetch(r0);
+  for (int rb = r0; rb < r1; rb += 16) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < LX; ++q) {
+      const int idx = t + q * PEXP_THREADS;
+      Xs[idx % 16][idx / 16] = px[q];
+    }
+#pragma unroll
+    for (int q = 0; q < LY; ++q) {
+      const int idx = t + q * PEXP_THREADS;
+      if (idx < 16 * NYT) Ys[idx % 16][idx / 16] = py[q];
+    }
+    __syncthreads();
+    if (rb + 16 < r1) fetch(rb + 16);
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      const double af = Xs[kq * 4 + fc][warp * 8 + fr];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) dmma884(acc[j][0], acc[j][1], af, Ys[kq * 4 + fc][j * 8 + fr]);
+    }
+  }
+  double* P = part + (size_t(e) * nch + ch) * size_t(nx) * ny;
+  const int a = a0 + warp * 8 + fr;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int b = j * 8 + 2 * fc + h;
+      if (a < nx && b < ny) P[a + size_t(b) * nx] = acc[j][h];
     }
 }
 
@@ -362,6 +457,26 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
                 const int* active, int* cnt) {
   if (E == 0 || nx == 0 || ny == 0) return;
   RedArgs ra{D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, cnt};
+  static const bool nomma = getenv("PEXP_NOXTYMMA") != nullptr;  // developer switch
+  if (!nomma && ny > 8 && ny <= 32 && nx >= 32) {
+    const int rch = xty_chunks(n, E * cdiv(nx, 64));
+    const int nch = cdiv(n, rch);
+    if (size_t(E) * nch * nx * ny > part_cap) fail(2, "xty partial buffer too small");
+    const bool same = (X == Y && xs_e == ys_e && y0 >= x0 && y0 + ny <= x0 + nx);
+    ProfScope ps(PC_XTY, st, double(E) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * E * double(n) * nx * ny);
+    dim3 grid(nch, cdiv(nx, 64), E);
+    if (ny <= 16)
+      k_xty_mma<16><<<grid, PEXP_THREADS, 0, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+    else
+      k_xty_mma<32><<<grid, PEXP_THREADS, 0, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+    dim3 g2(std::min(cdiv(nx * ny, PEXP_THREADS), 64), E);
+    k_reduce<<<g2, PEXP_THREADS, 0, st>>>(nx, ny, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, active);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+    return;
+  }
   if (ny <= 32) {
     int rsub, rch, nch;
     xty_tall_plan(n, E, nx, ny, rsub, rch, nch);
@@ -433,7 +548,7 @@ void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs
     const int nbt = nb <= 4 ? 4 : nb <= 8 ? 8 : nb <= 16 ? 16 : 32;
     size_t smem = size_t(std::max(nx, 1)) * nbt * sizeof(double);
     ProfScope ps(PC_COMBINE, st, double(E) * n * 8.0 * (nx + nb * (beta != 0.0 ? 2 : 1)), 2.0 * E * double(n) * nx * nb);
-    dim3 grid(cdiv(n, PEXP_THREADS), E);
+    dim3 grid(cdiv(n, 2 * PEXP_THREADS), E);
     const double* Mb = M + size_t(b0) * ldm;
     if (nbt == 4)
       k_combine<4><<<grid, PEXP_THREADS, smem, st>>>(n, X, xs_e, x0, nx, Mb, ms_e, ldm, O, os_e, o0 + b0, nb, alpha, beta, active, nxe);
