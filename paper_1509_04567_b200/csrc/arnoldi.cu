@@ -781,15 +781,17 @@ bool arnoldi_fused_ok(int m, int nv, int n, int E, bool have_global_scratch) {
 size_t arnoldi_scratch_doubles(int E, int kcap, int mcap) {
   const int MB = mb_for(std::min(mcap, 32));
   if (step_smem(MB, kcap, 0) <= 200 * 1024) return 0;  // every step fits shared memory
-  return size_t(E) * 8 * 2 * size_t(kcap) * MB;
+  return size_t(E) * 16 * 2 * size_t(kcap) * MB;
 }
 
 // cluster size: enough CTAs for ~2 waves over the 148 SMs, >= 512 rows per CTA, portable max 8
 static int step_cluster(int E, int n) {
   static const int force = getenv("PEXP_ACL") ? atoi(getenv("PEXP_ACL")) : 0;  // developer override
-  if (force > 0) return std::min(force, 8);
+  if (force > 0) return std::min(force, 16);
   int cs = 1;
   while (cs < 8 && long(E) * cs < 2 * 148 && n / (2 * cs) >= 512) cs *= 2;
+  // very small batches (e.g. 8 groups of homogeneous legs): a non-portable 16-CTA cluster
+  if (cs == 8 && E * 16 <= 148 && n / 16 >= 256) cs = 16;
   return cs;
 }
 

@@ -206,14 +206,16 @@ static __device__ int g_gemm_dmma = 1;
 
 __device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
                                 int ldb, double beta, double* C, int ldc, Grp g = kSolo) {
+  // 128 x 128 tiles unless that leaves CTAs of the group without a tile
+  const bool big = M > 64 && N > 64 && ((M + 127) / 128) * ((N + 127) / 128) >= g.size;
   if (g_gemm_dmma) {
-    if (M > 64 && N > 64)
+    if (big)
       cta_gemm_dmma<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
     else
       cta_gemm_dmma<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
     return;
   }
-  if (M > 64 && N > 64)
+  if (big)
     cta_gemm_t<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
   else
     cta_gemm_t<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);

@@ -58,8 +58,18 @@ __device__ inline void gbar(unsigned* cnt, unsigned* gen, unsigned nb) {
 }
 
 // Sum over CTAs of part[c*pw + j] for j < nval, in a fixed order; result to out[j] (smem).
-// One warp per value, lanes stride over the CTAs, then a warp tree.
+// Few CTAs (<= 32): one thread per value sums the CTAs in order (independent loads in flight);
+// many CTAs: one warp per value, lanes stride over the CTAs, then a warp tree.
 __device__ inline void grid_reduce(const double* part, int pw, int ncta, int j0, int nval, double* out) {
+  if (ncta <= 32) {
+    for (int j = threadIdx.x; j < nval; j += NT) {
+      double a = 0.0;
+      for (int c = 0; c < ncta; ++c) a += __ldcg(part + size_t(c) * pw + j0 + j);
+      out[j] = a;
+    }
+    __syncthreads();
+    return;
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int j = w; j < nval; j += NT / 32) {
     double a = 0.0;
