@@ -39,8 +39,13 @@ constexpr Grp kSolo{0, 1};
 // C reads/writes are coalesced); the next K-step is prefetched into registers while the current
 // one is consumed (hides the L2 latency of these L2-resident operands).
 // one shared staging buffer per kernel, shared by both tile instantiations
+// PEXP_GEMM_TM: largest CTA tile of the dense routines (64 keeps the projected-problem kernels at
+// <= 128 registers and ~95 KB of shared memory, i.e. two CTAs per SM)
+#ifndef PEXP_GEMM_TM
+#define PEXP_GEMM_TM 64
+#endif
 __device__ inline double* gemm_smem() {
-  __shared__ __align__(16) double buf[2 * 16 * (128 + 8)];
+  __shared__ __align__(16) double buf[2 * 16 * (PEXP_GEMM_TM + 8)];
   return buf;
 }
 
@@ -207,16 +212,16 @@ static __device__ int g_gemm_dmma = 1;
 __device__ inline void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, const double* B,
                                 int ldb, double beta, double* C, int ldc, Grp g = kSolo) {
   // 128 x 128 tiles unless that leaves CTAs of the group without a tile
-  const bool big = M > 64 && N > 64 && ((M + 127) / 128) * ((N + 127) / 128) >= g.size;
+  const bool big = PEXP_GEMM_TM >= 128 && M > 64 && N > 64 && ((M + 127) / 128) * ((N + 127) / 128) >= g.size;
   if (g_gemm_dmma) {
     if (big)
-      cta_gemm_dmma<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
+      cta_gemm_dmma<PEXP_GEMM_TM>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
     else
       cta_gemm_dmma<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
     return;
   }
   if (big)
-    cta_gemm_t<128>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
+    cta_gemm_t<PEXP_GEMM_TM>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
   else
     cta_gemm_t<64>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, g);
 }

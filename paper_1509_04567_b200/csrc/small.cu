@@ -24,8 +24,15 @@ namespace cg = cooperative_groups;
 // k_small_problem dynamic shared memory: replicated state 2*KSMALL_MAX, row partials CH_PSUM,
 // own rows KSMALL_MAX, residual ring 2*MAXS, then the CTA's slice of F (FS_CAP doubles)
 constexpr int CH_PSUM = KSMALL_MAX + 32;
+#if PEXP_GEMM_TM >= 128
 constexpr size_t SP_DYN = 180 * 1024;
 constexpr size_t HOM_DYN = 160 * 1024;
+constexpr int SMALL_MINB = 1;
+#else
+constexpr size_t SP_DYN = 72 * 1024;   // two CTAs per SM (with ~23 KB static shared memory)
+constexpr size_t HOM_DYN = 72 * 1024;
+constexpr int SMALL_MINB = 2;
+#endif
 constexpr size_t HOM_FS_CAP = HOM_DYN / 8 - 2 * 256;
 constexpr size_t FS_CAP = SP_DYN / 8 - (2 * KSMALL_MAX + CH_PSUM + KSMALL_MAX + 2 * MAXS);
 double g_piv_tol = getenv("PEXP_PIVTOL") ? atof(getenv("PEXP_PIVTOL")) : 1e-14;  // developer override
@@ -36,7 +43,8 @@ static int cluster_size_for(int E) {
   static const int force = getenv("PEXP_CLUSTER") ? atoi(getenv("PEXP_CLUSTER")) : 0;  // developer override
   if (force > 0) return force;
   int cs = 1;
-  while (cs < 8 && E * cs * 2 <= 148) cs *= 2;
+  while (cs < 8 && E * cs * 2 <= 148 * SMALL_MINB) cs *= 2;
+  // (16-CTA clusters measured slower here: E=8, N=208 expm 1.80 ms vs 1.15 ms with 8)
   return cs;
 }
 
@@ -550,7 +558,7 @@ __global__ void k_spline(int s, int mmax, const double* Kinv, const double* Cfin
 // is integrated exactly over the s-1 cubic pieces with ONE Pade-13 expm of the augmented
 // matrix (size D + Kp + 4m).  The residual is the current cycle's (it is the residual of the
 // whole accumulated approximation).
-__global__ void __launch_bounds__(PEXP_THREADS) k_small_problem(SPArgs a) {
+__global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPArgs a) {
   __shared__ int idx[KSMALL_MAX];
   __shared__ int tidx[MAXS], lpos[MAXS];
   __shared__ int s_K, s_mt, s_ml;
@@ -815,7 +823,7 @@ void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double
 // Zsum[e][i] (K-vectors), so that Yh_e[i] = V_e Zsum[e][i] is the group's share of
 // sum_{j<i} exp((T_{i+1} - T_{j+1}) A) v_j(T_{j+1}) (Eq.(superposition)).
 // Residual per leg and step (SaI form) against crit_c; convergence when every leg passes.
-__global__ void __launch_bounds__(PEXP_THREADS) k_small_hom(SPArgs a) {
+__global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_hom(SPArgs a) {
   extern __shared__ double hsm[];  // HOM_DYN bytes: LU scratch; later residual ring + F slice
   __shared__ int idx[KSMALL_MAX];
   __shared__ int tidx[MAXS], lpos[MAXS];
@@ -976,7 +984,7 @@ void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
 }
 
 // ---------------------------------------------------------------- batched expm (stage API)
-__global__ void __launch_bounds__(PEXP_THREADS)
+__global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB)
 k_expm_batched(int E, int N, const double* A, double* X, double* work, long long work_slot, int* iwork) {
   __shared__ double red[32];
   extern __shared__ double xsm[];  // HOM_DYN bytes: LU panel / permutation scratch
@@ -1061,6 +1069,9 @@ void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double*
 }
 
 void small_init() {
+  cudaFuncSetAttribute(k_small_problem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_small_hom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_expm_batched, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (getenv("PEXP_NODMMA")) {
     const int zero = 0;
     cudaMemcpyToSymbol(g_gemm_dmma, &zero, sizeof(int));
