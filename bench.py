@@ -304,6 +304,13 @@ def main():
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    # traffic: DRAM bytes per launch of this class from a committed `ncu --set full` capture
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        tj = json.load(open(tf)).get(dom)
+        if tj and tj.get("workload") == args.config:
+            roof["traffic"] = tj["dram_bytes_per_launch"]
+            roof["traffic_source"] = tj["source"]
     roof["share_of_step"] = d["ms"] / max(1e-9, sum(times))
     roof["launches_per_step"] = d["launches"] / args.steps
     classes = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,

@@ -626,10 +626,20 @@ __device__ inline void cl_sai_solve(cg::cluster_group& cl, int cs, int cr, int l
     for (int c = 0; c < CB; ++c) { cin[c] = c < nc ? carry_s[c0 + c] : 0.0; fc[c] = c < nc ? f_s[c0 + c] : 0.0; }
     seg_bwd_multi(g0, cnt, di, sup, periodic ? fz : nullptr, fc, W + size_t(c0) * ldw, ldw, W0 + size_t(c0) * ld,
                   ld, nc, cin, wsmM, nrm);
-    for (int c = 0; c < nc; ++c) {
-      const double nr = block_sum(nrm[c], red);
-      if (threadIdx.x == 0) xn[c0 + c] = nr;
+    // the nc column norms in one block reduction (warp shuffles, then warp partials in wsmM)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) nrm[c] = warp_sum(nrm[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < CB; ++c) wsmM[w * CB + c] = nrm[c];
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      double v = 0.0;
+      for (int k = 0; k < PEXP_THREADS / 32; ++k) v += wsmM[k * CB + threadIdx.x];
+      xn[c0 + threadIdx.x] = v;
     }
+    __syncthreads();
   }
   cl_allreduce(cl, cs, xn, s.n0, m);
 }
