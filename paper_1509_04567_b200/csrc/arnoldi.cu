@@ -238,10 +238,12 @@ __device__ inline void cta_apply(int ld, int rows, double* W, int m, const doubl
 // classes cls (1 accepted, 2 deferred, 0 dead), optional re-ordered norm0 (see k_block_chol).
 // m <= 32: the whole factorisation runs in warp 0 (lane i owns row i; warp argmax for the pivot,
 // __syncwarp between phases, no CTA barriers); one __syncthreads publishes the results.
+// Returns the smallest accepted scaled pivot (squared), +inf if none was accepted.
 template <int MB>
-__device__ inline void cta_chol_piv(int m, const double* G, const double* norm0, double defl, double dtol,
-                                    double piv_tol, SmemT& s, int* cls, int* perm, int* used, int* dead) {
+__device__ inline double cta_chol_piv(int m, const double* G, const double* norm0, double defl, double dtol,
+                                      double piv_tol, SmemT& s, int* cls, int* perm, int* used, int* dead) {
   constexpr int LD = MB + 1;
+  __shared__ double s_pmin;
   if (threadIdx.x < 32) {
     const int i = threadIdx.x;
     const unsigned full = 0xffffffffu;
@@ -262,6 +264,7 @@ __device__ inline void cta_chol_piv(int m, const double* G, const double* norm0,
     __syncwarp();
     const double best0 = dtol > 0.0 ? dtol : piv_tol;
     int np = 0;
+    double pmin = INFINITY;
     for (int t = 0; t < m; ++t) {
       // argmax of the remaining scaled pivots (strictly above best0; ties -> lowest index)
       double cv = -1.0;
@@ -273,6 +276,7 @@ __device__ inline void cta_chol_piv(int m, const double* G, const double* norm0,
         if (ov > cv || (ov == cv && oi < ci)) { cv = ov; ci = oi; }
       }
       if (cv < 0.0) break;  // uniform over the warp
+      pmin = fmin(pmin, cv);
       const int jb = ci;
       const double pv = sqrt(cv);
       double xw = 0.0;
@@ -325,8 +329,10 @@ __device__ inline void cta_chol_piv(int m, const double* G, const double* norm0,
       cls[i] = i < np ? 1 : (i < np + nd ? 2 : 0);
       if (norm0) s.n0p[i] = norm0[perm[i]];
     }
+    if (i == 0) s_pmin = pmin;
   }
   __syncthreads();
+  return s_pmin;
 }
 
 // ---------------------------------------------------------------- cluster-split SaI solve
@@ -713,7 +719,7 @@ __global__ void __launch_bounds__(PEXP_THREADS, MB <= 8 ? 2 : 1) k_arnoldi_step(
   cta_update<MB>(n, ldw, cnt, V, nv, W, m, s.Hs);
   // ---- in-block QR, stage A (accept kappa <= 1e4, defer the rest, drop below defl*|W0|)
   cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
-  cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 1e-8, A.piv_tol, s, cls, perm, used, dead);
+  const double pminA = cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 1e-8, A.piv_tol, s, cls, perm, used, dead);
   cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
   // ---- stage B: explicit CGS2 of deferred columns against accepted ones (skipped when the
   // stage-A factorisation deferred nothing; cls is identical in every CTA of the cluster)
@@ -733,12 +739,24 @@ __global__ void __launch_bounds__(PEXP_THREADS, MB <= 8 ? 2 : 1) k_arnoldi_step(
     __syncthreads();
     cta_apply<MB>(ldw, cnt, W, m, s.Mc, 1.0);
   }
-  // ---- stage C: final pivoted CholQR with deflation relative to |W0|
-  cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
-  for (int k = threadIdx.x; k < m; k += PEXP_THREADS) s.n0[k] = s.n0p[k];
+  // ---- stage C: final pivoted CholQR with deflation relative to |W0|.  Skipped when stage A
+  // accepted every column with scaled pivots >= 1e-2 (scaled Gram condition <= ~1e2, so one
+  // CholQR left the block orthonormal to ~1e-12 and BCGS pass 2 + its CholQR finish the job);
+  // the decision uses cluster-identical data.
+  __shared__ int s_nacc;
+  if (threadIdx.x == 0) {
+    int na = 0;
+    for (int k = 0; k < m; ++k) na += cls[k] == 1;
+    s_nacc = na;
+  }
   __syncthreads();
-  cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 0.0, A.piv_tol, s, cls, perm, used, dead);
-  cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
+  if (!(s_ndef == 0 && s_nacc == m && pminA >= 1e-2)) {
+    cl_gram<MB>(cl, cs, ldw, ldw, cnt, W, W, m, s);
+    for (int k = threadIdx.x; k < m; k += PEXP_THREADS) s.n0[k] = s.n0p[k];
+    __syncthreads();
+    cta_chol_piv<MB>(m, s.G, s.n0, A.defl, 0.0, A.piv_tol, s, cls, perm, used, dead);
+    cta_apply<MB>(ldw, cnt, W, m, s.Rinv, 0.0);
+  }
   // ---- BCGS pass 2 + CholQR
   cta_vtw<MB>(n, ldw, cnt, V, nv, W, m, s.Pp, s.Cx, s.ldc);
   if (A.hs_glob)

@@ -254,13 +254,19 @@ __device__ inline void cta_identity(int N, double* Y, int ldy, double d = 1.0, G
   grp_sync(g);
 }
 
-// max column abs-sum
+// max column abs-sum: one warp per column, lanes over rows (coalesced, 4 loads in flight per lane)
 __device__ inline double cta_norm1(int N, const double* A, int lda, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double mx = 0.0;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < N; ++i) s += fabs(A[i + size_t(j) * lda]);
-    mx = fmax(mx, s);
+  for (int j = w; j < N; j += nw) {
+    const double* col = A + size_t(j) * lda;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = lane;
+    for (; i + 96 < N; i += 128) {
+      s0 += fabs(col[i]); s1 += fabs(col[i + 32]); s2 += fabs(col[i + 64]); s3 += fabs(col[i + 96]);
+    }
+    for (; i < N; i += 32) s0 += fabs(col[i]);
+    mx = fmax(mx, warp_sum((s0 + s1) + (s2 + s3)));
   }
   return block_max(mx, red);
 }
@@ -381,13 +387,48 @@ __device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red, 
       }
     }
     grp_sync(g);
-    // the panel's interchanges on all other columns (one thread per column, group-split)
-    for (int j = threadIdx.x + g.rank * blockDim.x; j < N; j += blockDim.x * g.size) {
-      if (j >= k0 && j < k0 + kb) continue;
-      double* col = A + size_t(j) * lda;
-      for (int k = k0; k < k0 + kb; ++k) {
-        const int ip = piv[k];
-        if (ip != k) { const double t = col[k]; col[k] = col[ip]; col[ip] = t; }
+    // the panel's interchanges on all other columns, as one gather per column: the touched rows
+    // (panel rows and their swap partners, <= 2*NBL) and their source rows are composed once in
+    // shared memory, then (column, touched row) pairs are loaded in parallel through psm and stored
+    {
+      __shared__ int s_np, s_pos[64], s_src[64];
+      if (threadIdx.x == 0) {
+        int np = 0;
+        for (int k = k0; k < k0 + kb; ++k) {
+          const int cand[2] = {k, piv[k]};
+          for (int q = 0; q < 2; ++q) {
+            bool f = false;
+            for (int t = 0; t < np; ++t) f |= s_pos[t] == cand[q];
+            if (!f) { s_pos[np] = cand[q]; s_src[np] = cand[q]; ++np; }
+          }
+        }
+        for (int k = k0; k < k0 + kb; ++k) {  // apply the swaps to the row labels
+          const int ip = piv[k];
+          if (ip == k) continue;
+          int a = 0, b = 0;
+          for (int t = 0; t < np; ++t) { if (s_pos[t] == k) a = t; if (s_pos[t] == ip) b = t; }
+          const int tmp = s_src[a]; s_src[a] = s_src[b]; s_src[b] = tmp;
+        }
+        s_np = np;
+      }
+      __syncthreads();
+      const int np = s_np;
+      // columns of this CTA: outside the panel, group-split
+      const int ncol = N - kb, per = (ncol + g.size - 1) / g.size;
+      const int j0 = g.rank * per, j1 = min(ncol, j0 + per);
+      const int cb = max(1, psm_cap / max(np, 1));
+      for (int jc = j0; jc < j1; jc += cb) {
+        const int nc = min(cb, j1 - jc);
+        for (int t = threadIdx.x; t < nc * np; t += blockDim.x) {
+          const int q = t % np, jj = jc + t / np, j = jj < k0 ? jj : jj + kb;
+          psm[t] = A[s_src[q] + size_t(j) * lda];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * np; t += blockDim.x) {
+          const int q = t % np, jj = jc + t / np, j = jj < k0 ? jj : jj + kb;
+          A[s_pos[q] + size_t(j) * lda] = psm[t];
+        }
+        __syncthreads();
       }
     }
     grp_sync(g);
