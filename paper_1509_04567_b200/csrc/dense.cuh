@@ -387,48 +387,14 @@ __device__ inline bool cta_lu(int N, double* A, int lda, int* piv, double* red, 
       }
     }
     grp_sync(g);
-    // the panel's interchanges on all other columns, as one gather per column: the touched rows
-    // (panel rows and their swap partners, <= 2*NBL) and their source rows are composed once in
-    // shared memory, then (column, touched row) pairs are loaded in parallel through psm and stored
-    {
-      __shared__ int s_np, s_pos[64], s_src[64];
-      if (threadIdx.x == 0) {
-        int np = 0;
-        for (int k = k0; k < k0 + kb; ++k) {
-          const int cand[2] = {k, piv[k]};
-          for (int q = 0; q < 2; ++q) {
-            bool f = false;
-            for (int t = 0; t < np; ++t) f |= s_pos[t] == cand[q];
-            if (!f) { s_pos[np] = cand[q]; s_src[np] = cand[q]; ++np; }
-          }
-        }
-        for (int k = k0; k < k0 + kb; ++k) {  // apply the swaps to the row labels
-          const int ip = piv[k];
-          if (ip == k) continue;
-          int a = 0, b = 0;
-          for (int t = 0; t < np; ++t) { if (s_pos[t] == k) a = t; if (s_pos[t] == ip) b = t; }
-          const int tmp = s_src[a]; s_src[a] = s_src[b]; s_src[b] = tmp;
-        }
-        s_np = np;
-      }
-      __syncthreads();
-      const int np = s_np;
-      // columns of this CTA: outside the panel, group-split
-      const int ncol = N - kb, per = (ncol + g.size - 1) / g.size;
-      const int j0 = g.rank * per, j1 = min(ncol, j0 + per);
-      const int cb = max(1, psm_cap / max(np, 1));
-      for (int jc = j0; jc < j1; jc += cb) {
-        const int nc = min(cb, j1 - jc);
-        for (int t = threadIdx.x; t < nc * np; t += blockDim.x) {
-          const int q = t % np, jj = jc + t / np, j = jj < k0 ? jj : jj + kb;
-          psm[t] = A[s_src[q] + size_t(j) * lda];
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < nc * np; t += blockDim.x) {
-          const int q = t % np, jj = jc + t / np, j = jj < k0 ? jj : jj + kb;
-          A[s_pos[q] + size_t(j) * lda] = psm[t];
-        }
-        __syncthreads();
+    // the panel's interchanges on all other columns (one thread per column, group-split; a gather
+    // through shared memory with a serial composition of the swaps measured slower)
+    for (int j = threadIdx.x + g.rank * blockDim.x; j < N; j += blockDim.x * g.size) {
+      if (j >= k0 && j < k0 + kb) continue;
+      double* col = A + size_t(j) * lda;
+      for (int k = k0; k < k0 + kb; ++k) {
+        const int ip = piv[k];
+        if (ip != k) { const double t = col[k]; col[k] = col[ip]; col[ip] = t; }
       }
     }
     grp_sync(g);
