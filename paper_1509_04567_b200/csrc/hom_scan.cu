@@ -21,6 +21,7 @@
 //   D: reduce h; x -= V h; pass-2 dot partials and ||x||^2                          | barrier
 //   E: reduce h2; x -= V h2; ||x|| = sqrt(||x||^2 - ||h2||^2); v_{k+1}; H column; publish
 // Cross-CTA reductions sum the per-CTA partials in a fixed order (identical in every CTA).
+#include <cstdlib>
 #include "kernels.cuh"
 #include "dense.cuh"
 #include "scan.cuh"
@@ -151,26 +152,51 @@ __device__ static double hom_check(const ScanArgs& a, int K, double gam, double 
   __syncthreads();
   cta_expm_pade13(K, S2, ld, WK, ld, a.iwork, red, kSolo, psm, HS_PSM);
   const double htail = __ldcg(a.H + K + size_t(K - 1) * ldh);
+  // chaining z_q = F z_{q-1} (F = e^{h A_hat}): F staged in shared memory when it fits, each row's
+  // dot split over NT/K-way thread groups; the residuals |h_{K+1,K} (H^{-1} z_q)_K| / gamma are
+  // evaluated afterwards from the stored z history (no block reduction inside the sequential loop)
+  const bool fs = size_t(K) * K <= size_t(HS_PSM);
+  double* F = fs ? psm : S2;
+  const int ldf = fs ? K : ld;
+  if (fs)
+    for (int t = threadIdx.x; t < K * K; t += NT) F[t] = S2[(t % K) + size_t(t / K) * ld];
   for (int r = threadIdx.x; r < K; r += NT) z[r] = r == 0 ? beta : 0.0;
   __syncthreads();
   for (int r = threadIdx.x; r < K; r += NT) a.Zc[r] = z[r];
-  double maxres = 0.0;
+  const int ng = max(1, min(8, NT / max(K, 1)));  // thread groups per row
+  const int jper = (K + ng - 1) / ng;
   for (int q = 1; q < a.s; ++q) {
-    for (int r = threadIdx.x; r < K; r += NT) {
-      double v = 0.0;
-      for (int j = 0; j < K; ++j) v = fma(S2[r + size_t(j) * ld], z[j], v);
-      zn[r] = v;
+    const int r = threadIdx.x % K, gq = threadIdx.x / K;
+    if (threadIdx.x < ng * K) {
+      const int j0 = gq * jper, j1 = min(K, j0 + jper);
+      double v0 = 0.0, v1 = 0.0;
+      int j = j0;
+      for (; j + 1 < j1; j += 2) {
+        v0 = fma(F[r + size_t(j) * ldf], z[j], v0);
+        v1 = fma(F[r + size_t(j + 1) * ldf], z[j + 1], v1);
+      }
+      if (j < j1) v0 = fma(F[r + size_t(j) * ldf], z[j], v0);
+      zn[gq * K + r] = v0 + v1;
     }
     __syncthreads();
-    double xp = 0.0;
-    for (int r = threadIdx.x; r < K; r += NT) {
-      z[r] = zn[r];
-      a.Zc[size_t(q) * a.kcap + r] = zn[r];
-      xp = fma(S1[(K - 1) + size_t(r) * ld], zn[r], xp);
+    for (int rr = threadIdx.x; rr < K; rr += NT) {
+      double v = 0.0;
+      for (int g2 = 0; g2 < ng; ++g2) v += zn[g2 * K + rr];
+      z[rr] = v;
+      a.Zc[size_t(q) * a.kcap + rr] = v;
     }
-    const double x = block_sum(xp, red);
-    maxres = fmax(maxres, fabs(htail * x) / gam);
+    __syncthreads();
   }
+  // residuals of all nodes in parallel (one warp per node)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double maxres = 0.0;
+  for (int q = 1 + w; q < a.s; q += NT / 32) {
+    double xp = 0.0;
+    for (int r = lane; r < K; r += 32) xp = fma(S1[(K - 1) + size_t(r) * ld], __ldcg(a.Zc + size_t(q) * a.kcap + r), xp);
+    xp = warp_sum(xp);
+    maxres = fmax(maxres, fabs(htail * xp) / gam);
+  }
+  maxres = block_max(maxres, red);
   __syncthreads();
   return maxres;
 }
@@ -465,10 +491,18 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   }
 }
 
+// worker CTAs of the scan: one per 256 rows (at most 147); PEXP_SCAN_NW overrides (developer)
+static int scan_workers(int n) {
+  static const int force = getenv("PEXP_SCAN_NW") ? atoi(getenv("PEXP_SCAN_NW")) : 0;
+  const int lo = cdiv(n, NT * RPT_MAX);
+  if (force > 0) return std::max(lo, std::min(147, force));
+  return std::min(147, cdiv(n, NT));
+}
+
 bool hom_scan_ok(int n, int kcap) { return kcap <= KSMALL_MAX && n <= 147 * NT * RPT_MAX; }
 
 size_t hom_scan_bytes(int n, int s, int kcap) {
-  const int nw = std::min(147, cdiv(n, NT));
+  const int nw = scan_workers(n);
   const size_t pw = kcap + 8;
   return sizeof(double) * (size_t(kcap + 1) * n + size_t(kcap + 1) * kcap + size_t(s) * kcap + 2 * nw * pw +
                            4 * nw + 10 * size_t(kcap) * kcap) +
@@ -481,7 +515,7 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   Arena ar{ws, ws_bytes, 0};
   ScanArgs a{};
   a.P = P; a.s = s; a.n = n; a.kcap = kcap; a.periodic = F.periodic;
-  a.nw = std::min(147, cdiv(n, NT));
+  a.nw = scan_workers(n);
   a.seg = cdiv(n, a.nw);
   a.rpt = cdiv(a.seg, NT);
   if (a.rpt > RPT_MAX) fail(1, "hom_scan: n too large for the persistent scan");
