@@ -34,7 +34,8 @@ constexpr size_t HOM_DYN = 72 * 1024;
 constexpr int SMALL_MINB = 2;
 #endif
 constexpr size_t HOM_FS_CAP = HOM_DYN / 8 - 2 * 256;
-constexpr size_t FS_CAP = SP_DYN / 8 - (2 * KSMALL_MAX + CH_PSUM + KSMALL_MAX + 2 * MAXS);
+constexpr int RING_N = 64;  // pieces whose residual partials are kept (s - 1 <= 63)
+constexpr size_t FS_CAP = SP_DYN / 8 - (2 * KSMALL_MAX + CH_PSUM + KSMALL_MAX + RING_N * MAXS);
 double g_piv_tol = getenv("PEXP_PIVTOL") ? atof(getenv("PEXP_PIVTOL")) : 1e-14;  // developer override
 constexpr size_t SM2 = 2 * MAXS * (MAXS + 1) * sizeof(double);  // two padded 64x64 tiles
 
@@ -662,8 +663,9 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPAr
       double* zb1 = zsm + KSMALL_MAX;
       double* psum = zsm + 2 * KSMALL_MAX;  // [jp][nrt*32]
       double* zown = psum + CH_PSUM;        // [nr]
-      double* ring = zown + KSMALL_MAX;     // [2][MAXS] residual partials (read remotely by rank 0)
-      double* Fs = ring + 2 * MAXS;         // own rows of F, column-major (ld nr), if they fit
+      double* ring = zown + KSMALL_MAX;     // [RING_N][MAXS] per-piece residual partials (read by rank 0)
+      double* Fs = ring + RING_N * MAXS;    // own rows of F, column-major (ld nr), if they fit
+      const bool ring_all = np <= RING_N;   // keep every piece's partial: reduce after the chain
       const bool fsm = size_t(nr) * Dz <= FS_CAP;
       double* Fo = WK;                      // [np][Dz] forcing of every piece
       double* Rg = WK + size_t(np) * Dz;    // [mt][Kp]
@@ -744,10 +746,10 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPAr
             for (int rl = lane; rl < nr; rl += 32)
               if (r0 + rl >= D) sacc = fma(Rg[size_t(tc) * Kp + r0 + rl - D], zown[rl], sacc);
             sacc = warp_sum(sacc);
-            if (lane == 0) ring[(i & 1) * MAXS + tc] = sacc;
+            if (lane == 0) ring[(ring_all ? i : (i & 1)) * MAXS + tc] = sacc;
           }
         grp_sync(g);
-        if (g.rank == 0 && mt > 0) {  // residual of node i+1 (partials stable until the next barrier)
+        if (!ring_all && g.rank == 0 && mt > 0) {  // residual of node i+1 (partials stable until the next barrier)
           for (int tc = threadIdx.x; tc < mt; tc += blockDim.x) {
             double v = 0.0;
             for (int q = 0; q < g.size; ++q) v += (g.size > 1 ? cl.map_shared_rank(ring, q) : ring)[(i & 1) * MAXS + tc];
@@ -767,6 +769,28 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPAr
             maxres = fmax(maxres, sqrt(fmax(r2, 0.0)) / gam);
           }
         }
+      }
+      if (ring_all && g.rank == 0 && mt > 0) {  // residuals of all nodes after the chain (one thread per node)
+        double mr = 0.0;
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+          double ts[MAXS];
+          for (int tc = 0; tc < mt; ++tc) {
+            double v = 0.0;
+            for (int q = 0; q < g.size; ++q) v += (g.size > 1 ? cl.map_shared_rank(ring, q) : ring)[i * MAXS + tc];
+            ts[tc] = v;
+          }
+          double r2 = 0.0;
+          if (a.stop_rule == 1) {
+            const double* Gt = a.Gt + e * a.gts_e;
+            for (int i1 = 0; i1 < mt; ++i1)
+              for (int i2 = 0; i2 < mt; ++i2) r2 += ts[i1] * Gt[(tidx[i1] - K) + size_t(tidx[i2] - K) * m] * ts[i2];
+          } else {
+            for (int i1 = 0; i1 < mt; ++i1) r2 += ts[i1] * ts[i1];
+          }
+          mr = fmax(mr, sqrt(fmax(r2, 0.0)) / gam);
+        }
+        mr = block_max(mr, red);
+        if (threadIdx.x == 0) maxres = mr;
       }
       if (g.rank == 0 && threadIdx.x == 0) {
         a.res[e] = maxres;
