@@ -1,11 +1,14 @@
 """bench.py — Paraexp-EBK solve on B200 (driver contract).
 
-One step = one pexp_solve_linear call over config C2 (BASELINE.json configs[1]: Dirichlet
-advection-diffusion, n=4096, P=64 subintervals, s=64 samples, tol=1e-8, fp64): 64 EBK
-evaluations (truncated two-pass SVD, SaI block Arnoldi, projected Pade-13 expm) + 63 batched
-homogeneous legs + superposition.  value = EBK evaluations/s over all ranks.
+Default workload C5 (BASELINE.json configs[4], the largest config the north-star target is
+quoted on): viscous Burgers, periodic, n = 65536, nu = 1e-3, T = 1, P = 256 subintervals,
+s = 64 samples, tol = 1e-8, fp64, waveform relaxation to max-norm change < 1e-6.  One step =
+one pexp_solve_burgers call: every WR iteration runs the batched EBK over all 256 subintervals
+(truncated two-pass SVD, SaI block Arnoldi, projected Pade-13 expm, superposition) and the
+homogeneous scan.  value = EBK evaluations/s over all ranks (P x WR iterations per solve);
+the solve time is ms_per_step.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C1|C3|C4|C5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5|C1|C2|C3|C4]
 
 N>1 (torchrun): "replicas only" — the north star keeps the path on one GPU, so each rank
 solves an independent replica (weak scaling, no data-path collective; the timing max is
@@ -28,15 +31,16 @@ import numpy as np  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
+METRIC = "EBK evaluations/s (Paraexp-EBK solve; solve time = ms_per_step)"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -140,13 +144,48 @@ def cpu_baseline(p, cfg, budget_s=20.0):
             oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol, i_max=k)
             evals, sample = k, f"first {k} of {p.P} subintervals (nonhomogeneous EBK + homogeneous legs, i_max={k})"
     else:
+        # WR iteration 1 on the first k subintervals of the workload (same ΔT, n, s), k doubled
+        # until the sample costs about budget_s / 3, then timed again
         from oracle.wr import wr_map
-        U = np.broadcast_to(p.u0, (p.P, p.s, p.n)).copy()
-        wr_map(U, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol)
-        evals, sample = p.P, "one WR iteration (iteration 1) of the workload"
+        dT = p.T / p.P
+        k = 1
+        while True:
+            U = np.broadcast_to(p.u0, (k, p.s, p.n)).copy()
+            t1 = time.perf_counter()
+            wr_map(U, p.u0, p.nu, p.n, dT * k, k, p.s, p.tol)
+            if time.perf_counter() - t1 > budget_s / 3 or 2 * k > p.P:
+                break
+            k *= 2
+        t0 = time.perf_counter()
+        U = np.broadcast_to(p.u0, (k, p.s, p.n)).copy()
+        wr_map(U, p.u0, p.nu, p.n, dT * k, k, p.s, p.tol)
+        evals, sample = k, f"WR iteration 1 on the first {k} of {p.P} subintervals (EBK + scan)"
     dt = time.perf_counter() - t0
     return {"value": evals / dt, "unit": "EBK evals/s", "cores": int(cores), "kind": "oracle", "sample": sample,
             "seconds": round(dt, 3)}
+
+
+def fp64_peak(dev):
+    """Measured fp64 tensor-core peak on this GPU: cuBLAS DGEMM (DMMA) 8192^3, best of 5 (CUDA
+    events).  The roofline denominator for the fp64 contraction kernels."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    c = a @ b
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del a, b, c
+    torch.cuda.empty_cache()
+    return {"tflops": 2.0 * n ** 3 / (best / 1e3) / 1e12, "how": "cuBLAS DGEMM 8192^3 fp64 (torch.matmul), best of 5",
+            "derived_fma_peak_tflops": FP64_PEAK_TFLOPS}
 
 
 def max_over_ranks(ms: float, world: int, dev) -> float:
@@ -191,13 +230,15 @@ def run_reference(args):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    sample = ("first subinterval of C2 (1 EBK eval, oracle SaI Krylov at eta=1e-12) per step"
-              if cfg["kind"] == "linear" else "2 subintervals of one WR iteration per step")
-    line = {"impl": "reference", "metric": "EBK evaluations/s (Paraexp-EBK solve)", "value": val,
+    sample = (f"first subinterval of {args.config} (1 EBK eval + its legs, oracle SaI Krylov at eta=1e-12) per step"
+              if cfg["kind"] == "linear" else
+              f"WR iteration 1 on the first {evals} of {p.P} subintervals of {args.config} per step (EBK + scan)")
+    line = {"impl": "reference", "metric": METRIC, "value": val,
             "unit": "EBK evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d).2)",
-            "config": {"workload": args.config, "sample": sample},
+            "config": {"workload": args.config, "n": p.n, "bc": p.bc, "P": p.P, "s": p.s, "tol": p.tol,
+                       "sample": sample},
             "cpu_baseline": {"value": val, "unit": "EBK evals/s", "cores": int(cores), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": val, "unit": "EBK evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -219,8 +260,12 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     from paper_1509_04567_b200 import build
-    build.build()
+    if local == 0:           # one build per node; the other ranks wait, then load the same .so
+        build.build()
+    if world > 1:
+        dist.barrier()
     from paper_1509_04567_b200 import pexp
+    fp64 = fp64_peak(dev)
 
     p, cfg = workload(args.config)
     linear = cfg["kind"] == "linear"
@@ -256,7 +301,7 @@ def main():
     torch.cuda.synchronize()
     times = []
     launches = 0
-    pexp.profile_enable(True)
+    syncs = 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -268,9 +313,21 @@ def main():
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
             launches += st["kernel_launches"]
+            syncs += st["host_syncs"]
+    evals_per_step = st["evals"]
+    # per-kernel breakdown from ONE extra, separately profiled step (CUDA events around every
+    # launch on its stream); the timed steps above ran with the profiler off
+    flush.zero_()
+    torch.cuda.synchronize()
+    pexp.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    step()
+    e1.record()
+    e1.synchronize()
+    prof_step_ms = e0.elapsed_time(e1)
     prof = pexp.profile_read()
     pexp.profile_enable(False)
-    evals_per_step = st["evals"]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -304,11 +361,11 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     dom = max(prof, key=lambda k: prof[k]["ms"])
     d = prof[dom]
-    if dom in ("small_problem", "small_dense"):
+    if dom in ("small_problem", "small_hom", "small_dense"):
         ach = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] else 0.0
-        roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
-                "peak_source": "derived fp64 FMA peak 148x64x2x1.965GHz (DESIGN.md §8)"}
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": fp64["tflops"], "unit": "TFLOP/s",
+                "frac": ach / fp64["tflops"], "traffic": None,
+                "peak_source": "measured fp64 DGEMM (cuBLAS, DMMA) on this GPU in this run"}
     else:
         ach = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] else 0.0
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
@@ -321,16 +378,17 @@ def main():
         if tj and tj.get("workload") == args.config:
             roof["traffic"] = tj["dram_bytes_per_launch"]
             roof["traffic_source"] = tj["source"]
-    roof["share_of_step"] = d["ms"] / max(1e-9, sum(times))
-    roof["launches_per_step"] = d["launches"] / args.steps
-    classes = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+    roof["share_of_step"] = d["ms"] / max(1e-9, prof_step_ms)
+    roof["launches_per_step"] = d["launches"]
+    roof["ms_per_step"] = d["ms"]
+    classes = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"],
                    "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None,
                    "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None}
                for k, v in prof.items()}
 
     if rank == 0:
         line = {
-            "metric": "EBK evaluations/s (Paraexp-EBK solve; solve time = ms_per_step)",
+            "metric": METRIC,
             "value": value, "unit": "EBK evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded generators, SURVEY §8(d).2)",
@@ -341,6 +399,9 @@ def main():
                        "max_m": st["max_m"], "max_k": st["max_k"], "wr_iters": st["wr_iters"]},
             "roofline": roof, "kernel_classes": classes,
             "gpu_launches": int(launches / args.steps),
+            "host_syncs_per_step": syncs / args.steps,
+            "profiled_step_ms": prof_step_ms,
+            "fp64_peak": fp64,
             "clocks": clk.summary(),
             "e2e": e2e,
         }

@@ -18,8 +18,9 @@
  *     The library never frees caller memory.
  *   - All device work is enqueued on the stream given in pexp_options.stream
  *     (a cudaStream_t; NULL = legacy default stream).  A pexp_solve_* call returns
- *     after its work has completed (it synchronises that stream at the end and at
- *     a few convergence checks).
+ *     after its work has completed.  It synchronises that stream at the end and at
+ *     the host-side control points listed in DESIGN.md §5.7 (block-width selection,
+ *     Krylov convergence checks, WR stop test); pexp_stats.host_syncs counts them.
  *   - Device scratch comes from the caller: query pexp_workspace_bytes(), allocate
  *     (e.g. a torch uint8 CUDA tensor), bind with pexp_set_workspace().  The library
  *     never calls cudaMalloc for scratch.
@@ -55,7 +56,8 @@ typedef enum {
   PEXP_ECUDA = 3,     /* a CUDA runtime error (message carries cudaGetErrorString)    */
   PEXP_ENOCONV = 4,   /* Krylov column cap k_max reached above tolerance              */
   PEXP_EDIVERGED = 5, /* WR iterate non-finite or its change grew > 1e3x      */
-  PEXP_EPIVOT = 6     /* shift-and-invert factorisation hit a (relatively) zero pivot   */
+  PEXP_EPIVOT = 6     /* shift-and-invert factorisation: a pivot that is zero relative to
+                         its row (|d_i| <= 1e-13 (|T_ii| + |l_i c_{i-1}|)) or non-finite    */
 } pexp_status;
 
 typedef enum { PEXP_BC_PERIODIC = 0, PEXP_BC_DIRICHLET = 1 } pexp_bc;
@@ -79,6 +81,17 @@ typedef struct {
                              8 n basis_cols bytes per evaluation); 0 = k_max               */
   int32_t eval_chunk;     /* nonhomogeneous EBK evaluations resident at once (the basis
                              memory is eval_chunk * basis_cols * n * 8 bytes); 0 = all      */
+  int32_t route;          /* block Arnoldi route: 0 = auto (fused cluster step when the
+                             step's panels fit shared memory, else the streaming route),
+                             1 = always the streaming route (full-grid TMA/DMMA kernels per
+                             product), 2 = fused step where it fits       */
+  double defl_tol;        /* deflation: a new Krylov column is dropped when block Gram-
+                             Schmidt leaves < defl_tol of its pre-orthogonalisation norm
+                             (default 1e-10; DESIGN.md §3 #22)                            */
+  double piv_tol;         /* in-block Cholesky-QR: smallest accepted scaled pivot
+                             (default 1e-14)                               */
+  int32_t hom_group;      /* linear homogeneous legs sharing one block Krylov space
+                             (default 8, at most 16)                       */
 } pexp_options;
 
 /* Per-solve statistics (host memory, caller-owned). */
@@ -92,6 +105,16 @@ typedef struct {
   float ms_total;          /* device time of the call (CUDA events), ms                */
   int32_t evals;           /* nonhomogeneous EBK evaluations performed                 */
   int32_t kernel_launches; /* kernels this library launched during the call            */
+  int32_t host_syncs;      /* host<->device synchronisations the call performed         */
+  double delta_hist[64];   /* Burgers: delta_k of WR iterations k = 1..min(wr_iters, 64)  */
+  /* Optional per-evaluation records (host arrays, caller-owned, NULL = not recorded).
+   * Linear: index b*P + j (one EBK evaluation per subinterval j of problem b).
+   * Burgers: index k*P + j for WR iteration k < max_wr_iters, subinterval j.
+   * m_j: retained source rank (block width); k_j: total Krylov dimension at convergence
+   * (all restart cycles); gamma_j: shift-and-invert parameter (reading #4). */
+  int32_t* m_j;
+  int32_t* k_j;
+  double* gamma_j;
 } pexp_stats;
 
 /* Create a context for one spatial operator A = nu*D2 - a*D1 on n points.
@@ -156,7 +179,8 @@ PEXP_API pexp_status pexp_expm_batched(pexp_ctx* ctx, const double* A, int32_t E
  * Classes: 0 SaI solve, 1 X^T Y projections/Grams (incl. reduce), 2 tall-skinny combine,
  * 3 projected problem (Pade-13 expm + chaining + residual), 4 small dense (eig, Cholesky,
  * one-sided SVD, spline), 5 stencil / assembly / superposition, 6 factorisation,
- * 7 fused Arnoldi step (SaI solve + BCGS2 + in-block QR, one CTA per evaluation).
+ * 7 fused Arnoldi step (SaI solve + BCGS2 + in-block QR, one cluster per evaluation),
+ * 8 Burgers homogeneous scan (persistent), 9 grouped homogeneous legs' projected problem.
  * pexp_profile_enable(1) clears and starts recording CUDA events around every launch
  * (on the launch stream), with the launch's ALGORITHMIC bytes and flops;
  * pexp_profile_read() synchronises the device, fills per-class sums (ms, bytes, flops,

@@ -814,16 +814,12 @@ size_t arnoldi_scratch_doubles(int E, int kcap, int mcap) {
 
 // cluster size: enough CTAs for ~2 waves over the 148 SMs, >= 512 rows per CTA, portable max 8
 static int step_cluster(int E, int n) {
-  static const int force = getenv("PEXP_ACL") ? atoi(getenv("PEXP_ACL")) : 0;  // developer override
-  if (force > 0) return std::min(force, 16);
   int cs = 1;
   while (cs < 8 && long(E) * cs < 2 * 148 && n / (2 * cs) >= 512) cs *= 2;
   // very small batches (e.g. 8 groups of homogeneous legs): a non-portable 16-CTA cluster
   if (cs == 8 && E * 16 <= 148 && n / 16 >= 256) cs = 16;
   return cs;
 }
-
-extern double g_piv_tol;
 
 template <int MB>
 static void launch_mb(cudaStream_t st, const StepArgs& a, size_t smem) {
@@ -847,7 +843,7 @@ static void launch_mb(cudaStream_t st, const StepArgs& a, size_t smem) {
 void launch_arnoldi_step(cudaStream_t st, StepArgs a) {
   const int MB = mb_for(a.m);
   a.rc = RC;
-  a.piv_tol = g_piv_tol;
+  a.piv_tol = g_cfg.piv_tol;
   a.cs = step_cluster(a.E, a.n);
   const int nv = (a.b + 1) * a.m;
   const int per = step_rows(a.n, a.cs);
@@ -860,8 +856,8 @@ void launch_arnoldi_step(cudaStream_t st, StepArgs a) {
     smem = step_smem(MB, 0, per);
   }
   if (smem > 200 * 1024) fail(1, "fused Arnoldi step: block rows exceed shared memory");
-  ProfScope ps(PC_ARNOLDI, st, double(a.E) * a.n * 8.0 * (4.0 * nv + 12.0 * a.m),
-               double(a.E) * a.n * (8.0 * nv * a.m + 10.0 * a.m * a.m));
+  const double ea = eact(a.E, a.active);
+  ProfScope ps(PC_ARNOLDI, st, ea * a.n * 8.0 * (4.0 * nv + 12.0 * a.m), ea * a.n * (8.0 * nv * a.m + 10.0 * a.m * a.m));
   if (MB == 8)
     launch_mb<8>(st, a, smem);
   else if (MB == 16)

@@ -491,13 +491,8 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   }
 }
 
-// worker CTAs of the scan: one per 256 rows (at most 147); PEXP_SCAN_NW overrides (developer)
-static int scan_workers(int n) {
-  static const int force = getenv("PEXP_SCAN_NW") ? atoi(getenv("PEXP_SCAN_NW")) : 0;
-  const int lo = cdiv(n, NT * RPT_MAX);
-  if (force > 0) return std::max(lo, std::min(147, force));
-  return std::min(147, cdiv(n, NT));
-}
+// worker CTAs of the scan: one per 256 rows (at most 147)
+static int scan_workers(int n) { return std::min(147, cdiv(n, NT)); }
 
 bool hom_scan_ok(int n, int kcap) { return kcap <= KSMALL_MAX && n <= 147 * NT * RPT_MAX; }
 
@@ -542,18 +537,14 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
     ProfScope ps(PC_SCAN, st, double(P) * s * n * 24.0, 0.0);
     void* args[] = {&a};
     const size_t smem = sizeof(double) * (2 * (KSMALL_MAX + 8) + NT * RPT_MAX + HS_PSM);
-    static bool attr = false;
-    if (!attr) {
-      PEXP_CUDA_TRY(cudaFuncSetAttribute(k_hom_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    PEXP_CUDA_TRY(cudaFuncSetAttribute(k_hom_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PEXP_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hom_scan, dim3(a.nw + 1), dim3(NT), args, smem, st));
   }
   count_launch();
   PEXP_LAUNCH_CHECK();
   int hf[F_NFLAGS];
   PEXP_CUDA_TRY(cudaMemcpyAsync(hf, a.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
-  PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+  host_sync(st);
   if (hf[F_ERR]) fail(4 /* PEXP_ENOCONV */, "Krylov capacity reached (homogeneous scan)");
   return hf[F_KMAX];
 }

@@ -7,6 +7,25 @@ namespace pexp {
 
 constexpr int KSMALL_MAX = 1024;  // max Krylov columns (K + m) of one projected problem
 
+// Per-call numerical / routing configuration, set from pexp_options at the start of every
+// C-ABI call (thread-local: concurrent calls on different host threads do not interfere).
+struct CallCfg {
+  double defl = 1e-10;     // pexp_options.defl_tol
+  double piv_tol = 1e-14;  // pexp_options.piv_tol
+  int route = 0;           // pexp_options.route (0 auto, 1 streaming, 2 fused where it fits)
+  int hom_group = 8;       // pexp_options.hom_group
+  int syncs = 0;           // host synchronisations performed by the current call
+  int active_hint = -1;    // evaluations still active in the running EBK loop (-1: unknown);
+                           // the profiler's algorithmic byte/flop counts use it
+};
+extern thread_local CallCfg g_cfg;
+// Host synchronisation of the call's stream (counted into pexp_stats.host_syncs).
+void host_sync(cudaStream_t st);
+// Evaluations a masked launch over E evaluations actually processes (profiler accounting).
+inline double eact(int E, const void* active) {
+  return (active && g_cfg.active_hint >= 0 && g_cfg.active_hint < E) ? double(g_cfg.active_hint) : double(E);
+}
+
 // Tridiagonal rows of the operators A (not M = I - gamma*A): [nops][n] each.
 struct Ops {
   int n = 0, nops = 0;
@@ -128,7 +147,7 @@ void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long
                        long long ls_e, const int* active, bool pivoted, double dtol = 0.0,
                        double* norm0_out = nullptr);
 void launch_defer_corr(cudaStream_t st, int E, int N, const double* Gb, long long gs_e, const int* cls, long long cs_e,
-                       double* Mc, const int* active);
+                       double* Mc, const int* active, bool plus_identity = false);
 void launch_onesided_svd(cudaStream_t st, int E, int s, const double* C, const int* kk, double tau, double* Qs,
                          double* sig, double* Cs, int* m_out, const int* active);
 void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, const double* Qs,
@@ -183,7 +202,8 @@ void launch_hupdate(cudaStream_t st, int E, int rows, int m, const double* T, lo
                     long long rs_e, int ldr, double* H, long long hs_e, int ldh, const int* active);
 void launch_hom_setup(cudaStream_t st, int E, int mode, int P, int s, double h, double eta, const double* beta,
                       double* crit, int* npieces, int* active);
-void launch_update_active(cudaStream_t st, int E, const int* conv, int* active, int* count);
+void launch_update_active(cudaStream_t st, int E, const int* conv, int* active, int* count, int* krec = nullptr,
+                          int kval = 0);
 void launch_fill_i32(cudaStream_t st, int* p, int count, int v);
 void launch_fill_f64(cudaStream_t st, double* p, size_t count, double v);
 

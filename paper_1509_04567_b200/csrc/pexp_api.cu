@@ -16,8 +16,16 @@
 
 namespace pexp {
 thread_local long g_launches = 0;
+thread_local CallCfg g_cfg;
 bool g_prof_on = false;
+// PEXP_SYNC=1: synchronise after every launch to localise a device fault (debugging aid only;
+// it changes no numerics, routing or sizes).
 bool g_sync_debug = getenv("PEXP_SYNC") != nullptr;
+
+void host_sync(cudaStream_t st) {
+  PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+  ++g_cfg.syncs;
+}
 std::vector<ProfRec> g_prof;
 
 // ---------------------------------------------------------------- helper kernels
@@ -54,7 +62,7 @@ template <class T>
 static void h2d(cudaStream_t st, T* dst, const std::vector<T>& v) {
   if (v.empty()) return;
   PEXP_CUDA_TRY(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
-  PEXP_CUDA_TRY(cudaStreamSynchronize(st));  // pageable source: keep it alive until copied
+  host_sync(st);  // pageable source: keep it alive until copied
 }
 
 // ---------------------------------------------------------------- options
@@ -63,6 +71,7 @@ struct Opts {
   double tau_f, eta_f;
   int restart_blocks, kcap, stop_rule, kcyc, chunk;
   cudaStream_t st;
+  CallCfg cfg;
 };
 
 static Opts norm_opts(const pexp_options& o) {
@@ -76,6 +85,11 @@ static Opts norm_opts(const pexp_options& o) {
   r.chunk = o.eval_chunk > 0 ? o.eval_chunk : (1 << 30);
   r.st = (cudaStream_t)o.stream;
   r.stop_rule = o.stop_rule;
+  r.cfg.defl = o.defl_tol > 0 ? o.defl_tol : 1e-10;
+  r.cfg.piv_tol = o.piv_tol > 0 ? o.piv_tol : 1e-14;
+  r.cfg.route = o.route;
+  r.cfg.hom_group = o.hom_group > 0 ? std::min(o.hom_group, 16) : 8;
+  r.cfg.syncs = 0;
   return r;
 }
 
@@ -84,7 +98,7 @@ struct EbkBufs {
   int E = 0, n = 0, kcap = 0, ktot = 0, mcap = 0, nout = 0, s = 0, groups = 1;
   long long vs_e = 0, hs_e = 0, zs_e = 0;
   double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p, *R0, *critc;
-  int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc;
+  int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc, *krec;
   double* part;
   size_t part_cap;
   double* stepws = nullptr;  // fused Arnoldi step: global V^T W partials (large bases)
@@ -134,6 +148,7 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   B.fidx = ar.take<int>(E);
   B.opidx = ar.take<int>(E);
   B.xcnt = ar.take<int>(E);
+  B.krec = ar.take<int>(E);
   // ---- heavy, one chunk
   B.V = ar.take<double>(size_t(Ec) * kcap * n);
   B.H = ar.take<double>(size_t(Ec) * kcap * kcap);
@@ -181,7 +196,7 @@ static EbkBufs chunk_view(const EbkBufs& B, int c0, int Ec, int mb) {
   EbkBufs C = B;
   C.E = Ec;
   C.res += c0; C.gam += c0; C.crit += c0; C.active += c0; C.conv += c0; C.kfin += c0;
-  C.npieces += c0; C.fidx += c0; C.opidx += c0; C.xcnt += c0;
+  C.npieces += c0; C.fidx += c0; C.opidx += c0; C.xcnt += c0; C.krec += c0;
   C.beta += c0;  // kind-1 layout (forced chunks do not read beta)
   if (C.coef) C.coef += size_t(c0) * (B.s - 1) * 4 * mb;
   return C;
@@ -218,11 +233,17 @@ static void inblock_qr(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0,
   for (int rep = 0; rep < 2; ++rep) {
     launch_xty(st, E, n, B.V, ws_e, c0, m, B.V, ws_e, c0, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0, false,
                active, B.xcnt);
-    launch_defer_corr(st, E, m, B.G1, (long long)m * m, B.live + c0, B.kcap, B.Rinv, active);
-    if (m <= 32)
+    if (m <= 32) {
+      launch_defer_corr(st, E, m, B.G1, (long long)m * m, B.live + c0, B.kcap, B.Rinv, active);
       launch_combine(st, E, n, B.V, ws_e, c0, m, B.Rinv, (long long)m * m, m, B.V, ws_e, c0, m, 1.0, 1.0, active);
-    else
-      fail(1, "block width > 32 with deferred columns not supported");
+    } else {  // wider blocks: V_blk (I + Mc) out of place, then copied back
+      launch_defer_corr(st, E, m, B.G1, (long long)m * m, B.live + c0, B.kcap, B.Rinv, active, true);
+      launch_combine(st, E, n, B.V, ws_e, c0, m, B.Rinv, (long long)m * m, m, B.Wt2, (long long)m * n, 0, m, 1.0, 0.0,
+                     active);
+      PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.V + size_t(c0) * n, ws_e * sizeof(double), B.Wt2,
+                                      size_t(m) * n * sizeof(double), size_t(m) * n * sizeof(double), E,
+                                      cudaMemcpyDeviceToDevice, st));
+    }
   }
   chol_combine_block(st, B, E, n, m, c0, B.n0p, m, 0, 0.0, defl, nullptr, active);
 }
@@ -261,13 +282,13 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   launch_fill_i32(st, B.kfin, E, 0);
   launch_fill_i32(st, B.conv, E, 0);
   PEXP_LAUNCH_CHECK();
-  static const bool nofuse = getenv("PEXP_NOFUSE") != nullptr;  // developer switch
   // fused cluster step (arnoldi.cu) whenever the step's panels fit shared memory
   int steps = 0, last_check = -1;
   int next_check = std::max(4, 2 * m);
-  // deflation: a new column is dropped when BCGS leaves < 1e-10 of ||(I - gamma A)^{-1} v|| (well
-  // above the shift-and-invert solve rounding (~1e-13..1e-12), below the 1e-8 parity bar)
-  static const double defl = getenv("PEXP_DEFL") ? atof(getenv("PEXP_DEFL")) : 1e-10;  // developer override
+  // deflation: a new column is dropped when BCGS leaves < defl (default 1e-10) of
+  // ||(I - gamma A)^{-1} v|| (well above the shift-and-invert solve rounding (~1e-13..1e-12),
+  // below the 1e-8 parity bar); pexp_options.defl_tol
+  const double defl = g_cfg.defl;
   SPArgs a{};
   a.E = E; a.kcap = kcap; a.m = m; a.kind = kind;
   a.H = B.H; a.hs_e = B.hs_e; a.ldh = kcap;
@@ -314,11 +335,12 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     else
       launch_small_problem(st, a, B.nslots, Koff);
     PEXP_CUDA_TRY(cudaMemsetAsync(B.count, 0, sizeof(int), st));
-    launch_update_active(st, E, B.conv, B.active, B.count);
+    launch_update_active(st, E, B.conv, B.active, B.count, B.krec, Koff + K);
     int h_count = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&h_count, B.count, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    host_sync(st);
     remaining = h_count;
+    g_cfg.active_hint = remaining;
     last_check = K;
     info.max_k = std::max(info.max_k, K);
     info.max_ktot = std::max(info.max_ktot, Koff + K);
@@ -330,7 +352,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       PEXP_CUDA_TRY(cudaMemcpyAsync(hres.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
       PEXP_CUDA_TRY(cudaMemcpyAsync(hcrit.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
       PEXP_CUDA_TRY(cudaMemcpyAsync(hact.data(), B.active, E * sizeof(int), cudaMemcpyDeviceToHost, st));
-      PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+      host_sync(st);
       std::vector<double> preds;
       for (int e = 0; e < E; ++e) {
         if (!hact[e] || !(kind == 2 || hcrit[e] > 0)) continue;
@@ -348,45 +370,6 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
         predicted_next = (int)std::ceil(p80);
       }
     }
-    static const char* dump = getenv("PEXP_DUMP");
-    if (dump && E == 1) {  // developer dump of the Arnoldi state of a single evaluation
-      std::vector<double> hv(size_t(kcap) * n), hh(size_t(kcap) * kcap), hz(size_t(B.nout) * kcap);
-      std::vector<int> hl(kcap);
-      cudaMemcpy(hv.data(), B.V, hv.size() * 8, cudaMemcpyDeviceToHost);
-      cudaMemcpy(hh.data(), B.H, hh.size() * 8, cudaMemcpyDeviceToHost);
-      cudaMemcpy(hz.data(), B.Z, hz.size() * 8, cudaMemcpyDeviceToHost);
-      cudaMemcpy(hl.data(), B.live, hl.size() * 4, cudaMemcpyDeviceToHost);
-      std::string base = std::string(dump) + "_K" + std::to_string(K);
-      FILE* fp = fopen((base + ".bin").c_str(), "wb");
-      if (fp) {
-        int hdr[5] = {n, kcap, K, m, B.nout};
-        fwrite(hdr, 4, 5, fp);
-        fwrite(hl.data(), 4, hl.size(), fp);
-        fwrite(hv.data(), 8, hv.size(), fp);
-        fwrite(hh.data(), 8, hh.size(), fp);
-        fwrite(hz.data(), 8, hz.size(), fp);
-        fclose(fp);
-      }
-    }
-    static const bool dbg = getenv("PEXP_DEBUG") != nullptr;
-    if (dbg) {  // developer trace: residual/target distribution at this check
-      std::vector<double> r(E), c(E);
-      std::vector<int> lv(size_t(E) * kcap), cv(E);
-      cudaMemcpy(r.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost);
-      cudaMemcpy(c.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost);
-      cudaMemcpy(cv.data(), B.conv, E * sizeof(int), cudaMemcpyDeviceToHost);
-      cudaMemcpy(lv.data(), B.live, size_t(E) * kcap * sizeof(int), cudaMemcpyDeviceToHost);
-      std::vector<double> q;
-      int tail_live = 0, dead_total = 0;
-      for (int e = 0; e < E; ++e) {
-        q.push_back(kind == 2 ? r[e] : (c[e] > 0 ? r[e] / c[e] : -1));
-        for (int j = K; j < K + m; ++j) tail_live += lv[size_t(e) * kcap + j];
-        for (int j = 0; j < K; ++j) dead_total += !lv[size_t(e) * kcap + j];
-      }
-      std::sort(q.begin(), q.end());
-      fprintf(stderr, "[pexp] kind=%d E=%d m=%d K=%d remaining=%d ratio min=%.3g med=%.3g max=%.3g tail_live=%d dead=%d\n",
-              kind, E, m, K, remaining, q.front(), q[q.size() / 2], q.back(), tail_live, dead_total);
-    }
   };
   // initial active count (some evals may start inactive: zero source / zero start vector)
   {
@@ -394,8 +377,9 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     launch_update_active(st, E, B.conv, B.active, B.count);
     int h_count = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&h_count, B.count, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    host_sync(st);
     remaining = h_count;
+    g_cfg.active_hint = remaining;
   }
   while (remaining > 0) {
     const bool cyc_full = (steps + 2) * m > kcap;            // no room for another block + tail
@@ -438,7 +422,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     }
     const int b = steps, nv = (b + 1) * m;
     const long long ws_e = B.vs_e;
-    if (!nofuse && arnoldi_fused_ok(m, nv, n, E, B.stepws != nullptr)) {  // one cluster per evaluation: whole step
+    if (g_cfg.route != 1 && arnoldi_fused_ok(m, nv, n, E, B.stepws != nullptr)) {  // one cluster per evaluation: whole step
       StepArgs sa{};
       sa.E = E; sa.n = n; sa.m = m; sa.b = b; sa.kcap = kcap; sa.periodic = F.periodic;
       sa.V = B.V; sa.vs_e = B.vs_e; sa.H = B.H; sa.hs_e = B.hs_e; sa.live = B.live; sa.fidx = B.fidx;
@@ -485,11 +469,12 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     }
   }
   info.unconverged = remaining;
+  g_cfg.active_hint = -1;
   {  // worst residual / target over the evaluations at their last check (diagnostic)
     std::vector<double> r(E), c(E);
     PEXP_CUDA_TRY(cudaMemcpyAsync(r.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
     PEXP_CUDA_TRY(cudaMemcpyAsync(c.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    host_sync(st);
     for (int e = 0; e < E; ++e)
       if (last_check >= 0 && (kind == 2 || c[e] > 0))
         info.worst_res_ratio = std::max(info.worst_res_ratio, kind == 2 ? r[e] : r[e] / c[e]);
@@ -576,7 +561,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
     launch_xty(st, E, n, X, gs_e, 0, s, X, gs_e, 0, s, part, part_cap, S.Gs, (long long)s * s, s, 0, 0, false, nullptr, B->xcnt);
     launch_sym_eig_select(st, E, s, S.Gs, S.lam, S.Msel, S.off, S.sigma1, p, tau, theta, nullptr);
     PEXP_CUDA_TRY(cudaMemcpyAsync(offh.data(), S.off, E * sizeof(int), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    host_sync(st);
     int kn = 0;
     for (int e = 0; e < E; ++e) kn = std::max(kn, offh[e]);
     if (kn == 0) break;  // all-zero samples: nothing selected
@@ -603,7 +588,7 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
   launch_onesided_svd(st, E, s, S.Cb, S.off, tau, S.Qs, S.sig, S.Cs, S.me, nullptr);
   std::vector<int> mh(E);
   PEXP_CUDA_TRY(cudaMemcpyAsync(mh.data(), S.me, E * sizeof(int), cudaMemcpyDeviceToHost, st));
-  PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+  host_sync(st);
   int mmax = 0;
   for (int e = 0; e < E; ++e) mmax = std::max(mmax, mh[e]);
   if (me_host) std::copy(mh.begin(), mh.end(), me_host);
@@ -706,12 +691,30 @@ static pexp_status guarded(pexp_ctx* c, F&& f) {
   }
 }
 
-// Homogeneous legs per group (one shared block Krylov space per group; <= 16, KSMALL limits)
-static int hom_group_width(int P) {
-  static const int force = getenv("PEXP_MH") ? atoi(getenv("PEXP_MH")) : 0;  // developer override
-  const int w = force > 0 ? std::min(force, 16) : 8;  // measured on C2: 8 legs per group beat 16 (48 vs 58 ms)
+// Homogeneous legs per group (one shared block Krylov space per group; <= 16, KSMALL limits).
+// pexp_options.hom_group, default 8 (measured on C2: 8 legs per group beat 16, 48 vs 58 ms).
+static int hom_group_width(const pexp_ctx* c, int P) {
+  const int w = c->opt.hom_group > 0 ? std::min(c->opt.hom_group, 16) : 8;
   return std::max(1, std::min(w, P - 1));
 }
+
+// Two CUDA events of a timed call, destroyed on every exit path (errors throw).
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() {
+    PEXP_CUDA_TRY(cudaEventCreate(&a));
+    PEXP_CUDA_TRY(cudaEventCreate(&b));
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  float ms() {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    return t;
+  }
+};
 
 // ---------------------------------------------------------------- workspace plans
 struct LinPlan {
@@ -749,7 +752,7 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
   alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable);
   if (P > 1) {
-    const int mh = hom_group_width(P), G = cdiv(P - 1, mh), Eg = Bt * G;
+    const int mh = hom_group_width(c, P), G = cdiv(P - 1, mh), Eg = Bt * G;
     // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
     // 16 legs -> 288 columns); give it at least 24 block steps
     const int kcap_h = std::min(KSMALL_MAX - 64, std::max(o.kcap, 24 * mh));
@@ -821,12 +824,16 @@ static size_t bur_bytes(const pexp_ctx* c, int P) {
   return ar.off;
 }
 
+// One-time per-device kernel attributes (> 48 KB dynamic shared memory, cluster sizes).
 static void init_once() {
-  static bool done = false;
-  if (!done) {
+  static unsigned long long done = 0;  // bit d: device d initialised
+  int dev = 0;
+  PEXP_CUDA_TRY(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(done & bit)) {
     tsmm_init();
     small_init();
-    done = true;
+    done |= bit;
   }
 }
 
@@ -882,6 +889,8 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
   if (o.k_max < 0 || o.k_max > KSMALL_MAX - 64) return PEXP_EINVAL;
   if (o.stop_rule < 0 || o.stop_rule > 1) return PEXP_EINVAL;
   if (o.basis_cols < 0 || o.eval_chunk < 0) return PEXP_EINVAL;
+  if (o.route < 0 || o.route > 2 || o.defl_tol < 0 || o.piv_tol < 0 || o.hom_group < 0 || o.hom_group > 16)
+    return PEXP_EINVAL;
   pexp_ctx* c = new pexp_ctx;
   c->n = n;
   c->bc = bc;
@@ -934,6 +943,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     init_once();
     g_launches = 0;
     Opts o = norm_opts(ctx->opt);
+    g_cfg = o.cfg;
     cudaStream_t st = o.st;
     const int n = (int)ctx->n, Bt = ctx->batch, s = o.s, E = Bt * P, Eh = Bt * (P - 1);
     const bool periodic = ctx->bc == PEXP_BC_PERIODIC;
@@ -941,10 +951,8 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     Arena ar{ctx->ws, ctx->ws_bytes, 0};
     LinPlan L;
     plan_linear(ar, L, ctx, P);
-    cudaEvent_t e0, e1;
-    PEXP_CUDA_TRY(cudaEventCreate(&e0));
-    PEXP_CUDA_TRY(cudaEventCreate(&e1));
-    PEXP_CUDA_TRY(cudaEventRecord(e0, st));
+    EventPair ev;
+    PEXP_CUDA_TRY(cudaEventRecord(ev.a, st));
     // operators and factorisations: f < Bt: gamma = dT/10 (nonhomogeneous); f >= Bt: gamma = T/10 (legs)
     h2d(st, L.nu_d, ctx->nu);
     h2d(st, L.a_d, ctx->a);
@@ -968,12 +976,14 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     h2d(st, L.B.fidx, fe);
     h2d(st, L.B.opidx, fe);
     h2d(st, L.B.gam, ge);
-    int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, nullptr);
+    std::vector<int> me(E);
+    int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, me.data());
     sf.join();
     int herr = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
-    if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
+    host_sync(st);
+    if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: a pivot is zero relative to its row or non-finite");
+    launch_fill_i32(st, L.B.krec, E, 0);
     RunInfo ri{}, rh{};
     if (mmax > 0) {
       ri = ebk_forced_chunked(st, L.B, L.S, L.F, L.O, periodic, E, mmax, h, s, s - 1, 2, 1, L.Yend, n, o.stop_rule,
@@ -986,7 +996,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
       // homogeneous legs, grouped: up to 16 consecutive legs share one block Krylov space
       // (EBK for the homogeneous part too); group eh = b*G + g holds legs
       // j = g*mh .. g*mh+mh-1 of problem b
-      const int mh = hom_group_width(P);
+      const int mh = hom_group_width(ctx, P);
       G = cdiv(P - 1, mh);
       const int Eg = Bt * G;
       EbkBufs& Bh = L.Bh;
@@ -1004,7 +1014,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
                                       size_t(mh) * n * sizeof(double), Eg, cudaMemcpyDeviceToDevice, st));
       launch_xty(st, Eg, n, Bh.V, Bh.vs_e, 0, mh, Bh.V, Bh.vs_e, 0, mh, Bh.part, Bh.part_cap, Bh.G0,
                  (long long)mh * mh, mh, 0, 0, false, nullptr, Bh.xcnt);
-      static const double defl_h = getenv("PEXP_DEFL") ? atof(getenv("PEXP_DEFL")) : 1e-10;
+      const double defl_h = g_cfg.defl;
       inblock_qr(st, Bh, Eg, n, mh, 0, Bh.G0, (long long)mh * mh, mh, defl_h, nullptr);
       chol_combine_block(st, Bh, Eg, n, mh, 0, nullptr, 0, 0, 0.0, defl_h, nullptr, nullptr);
       launch_xty(st, Eg, n, Bh.V, Bh.vs_e, 0, mh, Bh.Wt, (long long)mh * n, 0, mh, Bh.part, Bh.part_cap, Bh.R0,
@@ -1015,15 +1025,22 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
                      (long long)P * n, 0, P, 1.0, 0.0, nullptr, Bh.kfin);
     }
     launch_superpose(st, Bt, P, n, u0, L.Yend, P > 1 ? L.Yh : nullptr, (long long)P * n, n, G, out);
-    PEXP_CUDA_TRY(cudaEventRecord(e1, st));
-    PEXP_CUDA_TRY(cudaEventSynchronize(e1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    PEXP_CUDA_TRY(cudaEventRecord(ev.b, st));
+    PEXP_CUDA_TRY(cudaEventSynchronize(ev.b));
+    ++g_cfg.syncs;
+    const float ms = ev.ms();
     check_err(st);
     if (st_out) {
+      int32_t *mj = st_out->m_j, *kj = st_out->k_j;
+      double* gj = st_out->gamma_j;
       std::memset(st_out, 0, sizeof(*st_out));
+      st_out->m_j = mj; st_out->k_j = kj; st_out->gamma_j = gj;
+      if (mj) std::copy(me.begin(), me.end(), mj);
+      if (kj) {
+        PEXP_CUDA_TRY(cudaMemcpy(kj, L.B.krec, E * sizeof(int), cudaMemcpyDeviceToHost));
+        ++g_cfg.syncs;
+      }
+      if (gj) std::fill(gj, gj + E, dT / 10);
       st_out->max_m = mmax;
       st_out->max_k = std::max(ri.max_ktot, rh.max_ktot);
       st_out->restarts = ri.restarts;
@@ -1031,6 +1048,7 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
       st_out->ms_total = ms;
       st_out->evals = E;
       st_out->kernel_launches = (int)g_launches;
+      st_out->host_syncs = g_cfg.syncs;
     }
     if (ri.unconverged || rh.unconverged)
       fail(PEXP_ENOCONV, "Krylov capacity k_max reached before the residual target (" +
@@ -1058,6 +1076,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
     init_once();
     g_launches = 0;
     Opts o = norm_opts(ctx->opt);
+    g_cfg = o.cfg;
     cudaStream_t st = o.st;
     const int n = (int)ctx->n, s = o.s, E = P;
     const double dT = T / P, h = dT / (s - 1), tau = o.tau_f * tol, eta = o.eta_f * tol;
@@ -1065,10 +1084,12 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
     Arena ar{ctx->ws, ctx->ws_bytes, 0};
     BurPlan L;
     plan_burgers(ar, L, ctx, P);
-    cudaEvent_t e0, e1;
-    PEXP_CUDA_TRY(cudaEventCreate(&e0));
-    PEXP_CUDA_TRY(cudaEventCreate(&e1));
-    PEXP_CUDA_TRY(cudaEventRecord(e0, st));
+    EventPair ev;
+    PEXP_CUDA_TRY(cudaEventRecord(ev.a, st));
+    int32_t* rec_m = st_out ? st_out->m_j : nullptr;
+    int32_t* rec_k = st_out ? st_out->k_j : nullptr;
+    double* rec_g = st_out ? st_out->gamma_j : nullptr;
+    std::vector<double> dhist;
     std::vector<int> iota(P);
     for (int j = 0; j < P; ++j) iota[j] = j;
     h2d(st, L.iota, iota);
@@ -1084,13 +1105,18 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       SideFactor sf(ctx, st);
       launch_factor(sf.stream(), L.F, P, L.iota, L.B.gam, L.O, L.err);
       launch_burgers_source(st, P, s, n, nu, u0, L.Uk, L.ubar, L.G);
-      int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, nullptr);
+      std::vector<int> me(E);
+      int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, me.data());
       sf.join();
       int herr = 0;
       PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
-      PEXP_CUDA_TRY(cudaStreamSynchronize(st));
-      if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
+      host_sync(st);
+      if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: a pivot is zero relative to its row or non-finite");
       max_m = std::max(max_m, mmax);
+      if (rec_m) std::copy(me.begin(), me.end(), rec_m + size_t(k) * P);
+      if (rec_g) PEXP_CUDA_TRY(cudaMemcpyAsync(rec_g + size_t(k) * P, L.B.gam, P * sizeof(double),
+                                               cudaMemcpyDeviceToHost, st));
+      launch_fill_i32(st, L.B.krec, E, 0);
       if (mmax > 0) {
         RunInfo ri = ebk_forced_chunked(st, L.B, L.S, L.F, L.O, true, E, mmax, h, s, 1, s, 0, L.Y, (long long)s * n,
                                         o.stop_rule, o.restart_blocks);
@@ -1100,11 +1126,12 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       } else {
         PEXP_CUDA_TRY(cudaMemsetAsync(L.Y, 0, size_t(P) * s * n * sizeof(double), st));
       }
+      if (rec_k) PEXP_CUDA_TRY(cudaMemcpyAsync(rec_k + size_t(k) * P, L.B.krec, P * sizeof(int),
+                                               cudaMemcpyDeviceToHost, st));
       PEXP_CUDA_TRY(cudaMemsetAsync(L.delta, 0, sizeof(double), st));
-      static const bool noscan = getenv("PEXP_NOSCAN") != nullptr;  // developer switch: host-driven scan
-      if (L.scan_ws && !noscan) {
+      if (L.scan_ws) {  // persistent cooperative scan; host-driven fallback beyond its row capacity
         const int k1 = std::min(o.kcap, 512);
-        static const double defl_s = getenv("PEXP_DEFL") ? atof(getenv("PEXP_DEFL")) : 1e-10;
+        const double defl_s = g_cfg.defl;
         max_k = std::max(max_k, launch_hom_scan(st, L.F, L.B.gam, P, s, n, k1, h, eta, defl_s, u0, L.Y, L.Uk, L.Un,
                                                 L.delta, L.scan_ws, L.scan_bytes));
       } else
@@ -1130,8 +1157,9 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
         launch_wr_step(st, s, n, u0, L.Wh, L.Y + off, L.Uk + off, L.Un + off, L.uhat, L.delta);
       }
       PEXP_CUDA_TRY(cudaMemcpyAsync(&delta, L.delta, sizeof(double), cudaMemcpyDeviceToHost, st));
-      PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+      host_sync(st);
       std::swap(L.Uk, L.Un);
+      dhist.push_back(delta);
       ++iters;
       if (delta0 < 0) delta0 = delta;
       if (!std::isfinite(delta) || delta > 1e3 * delta0)
@@ -1139,15 +1167,16 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       if (delta < wr_tol) break;
     }
     launch_copy_end(st, P, s, n, L.Uk, out);
-    PEXP_CUDA_TRY(cudaEventRecord(e1, st));
-    PEXP_CUDA_TRY(cudaEventSynchronize(e1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    PEXP_CUDA_TRY(cudaEventRecord(ev.b, st));
+    PEXP_CUDA_TRY(cudaEventSynchronize(ev.b));
+    ++g_cfg.syncs;
+    const float ms = ev.ms();
     check_err(st);
     if (st_out) {
       std::memset(st_out, 0, sizeof(*st_out));
+      st_out->m_j = rec_m; st_out->k_j = rec_k; st_out->gamma_j = rec_g;
+      for (int q = 0; q < std::min<int>(iters, 64); ++q) st_out->delta_hist[q] = dhist[q];
+      st_out->host_syncs = g_cfg.syncs;
       st_out->wr_iters = iters;
       st_out->wr_last_delta = delta;
       st_out->max_m = max_m;
@@ -1167,6 +1196,7 @@ pexp_status pexp_sai_solve(pexp_ctx* ctx, int32_t b, double gamma, const double*
   return guarded(ctx, [&] {
     init_once();
     Opts o = norm_opts(ctx->opt);
+    g_cfg = o.cfg;
     cudaStream_t st = o.st;
     const int n = (int)ctx->n;
     Arena ar{ctx->ws, ctx->ws_bytes, 0};
@@ -1186,8 +1216,8 @@ pexp_status pexp_sai_solve(pexp_ctx* ctx, int32_t b, double gamma, const double*
     launch_sai_solve(st, L.F, nullptr, 1, ncols, rhs, 0, 0, x, 0, 0, nullptr);
     int herr = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
-    if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: non-positive pivot");
+    host_sync(st);
+    if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: a pivot is zero relative to its row or non-finite");
   });
 }
 
@@ -1203,6 +1233,7 @@ pexp_status pexp_source_svd(pexp_ctx* ctx, const double* G, int32_t E, double to
   return guarded(ctx, [&] {
     init_once();
     Opts o = norm_opts(ctx->opt);
+    g_cfg = o.cfg;
     cudaStream_t st = o.st;
     const int n = (int)ctx->n, s = o.s;
     Arena ar{ctx->ws, ctx->ws_bytes, 0};
@@ -1215,7 +1246,7 @@ pexp_status pexp_source_svd(pexp_ctx* ctx, const double* G, int32_t E, double to
     int mb = std::max(mmax, 1);
     launch_combine(st, E, n, L.S.U, (long long)s * n, 0, mb, L.S.Cfin, (long long)mb * s, mb, proj, (long long)s * n, 0,
                    s, 1.0, 0.0, nullptr);
-    PEXP_CUDA_TRY(cudaStreamSynchronize(st));
+    host_sync(st);
   });
 }
 
@@ -1232,7 +1263,7 @@ pexp_status pexp_expm_batched(pexp_ctx* ctx, const double* A, int32_t E, int32_t
     double* work = ar.take<double>(size_t(nslots) * 7 * N * N);
     int* iwork = ar.take<int>(size_t(nslots) * N);
     launch_expm_batched(o.st, E, N, A, X, work, 7LL * N * N, iwork, nslots);
-    PEXP_CUDA_TRY(cudaStreamSynchronize(o.st));
+    host_sync(o.st);
   });
 }
 

@@ -36,13 +36,10 @@ constexpr int SMALL_MINB = 2;
 constexpr size_t HOM_FS_CAP = HOM_DYN / 8 - 2 * 256;
 constexpr int RING_N = 64;  // pieces whose residual partials are kept (s - 1 <= 63)
 constexpr size_t FS_CAP = SP_DYN / 8 - (2 * KSMALL_MAX + CH_PSUM + KSMALL_MAX + RING_N * MAXS);
-double g_piv_tol = getenv("PEXP_PIVTOL") ? atof(getenv("PEXP_PIVTOL")) : 1e-14;  // developer override
 constexpr size_t SM2 = 2 * MAXS * (MAXS + 1) * sizeof(double);  // two padded 64x64 tiles
 
 // Cluster size so that (evaluations x cluster) fills the 148 SMs (portable maximum 8).
 static int cluster_size_for(int E) {
-  static const int force = getenv("PEXP_CLUSTER") ? atoi(getenv("PEXP_CLUSTER")) : 0;  // developer override
-  if (force > 0) return force;
   int cs = 1;
   while (cs < 8 && E * cs * 2 <= 148 * SMALL_MINB) cs *= 2;
   // (16-CTA clusters measured slower here: E=8, N=208 expm 1.80 ms vs 1.15 ms with 8)
@@ -355,7 +352,7 @@ k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm
 // Correction for deferred columns (class 2) against accepted orthonormal columns (class 1):
 // Mc[a][k] = -Gb[a][k] for a in A, k in D (so that Block += Block * Mc is one CGS step).
 __global__ void k_defer_corr(int N, const double* Gb, long long gs_e, const int* cls, long long cs_e, double* Mc,
-                             const int* active) {
+                             const int* active, int plus_identity) {
   const int e = blockIdx.x;
   if (active && !active[e]) return;
   const int* c = cls + e * cs_e;
@@ -363,14 +360,14 @@ __global__ void k_defer_corr(int N, const double* Gb, long long gs_e, const int*
   double* M = Mc + size_t(e) * N * N;
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
     int a = idx % N, k = idx / N;
-    M[idx] = (c[a] == 1 && c[k] == 2) ? -G[a + size_t(k) * N] : 0.0;
+    M[idx] = ((c[a] == 1 && c[k] == 2) ? -G[a + size_t(k) * N] : 0.0) + (plus_identity && a == k ? 1.0 : 0.0);
   }
 }
 
 void launch_defer_corr(cudaStream_t st, int E, int N, const double* Gb, long long gs_e, const int* cls, long long cs_e,
-                       double* Mc, const int* active) {
+                       double* Mc, const int* active, bool plus_identity) {
   ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
-  k_defer_corr<<<E, 128, 0, st>>>(N, Gb, gs_e, cls, cs_e, Mc, active);
+  k_defer_corr<<<E, 128, 0, st>>>(N, Gb, gs_e, cls, cs_e, Mc, active, plus_identity ? 1 : 0);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }
@@ -1000,7 +997,7 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_hom(SPArgs a
 void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots) {
   if (a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
   if (a.m > 16) fail(1, "grouped legs: at most 16 legs per group");
-  ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * a.K * a.K * a.K));
+  ProfScope ps(PC_SMALLHOM, st, 0.0, eact(a.E, a.active) * (22.0 * a.K * a.K * a.K));
   const int ncl = std::min(a.E, nslots);
   launch_clustered(k_small_hom, ncl, cluster_size_for(ncl), HOM_DYN, st, a);
   count_launch();
@@ -1039,7 +1036,7 @@ void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long
   if (N > MAXS) fail(1, "block width > 64 not supported");
   ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
   k_block_chol<<<E, PEXP_THREADS, SM2, st>>>(N, G, gs_e, ldg, norm0, ns_e, ldn, defl, Rinv, Rprev, rps_e, ldrp,
-                                            Rout, rs_e, ldr, live, ls_e, active, pivoted ? 1 : 0, g_piv_tol, dtol,
+                                            Rout, rs_e, ldr, live, ls_e, active, pivoted ? 1 : 0, g_cfg.piv_tol, dtol,
                                             norm0_out);
   count_launch();
   PEXP_LAUNCH_CHECK();
@@ -1076,7 +1073,7 @@ void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax
   size_t smem = SP_DYN;
   {
   const double N = Dmax + a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
-  ProfScope ps(PC_SMALL, st, 0.0, double(a.E) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
+  ProfScope ps(PC_SMALL, st, 0.0, eact(a.E, a.active) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
   const int ncl = std::min(a.E, nslots);
   launch_clustered(k_small_problem, ncl, cluster_size_for(ncl), smem, st, a);
   }
@@ -1096,10 +1093,6 @@ void small_init() {
   cudaFuncSetAttribute(k_small_problem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_small_hom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_expm_batched, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (getenv("PEXP_NODMMA")) {
-    const int zero = 0;
-    cudaMemcpyToSymbol(g_gemm_dmma, &zero, sizeof(int));
-  }
   cudaFuncSetAttribute(k_sym_eig_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_block_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);
   cudaFuncSetAttribute(k_onesided_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM2);

@@ -242,9 +242,12 @@ __global__ void k_hom_setup(int E, int mode, int P, int s, double h, double eta,
   }
 }
 
-__global__ void k_update_active(int E, const int* conv, int* active, int* count) {
+__global__ void k_update_active(int E, const int* conv, int* active, int* count, int* krec, int kval) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-    if (active[e] && conv[e]) active[e] = 0;
+    if (active[e] && conv[e]) {
+      active[e] = 0;
+      if (krec) krec[e] = kval;  // total Krylov dimension at convergence (pexp_stats.k_j)
+    }
     if (active[e]) atomicAdd(count, 1);
   }
 }
@@ -446,10 +449,10 @@ void launch_hom_setup(cudaStream_t st, int E, int mode, int P, int s, double h, 
   PEXP_LAUNCH_CHECK();
 }
 
-void launch_update_active(cudaStream_t st, int E, const int* conv, int* active, int* count) {
+void launch_update_active(cudaStream_t st, int E, const int* conv, int* active, int* count, int* krec, int kval) {
   if (E == 0) return;
   { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
-  k_update_active<<<std::min(cdiv(E, PEXP_THREADS), 256), PEXP_THREADS, 0, st>>>(E, conv, active, count);
+  k_update_active<<<std::min(cdiv(E, PEXP_THREADS), 256), PEXP_THREADS, 0, st>>>(E, conv, active, count, krec, kval);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();

@@ -234,8 +234,9 @@ void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E,
                       int cout0, const int* active) {
   if (E == 0 || ncols == 0) return;
   // algorithmic: read rhs + write x per column, factors once per distinct factor (<= E)
-  ProfScope ps(PC_SOLVE, st, double(E) * ncols * F.n * 16.0 + double(std::min(E, F.nf)) * F.n * 8.0 * (F.periodic ? 5 : 3),
-               double(E) * ncols * F.n * (F.periodic ? 8.0 : 6.0));
+  const double ea = eact(E, active);
+  ProfScope ps(PC_SOLVE, st, ea * ncols * F.n * 16.0 + std::min(ea, double(F.nf)) * F.n * 8.0 * (F.periodic ? 5 : 3),
+               ea * ncols * F.n * (F.periodic ? 8.0 : 6.0));
   dim3 grid(ncols, E);
   k_sai_solve<<<grid, PEXP_THREADS, 0, st>>>(F.n, F.periodic, fidx, F.l, F.dinv, F.sup, F.z, F.w,
                                               rhs, rs_e, cin0, out, os_e, cout0, active);

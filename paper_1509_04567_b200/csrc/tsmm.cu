@@ -457,13 +457,12 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
                 const int* active, int* cnt) {
   if (E == 0 || nx == 0 || ny == 0) return;
   RedArgs ra{D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, cnt};
-  static const bool nomma = getenv("PEXP_NOXTYMMA") != nullptr;  // developer switch
-  if (!nomma && ny > 8 && ny <= 32 && nx >= 32) {
+  if (ny > 8 && ny <= 32 && nx >= 32) {
     const int rch = xty_chunks(n, E * cdiv(nx, 64));
     const int nch = cdiv(n, rch);
     if (size_t(E) * nch * nx * ny > part_cap) fail(2, "xty partial buffer too small");
     const bool same = (X == Y && xs_e == ys_e && y0 >= x0 && y0 + ny <= x0 + nx);
-    ProfScope ps(PC_XTY, st, double(E) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * E * double(n) * nx * ny);
+    ProfScope ps(PC_XTY, st, eact(E, active) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * eact(E, active) * double(n) * nx * ny);
     dim3 grid(nch, cdiv(nx, 64), E);
     if (ny <= 16)
       k_xty_mma<16><<<grid, PEXP_THREADS, 0, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part, active);
@@ -482,7 +481,7 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
     xty_tall_plan(n, E, nx, ny, rsub, rch, nch);
     if (size_t(E) * nch * nx * ny > part_cap) fail(2, "xty partial buffer too small");
     const bool same = (X == Y && xs_e == ys_e && y0 >= x0 && y0 + ny <= x0 + nx);
-    ProfScope ps(PC_XTY, st, double(E) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * E * double(n) * nx * ny);
+    ProfScope ps(PC_XTY, st, eact(E, active) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * eact(E, active) * double(n) * nx * ny);
     size_t smem = (size_t(rsub) * ny + size_t(nx) * ny) * sizeof(double);
     if (smem > 200 * 1024) fail(1, "xty: nx*ny too large for the tall path");
     dim3 grid(nch, E);
@@ -511,7 +510,7 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
   int ntiles = (nxp / RA) * (nyp / RB);
   size_t smem = size_t(TR) * (nxp + nyp) * sizeof(double);
   const bool same = (X == Y && xs_e == ys_e && y0 >= x0 && y0 + ny <= x0 + nx);
-  ProfScope ps(PC_XTY, st, double(E) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * E * double(n) * nx * ny);
+  ProfScope ps(PC_XTY, st, eact(E, active) * n * 8.0 * (nx + (same ? 0 : ny)), 2.0 * eact(E, active) * double(n) * nx * ny);
   dim3 grid(nch, E);
   if (nx > 32 && ny > 32 && nx <= 64 && ny <= 64) {
     k_xty_sq<<<grid, PEXP_THREADS, 0, st>>>(n, rch, X, xs_e, x0, nx, Y, ys_e, y0, ny, part);
@@ -547,7 +546,8 @@ void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs
       fail(1, "combine: in-place product with more than 32 output columns");
     const int nbt = nb <= 4 ? 4 : nb <= 8 ? 8 : nb <= 16 ? 16 : 32;
     size_t smem = size_t(std::max(nx, 1)) * nbt * sizeof(double);
-    ProfScope ps(PC_COMBINE, st, double(E) * n * 8.0 * (nx + nb * (beta != 0.0 ? 2 : 1)), 2.0 * E * double(n) * nx * nb);
+    ProfScope ps(PC_COMBINE, st, eact(E, active) * n * 8.0 * (nx + nb * (beta != 0.0 ? 2 : 1)),
+                 2.0 * eact(E, active) * double(n) * nx * nb);
     dim3 grid(cdiv(n, 2 * PEXP_THREADS), E);
     const double* Mb = M + size_t(b0) * ldm;
     if (nbt == 4)

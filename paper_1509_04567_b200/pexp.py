@@ -27,23 +27,36 @@ EXPORTED = ["pexp_create", "pexp_create_batched", "pexp_destroy", "pexp_last_err
             "pexp_workspace_bytes", "pexp_set_workspace", "pexp_solve_linear", "pexp_solve_burgers",
             "pexp_sai_solve", "pexp_source_svd", "pexp_expm_batched", "pexp_profile_enable", "pexp_profile_read"]
 PROFILE_CLASSES = ["sai_solve", "xty", "combine", "small_problem", "small_dense", "stencil", "factor",
-                   "arnoldi_step", "hom_scan"]
+                   "arnoldi_step", "hom_scan", "small_hom"]
 
 
 class Options(C.Structure):
     _fields_ = [("s", C.c_int32), ("node_rule", C.c_int32), ("svd_tau_factor", C.c_double),
                 ("stop_factor", C.c_double), ("restart_blocks", C.c_int32), ("k_max", C.c_int32),
                 ("stream", C.c_void_p), ("stop_rule", C.c_int32), ("basis_cols", C.c_int32),
-                ("eval_chunk", C.c_int32)]
+                ("eval_chunk", C.c_int32), ("route", C.c_int32), ("defl_tol", C.c_double),
+                ("piv_tol", C.c_double), ("hom_group", C.c_int32)]
 
 
 class Stats(C.Structure):
     _fields_ = [("wr_iters", C.c_int32), ("wr_last_delta", C.c_double), ("max_m", C.c_int32),
                 ("max_k", C.c_int32), ("restarts", C.c_int32), ("best_residual", C.c_double),
-                ("ms_total", C.c_float), ("evals", C.c_int32), ("kernel_launches", C.c_int32)]
+                ("ms_total", C.c_float), ("evals", C.c_int32), ("kernel_launches", C.c_int32),
+                ("host_syncs", C.c_int32), ("delta_hist", C.c_double * 64),
+                ("m_j", C.POINTER(C.c_int32)), ("k_j", C.POINTER(C.c_int32)), ("gamma_j", C.POINTER(C.c_double))]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("delta_hist", "m_j", "k_j", "gamma_j")}
+        d["delta_hist"] = list(self.delta_hist[:min(max(self.wr_iters, 0), 64)])
+        return d
+
+
+def _records(nrec: int):
+    """Caller-owned host arrays for the per-evaluation records of pexp_stats."""
+    m = (C.c_int32 * nrec)()
+    k = (C.c_int32 * nrec)()
+    g = (C.c_double * nrec)()
+    return m, k, g
 
 
 _P = C.c_void_p
@@ -93,7 +106,8 @@ class Context:
     def __init__(self, n: int, bc: str = "periodic", nu=1e-2, a=0.0, *, s: int = 32, k_max: int = 256,
                  svd_tau_factor: float = 0.01, stop_factor: float = 0.1, restart_blocks: int = 20,
                  stream: Optional[torch.cuda.Stream] = None, stop_rule: int = 0, basis_cols: int = 0,
-                 eval_chunk: int = 0):
+                 eval_chunk: int = 0, route: int = 0, defl_tol: float = 0.0, piv_tol: float = 0.0,
+                 hom_group: int = 0):
         self.n, self.bc, self.s = int(n), bc, int(s)
         self._stream = stream
         nu = [float(v) for v in (nu if hasattr(nu, "__len__") else [nu])]
@@ -103,7 +117,7 @@ class Context:
         self.batch = len(nu)
         handle = stream.cuda_stream if stream is not None else None  # None = legacy default stream
         self.opt = Options(self.s, 0, svd_tau_factor, stop_factor, restart_blocks, k_max, handle, stop_rule,
-                           basis_cols, eval_chunk)
+                           basis_cols, eval_chunk, route, defl_tol, piv_tol, hom_group)
         self._h = _P()
         arr = C.c_double * self.batch
         st = _lib.pexp_create_batched(C.byref(self._h), self.n, BC[bc], self.batch, arr(*nu), arr(*a),
@@ -140,24 +154,41 @@ class Context:
         return t.view(P, self.s)
 
     def solve_linear(self, u0: torch.Tensor, src: torch.Tensor, T: float, P: int, tol: float,
-                     out: Optional[torch.Tensor] = None):
+                     out: Optional[torch.Tensor] = None, records: bool = False):
         self.ensure_workspace(P, u0.device)
         if out is None:
             out = torch.empty((self.batch, P, self.n), dtype=torch.float64, device=u0.device)
         st = Stats()
+        if records:
+            rm, rk, rg = _records(self.batch * P)
+            st.m_j, st.k_j, st.gamma_j = (C.cast(rm, C.POINTER(C.c_int32)), C.cast(rk, C.POINTER(C.c_int32)),
+                                           C.cast(rg, C.POINTER(C.c_double)))
         self._check(_lib.pexp_solve_linear(self._h, _dev(u0, "u0"), _dev(src, "src"), float(T), int(P), float(tol),
                                            _dev(out, "out"), C.byref(st)))
-        return out, st.as_dict()
+        d = st.as_dict()
+        if records:
+            d["m_j"], d["k_j"], d["gamma_j"] = list(rm), list(rk), list(rg)
+        return out, d
 
     def solve_burgers(self, u0: torch.Tensor, nu: float, T: float, P: int, tol: float, max_wr_iters: int = 30,
-                      out: Optional[torch.Tensor] = None):
+                      out: Optional[torch.Tensor] = None, records: bool = False):
         self.ensure_workspace(P, u0.device, kind=1)
         if out is None:
             out = torch.empty((P, self.n), dtype=torch.float64, device=u0.device)
         st = Stats()
+        if records:
+            rm, rk, rg = _records(int(max_wr_iters) * P)
+            st.m_j, st.k_j, st.gamma_j = (C.cast(rm, C.POINTER(C.c_int32)), C.cast(rk, C.POINTER(C.c_int32)),
+                                           C.cast(rg, C.POINTER(C.c_double)))
         self._check(_lib.pexp_solve_burgers(self._h, _dev(u0, "u0"), float(nu), float(T), int(P), float(tol),
                                             int(max_wr_iters), _dev(out, "out"), C.byref(st)))
-        return out, st.as_dict()
+        d = st.as_dict()
+        if records:
+            K = d["wr_iters"]
+            d["m_j"] = [list(rm[k * P:(k + 1) * P]) for k in range(K)]
+            d["k_j"] = [list(rk[k * P:(k + 1) * P]) for k in range(K)]
+            d["gamma_j"] = [list(rg[k * P:(k + 1) * P]) for k in range(K)]
+        return out, d
 
     def sai_solve(self, b: int, gamma: float, rhs: torch.Tensor) -> torch.Tensor:
         self.ensure_workspace(1, rhs.device)

@@ -86,3 +86,41 @@ def test_workspace_query_and_solve_without_workspace(P):
     assert st == P.PEXP_EINVAL
     st = lib.pexp_solve_burgers(d._h, 1, 1e-2, 1.0, 4, 1e-8, 30, 1, None)
     assert st == P.PEXP_EINVAL and b"periodic" in lib.pexp_last_error(d._h)
+
+
+def test_struct_layout_matches_header(P, tmp_path):
+    """The ctypes mirrors of pexp_options / pexp_stats have the C compiler's layout."""
+    import subprocess
+    fields_o = [f for f, _ in P.Options._fields_]
+    fields_s = [f for f, _ in P.Stats._fields_]
+    src = tmp_path / "layout.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pexp.h"', "int main(void) {",
+             'printf("%zu %zu\\n", sizeof(pexp_options), sizeof(pexp_stats));']
+    lines += [f'printf("%zu\\n", offsetof(pexp_options, {f}));' for f in fields_o]
+    lines += [f'printf("%zu\\n", offsetof(pexp_stats, {f}));' for f in fields_s]
+    lines += ["return 0; }"]
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert vals[0] == C.sizeof(P.Options) and vals[1] == C.sizeof(P.Stats)
+    offs = vals[2:]
+    assert offs[:len(fields_o)] == [getattr(P.Options, f).offset for f in fields_o]
+    assert offs[len(fields_o):] == [getattr(P.Stats, f).offset for f in fields_s]
+
+
+def test_option_validation(P):
+    for kw in ({"route": 3}, {"route": -1}, {"hom_group": 17}, {"defl_tol": -1.0}, {"piv_tol": -1.0}):
+        with pytest.raises(P.PexpError):
+            P.Context(64, "periodic", 1e-2, 1.0, **kw)
+    P.Context(64, "periodic", 1e-2, 1.0, route=1, hom_group=16, defl_tol=1e-9, piv_tol=1e-13)
+
+
+def test_no_environment_knobs_in_library(root):
+    """Numerics and routing come from pexp_options only (SURVEY §5 'no env-var magic'); the one
+    environment read left is the PEXP_SYNC fault-localisation switch (no numerical effect)."""
+    csrc = os.path.join(root, "paper_1509_04567_b200", "csrc")
+    reads = []
+    for f in os.listdir(csrc):
+        reads += re.findall(r'getenv\("(\w+)"\)', open(os.path.join(csrc, f)).read())
+    assert reads == ["PEXP_SYNC"], reads

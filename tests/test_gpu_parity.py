@@ -110,9 +110,9 @@ def test_expm_batched_vs_scipy():
 
 # ---------------------------------------------------------------- linear Paraexp-EBK solves
 
-def _linear(p, k_max=256, **kw):
+def _linear(p, k_max=256, records=False, **kw):
     c = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=p.s, k_max=k_max, **kw)
-    out, st = c.solve_linear(t(p.u0), t(p.src), p.T, p.P, p.tol)
+    out, st = c.solve_linear(t(p.u0), t(p.src), p.T, p.P, p.tol, records=records)
     return out.cpu().numpy(), st
 
 
@@ -120,27 +120,33 @@ def _oracle_linear(p, **kw):
     return oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol, **kw)
 
 
-def test_linear_config1_full():
+ROUTES = [0, 1]  # pexp_options.route: 0 auto (fused cluster step where it fits), 1 streaming route
+
+
+@pytest.mark.parametrize("route", ROUTES)
+def test_linear_config1_full(route):
     p = synth.config1()
-    out, st = _linear(p)
+    out, st = _linear(p, route=route)
     ref = _oracle_linear(p)
     assert rel(out, ref) < 1e-8, st
     assert st["max_m"] == 4
 
 
+@pytest.mark.parametrize("route", ROUTES)
 @pytest.mark.parametrize("bc,n,nu,a", [("periodic", 777, 5e-3, 1.3), ("dirichlet", 600, 1e-3, 1.0)])
-def test_linear_generic_deep_arnoldi(bc, n, nu, a):
+def test_linear_generic_deep_arnoldi(bc, n, nu, a, route):
     """Non-Fourier data: the Krylov space is not invariant; deep Arnoldi, ragged n."""
     p = synth.generic_linear(n=n, bc=bc, nu=nu, a=a, P=5, s=12, T=0.5, seed=7)
-    out, st = _linear(p)
+    out, st = _linear(p, route=route)
     ref = _oracle_linear(p)
     assert rel(out, ref) < 1e-8, st
     assert st["max_k"] > 20
 
 
-def test_linear_config2_reduced():
+@pytest.mark.parametrize("route", ROUTES)
+def test_linear_config2_reduced(route):
     p = synth.config2(n=1200, P=16, T=0.25, s=64)     # same subinterval length dT = 1/64 as C2
-    out, st = _linear(p, k_max=384)
+    out, st = _linear(p, k_max=384, route=route)
     ref = _oracle_linear(p)
     assert rel(out, ref) < 1e-8, st
 
@@ -165,12 +171,13 @@ def test_linear_config4_full_batch_sampled():
         assert rel(out[b], ref[0]) < 1e-8, (b, st)
 
 
+@pytest.mark.parametrize("route", ROUTES)
 @pytest.mark.parametrize("restart_blocks,basis_cols", [(3, 0), (-1, 40), (20, 0)])
-def test_linear_restart_nested_exact(restart_blocks, basis_cols):
+def test_linear_restart_nested_exact(restart_blocks, basis_cols, route):
     """Exact nested restart (DESIGN.md §3 #5): the cycle residual becomes the next cycle's
     source; the result must match the unrestarted oracle to the same 1e-8."""
     p = synth.generic_linear(n=777, bc="periodic", nu=5e-3, a=1.3, P=5, s=12, T=0.5, seed=7)
-    out, st = _linear(p, k_max=512, restart_blocks=restart_blocks, basis_cols=basis_cols)
+    out, st = _linear(p, k_max=512, restart_blocks=restart_blocks, basis_cols=basis_cols, route=route)
     ref = _oracle_linear(p)
     assert rel(out, ref) < 1e-8, st
     if restart_blocks != 20:
@@ -206,48 +213,109 @@ def test_linear_P1_and_unforced_and_zero():
     assert torch.count_nonzero(z).item() == 0
 
 
-def test_linear_config2_full_size_sampled():
-    """C2 at its full size in the bench's launch configuration; the oracle computes the first
-    two outputs u(T_1), u(T_2) (which depend only on subintervals 1-2)."""
+def _golden(name):
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)
+    if not os.path.exists(path):
+        pytest.fail(f"stored oracle reference {name} missing: run scripts/gen_oracle_refs.py")
+    return np.load(path)
+
+
+def test_linear_config2_full_size_all_outputs():
+    """C2 at its full size (BASELINE configs[1]) in the bench's launch configuration: all 64
+    outputs u(T_1..T_64) (every nonhomogeneous evaluation and all 8 homogeneous leg groups)
+    against the stored oracle reference (tests/golden/c2full_oracle.npz, written by
+    scripts/gen_oracle_refs.py, which calls only oracle/)."""
     p = synth.config2()
-    out, st = _linear(p, k_max=384)
-    ref = _oracle_linear(p, i_max=2)
-    assert rel(out[0, :2], ref[0]) < 1e-8, st
-    assert np.all(np.isfinite(out))
+    out, st = _linear(p, k_max=384, records=True)
+    ref = _golden("c2full_oracle.npz")
+    assert rel(out, ref["out"]) < 1e-8, st
+    for i in range(p.P):   # every output on its own, incl. the late legs of the last group
+        assert rel(out[0, i], ref["out"][0, i]) < 1e-8, i
+    assert st["m_j"] == ref["m"][0].tolist()     # retained ranks m_j equal the oracle's
+
+
+@pytest.mark.parametrize("route", ROUTES)
+@pytest.mark.parametrize("s,n,P,restart_blocks", [(20, 700, 4, 0), (20, 700, 4, 3), (40, 900, 3, 0)])
+def test_linear_wide_blocks(s, n, P, restart_blocks, route):
+    """Block widths 8 < m <= 32 and m > 32 (a rough 1e-6-noise source keeps every sample:
+    m = s): the DMMA projections, the deferred-column in-block QR at m > 32 and nested restarts
+    at wide blocks, on both Arnoldi routes."""
+    p = synth.generic_linear(n=n, bc="periodic", nu=5e-3, a=1.3, P=P, s=s, T=0.5, seed=7, rank=3, noise=1e-6)
+    out, st = _linear(p, k_max=640, restart_blocks=restart_blocks, route=route, records=True)
+    ref, info = _oracle_linear(p, dense_max=0, return_info=True)
+    assert st["m_j"] == info["m"][0].tolist() == [s] * P
+    assert rel(out, ref) < 1e-8, st
+    if restart_blocks == 3:
+        assert st["restarts"] >= 1, st
 
 
 # ---------------------------------------------------------------- Burgers WR
 
-def _burgers(p, k_max=256, **kw):
+def _burgers(p, k_max=256, records=False, **kw):
     c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=k_max, **kw)
-    out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters)
+    out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters, records=records)
     return out.cpu().numpy(), st
 
 
-def test_burgers_small():
+@pytest.mark.parametrize("route", ROUTES)
+def test_burgers_small(route):
     p = synth.config3(n=256, P=4, s=12, T=0.2, nu=0.02)
-    out, st = _burgers(p)
+    out, st = _burgers(p, route=route)
     ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
     assert abs(out.sum(axis=1) - p.u0.sum()).max() < 1e-9 * np.abs(p.u0).sum()
 
 
-def test_burgers_config3_full():
+@pytest.mark.parametrize("route", ROUTES)
+def test_burgers_config3_full(route):
     p = synth.config3()
-    out, st = _burgers(p)
+    out, st = _burgers(p, route=route)
     ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
 
 
-def test_burgers_small_restarted():
+@pytest.mark.parametrize("route", ROUTES)
+def test_burgers_small_restarted(route):
     p = synth.config3(n=256, P=4, s=12, T=0.2, nu=0.02)
-    out, st = _burgers(p, k_max=512, restart_blocks=-1, basis_cols=40)
+    out, st = _burgers(p, k_max=512, restart_blocks=-1, basis_cols=40, route=route)
     ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
     assert st["restarts"] >= 1, st
+
+
+@pytest.mark.parametrize("route", ROUTES)
+def test_burgers_c5proxy_to_convergence(route):
+    """C5-shaped WR run to convergence (SURVEY §8(d).2 C5 generator at n = 8192, ν = 1e-3,
+    s = 64, ΔT = 1/256, T = 0.25): the steep front forms, block widths reach ~25 and the
+    per-subinterval Jacobians differ, i.e. the iterations the C5 first-iterate check cannot
+    see.  Reference: the oracle to convergence (tests/golden/c5proxy_oracle.npz, written by
+    scripts/gen_oracle_refs.py); equal WR iteration counts and equal retained ranks m_j in
+    every iteration."""
+    p = synth.config5(n=8192, P=64, T=0.25)
+    ref = _golden("c5proxy_oracle.npz")
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=960, route=route)
+    out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters, records=True)
+    out = out.cpu().numpy()
+    assert st["wr_iters"] == int(ref["iters"]), (st["delta_hist"], ref["delta"])
+    assert rel(out, ref["out"]) < 1e-8, st
+    K = st["wr_iters"]
+    assert np.array(st["m_j"]).tolist() == ref["m"][:K].tolist()
+    assert np.abs(out.sum(axis=1) - p.u0.sum()).max() < 1e-9 * np.abs(p.u0).sum()
+
+
+def test_stats_records_linear():
+    """pexp_stats per-evaluation records: m_j equal the oracle's ranks, k_j > 0, gamma_j = ΔT/10."""
+    p = synth.config2(n=1200, P=16, T=0.25, s=64)
+    out, st = _linear(p, k_max=384, records=True)
+    ref, info = _oracle_linear(p, return_info=True)
+    assert st["m_j"] == info["m"][0].tolist()
+    assert min(st["k_j"]) > 0 and max(st["k_j"]) <= st["max_k"]
+    assert np.allclose(st["gamma_j"], p.T / p.P / 10)
+    assert st["host_syncs"] >= 1
 
 
 def test_burgers_small_chunked():

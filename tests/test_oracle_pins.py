@@ -317,13 +317,16 @@ def test_paraexp_krylov_equals_dense_dirichlet():
 
 # ---------------------------------------------------------------- waveform relaxation
 
-def test_wr_first_iterate_closed_form():
+@pytest.mark.parametrize("dense_max", [1024, 0])
+def test_wr_first_iterate_closed_form(dense_max):
     """u_0 ≡ u0 ⇒ ū_j = u0, one operator B = νD2 + J(u0), constant source c = νD2u0 - u0∘D1u0
-    ⇒ u_1(t) = u0 + t φ1(tB) c (SURVEY §8(c).4 'WR iteration 1')."""
+    ⇒ u_1(t) = u0 + t φ1(tB) c (SURVEY §8(c).4 'WR iteration 1').  dense_max = 0 forces the
+    Krylov branch of wr_map (the one the n > 1024 parity references use) for the nonhomogeneous
+    legs and the scan."""
     from scipy.linalg import expm
     p = synth.config3(n=96, P=3, s=7, T=0.15, nu=0.03)
     U0 = np.broadcast_to(p.u0, (p.P, p.s, p.n)).copy()
-    U1 = wr_map(U0, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol)
+    U1 = wr_map(U0, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol, dense_max=dense_max)
     B = (p.nu * d2_matrix(p.n) + burgers_J(p.u0, p.n)).toarray()
     c = p.nu * (d2_matrix(p.n) @ p.u0) - p.u0 * (d1_matrix(p.n) @ p.u0)
     t = synth.node_times(p.T, p.P, p.s)
@@ -334,22 +337,24 @@ def test_wr_first_iterate_closed_form():
             assert np.linalg.norm(U1[j, i] - ex) <= 1e-10 * np.linalg.norm(ex), (j, i)
 
 
-def test_wr_mass_conserved_every_iterate():
+@pytest.mark.parametrize("dense_max", [1024, 0])
+def test_wr_mass_conserved_every_iterate(dense_max):
     p = synth.config3(n=128, P=4, s=8, T=0.2, nu=0.02)
     U = np.broadcast_to(p.u0, (p.P, p.s, p.n)).copy()
     m0 = p.u0.sum()
     for _ in range(3):
-        U = wr_map(U, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol)
+        U = wr_map(U, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol, dense_max=dense_max)
         assert np.max(np.abs(U.sum(axis=2) - m0)) <= 1e-9 * np.abs(p.u0).sum()
 
 
-def test_wr_fixed_point_vs_bruteforce_radau():
+@pytest.mark.parametrize("dense_max", [1024, 0])
+def test_wr_fixed_point_vs_bruteforce_radau(dense_max):
     """Tiny grid: the converged WR iterate vs an independent implicit integrator (Radau) on the
     full semi-discrete Burgers u' = νD2u - u∘D1u; agreement at the level of the
-    source-interpolation error."""
+    source-interpolation error.  dense_max = 0: the SaI Krylov branch and the Krylov scan."""
     p = synth.config3(n=32, P=4, s=16, T=0.2, nu=0.05)
     out, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, wr_tol=1e-13,
-                                     max_wr_iters=40, return_info=True)
+                                     max_wr_iters=40, return_info=True, dense_max=dense_max)
     D1, D2 = d1_matrix(p.n).toarray(), d2_matrix(p.n).toarray()
     f = lambda t, u: p.nu * D2 @ u - u * (D1 @ u)
     Tj = np.arange(1, p.P + 1) * p.T / p.P
@@ -359,10 +364,11 @@ def test_wr_fixed_point_vs_bruteforce_radau():
     assert err < 1e-7, err
 
 
-def test_wr_P1_vs_P4_same_solution():
+@pytest.mark.parametrize("dense_max", [1024, 0])
+def test_wr_P1_vs_P4_same_solution(dense_max):
     p = synth.config3(n=64, P=1, s=24, T=0.1, nu=0.05)
-    o1 = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, 1, 24, p.tol, wr_tol=1e-12)
-    o4 = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, 4, 8, p.tol, wr_tol=1e-12)
+    o1 = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, 1, 24, p.tol, wr_tol=1e-12, dense_max=dense_max)
+    o4 = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, 4, 8, p.tol, wr_tol=1e-12, dense_max=dense_max)
     assert np.linalg.norm(o1[-1] - o4[-1]) <= 1e-7 * np.linalg.norm(o1[-1])
 
 
@@ -373,3 +379,20 @@ def test_trapezoid_mean_exact_for_linear_in_time():
     tt = np.linspace(0, 1, s)
     U = a[None] + tt[:, None] * b[None]
     np.testing.assert_allclose(trapezoid_mean(U), a + 0.5 * b, rtol=1e-14)
+
+
+def test_wr_krylov_branch_equals_dense_branch_steep():
+    """The two branches of wr_map on a steep-front case (ν = 2e-3, n = 128, several iterations,
+    block widths > 1 and per-subinterval Jacobians that differ): the Krylov branch (SaI block
+    Arnoldi + Krylov scan, used by every n > 1024 parity reference) equals the dense-expm
+    branch (the definition) to the Krylov stop tolerance."""
+    p = synth.config5(n=128, P=4, s=16, T=0.2, nu=2e-3)
+    U = np.broadcast_to(p.u0, (p.P, p.s, p.n)).copy()
+    for k in range(4):
+        info_d, info_k = {}, {}
+        Ud = wr_map(U, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol, info=info_d)
+        Uk = wr_map(U, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol, dense_max=0, info=info_k)
+        assert info_d["m"] == info_k["m"]
+        assert np.linalg.norm(Ud - Uk) <= 1e-10 * np.linalg.norm(Ud), k
+        U = Ud
+    assert max(info_d["m"]) > 1
