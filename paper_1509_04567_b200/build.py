@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpexp.so")
-SOURCES = ["tridiag.cu", "tsmm.cu", "small.cu", "stencil.cu", "arnoldi.cu", "hom_scan.cu", "pexp_api.cu"]
+SOURCES = ["tridiag.cu", "tsmm.cu", "small.cu", "stencil.cu", "arnoldi.cu", "hom_scan.cu", "stream.cu", "pexp_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

@@ -102,6 +102,8 @@ struct EbkBufs {
   double* part;
   size_t part_cap;
   double* stepws = nullptr;  // fused Arnoldi step: global V^T W partials (large bases)
+  double* spart = nullptr;   // streaming route: per-chunk partials of [V W]^T W
+  size_t spart_cap = 0;
   double* work;
   int* iwork;
   int nslots, Nmax;
@@ -173,6 +175,10 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   {
     const size_t sw = arnoldi_scratch_doubles(Ec, kcap, mcap);
     B.stepws = sw ? ar.take<double>(sw) : nullptr;
+  }
+  if (stream_ok(n, std::min(mcap, 32))) {
+    B.spart_cap = stream_part_doubles(Ec, n, kcap, std::min(mcap, 32));
+    B.spart = ar.take<double>(B.spart_cap);
   }
   B.Nmax = ktot + (forced ? 4 * mcap : 0);
   B.work_slot = 10LL * B.Nmax * B.Nmax;
@@ -430,6 +436,25 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       sa.W0 = B.Wt; sa.w0s_e = (long long)m * n; sa.active = B.active; sa.defl = defl;
       sa.hs_g = B.stepws;
       launch_arnoldi_step(st, sa);
+    } else if (B.spart && m <= 32) {  // streaming route: TMA-fed DMMA products (stream.cu)
+    launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
+    PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.Wt, size_t(m) * n * sizeof(double), B.V + size_t(nv) * n,
+                                    ws_e * sizeof(double), size_t(m) * n * sizeof(double), E,
+                                    cudaMemcpyDeviceToDevice, st));
+    // BCGS pass 1: H[0:nv, block b] = V^T W0 and the W0 Gram (deflation reference) in one pass
+    launch_sproj(st, E, n, B.V, ws_e, nv, B.V + size_t(nv) * n, ws_e, m, B.spart, B.spart_cap, B.H, B.hs_e, kcap, 0,
+                 b * m, false, B.G0, (long long)m * m, B.active);
+    launch_supdate(st, E, n, B.V, ws_e, nv, B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.V + size_t(nv) * n, ws_e, m,
+                   -1.0, 1.0, B.active);
+    inblock_qr(st, B, E, n, m, nv, B.G0, (long long)m * m, m, defl, B.active);
+    // BCGS pass 2 + CholQR
+    launch_sproj(st, E, n, B.V, ws_e, nv, B.V + size_t(nv) * n, ws_e, m, B.spart, B.spart_cap, B.T,
+                 (long long)kcap * B.mcap, nv, 0, 0, false, nullptr, 0, B.active);
+    launch_supdate(st, E, n, B.V, ws_e, nv, B.T, (long long)kcap * B.mcap, nv, B.V + size_t(nv) * n, ws_e, m, -1.0,
+                   1.0, B.active);
+    chol_combine_block(st, B, E, n, m, nv, nullptr, 0, 0, 0.0, defl, nullptr, B.active);
+    launch_xty(st, E, n, B.V, ws_e, nv, m, B.Wt, (long long)m * n, 0, m, B.part, B.part_cap, B.H, B.hs_e, kcap, nv,
+               b * m, false, B.active, B.xcnt);
     } else {
     // W = (I - gamma A)^{-1} V_b  -> columns [nv, nv+m)
     launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
@@ -833,6 +858,7 @@ static void init_once() {
   if (!(done & bit)) {
     tsmm_init();
     small_init();
+    stream_init();
     done |= bit;
   }
 }

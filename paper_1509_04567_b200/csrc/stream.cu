@@ -1,0 +1,430 @@
+// stream.cu — the streaming route's tall-skinny products (subsystem 2, block classical
+// Gram-Schmidt with reorthogonalisation, PAPER.md:171-176 Eq.(blockKrylovSubspace)) for long
+// columns (C5: n = 65536), where the fused cluster step's block rows do not fit on chip:
+//
+//   k_sproj   : D = X^T Y  and  G = Y^T Y   (X = the basis V[:, 0:nx], Y = the new block, ny <= 32)
+//   k_supdate : Y = beta Y + alpha X M       (M: nx x ny, e.g. W -= V H)
+//
+// Both are persistent, warp-specialised kernels: one producer warp streams the CTA's row chunk of
+// X through a ring of shared-memory stages with 1D bulk TMA copies (cp.async.bulk, completion on
+// mbarriers: UBLKCP in SASS), eight consumer warps run the contraction on the fp64 tensor cores
+// (DMMA m8n8k4).  A stage holds 8 columns of X for R = 512 rows (each column one 4 KB bulk copy,
+// column stride padded by 32 B so a fragment load is exactly two shared-memory wavefronts).
+//
+// k_sproj: consumer warp w owns rows [64w, 64w + 64) of the chunk and keeps its Y rows as DMMA B
+// fragments in registers for the whole item; per stage it accumulates the 8 x ny tile of X^T Y over
+// its rows, the 8 warps' tiles are summed through shared memory in warp order and written as the
+// chunk's partial; G = Y^T Y uses the same registers as A and B operands.  Partials are summed in
+// chunk order by k_sred (deterministic, parallel over outputs).
+// k_supdate: consumer warp w owns the same 64 rows; its D fragments (64 rows x ny) stay in
+// registers across all stages (the sum over X's columns is the DMMA k-dimension), B fragments are
+// the matching 8 rows of M per stage (L1/L2 resident), the epilogue writes beta Y + alpha acc.
+//
+// Requirements (checked by stream_ok): n even (16-byte aligned column starts for the bulk copies),
+// ny <= 32.  Algorithmic bytes: X read once per launch (8 n nx), Y read once (and written once by
+// k_supdate); DMMA flops 2 n nx ny (+ 2 n ny^2 for G).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pexp {
+
+namespace {
+
+constexpr int SR = 512;                 // rows per work item (chunk)
+constexpr int SCOLS = 8;                // X columns per stage
+constexpr int SNW = 8;                  // consumer warps
+constexpr int STHREADS = (SNW + 1) * 32;
+constexpr int SNST = 4;                 // ring stages
+constexpr int SCOL_STRIDE = SR + 4;     // doubles per staged column (32 B pad)
+constexpr int SSTAGE = SCOLS * SCOL_STRIDE;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(SNW * 32) : "memory"); }
+
+struct Item {
+  int e, c;  // evaluation, row chunk
+};
+
+// Work items (e, c) with active[e] != 0, enumerated identically by producer and consumers.
+__device__ __forceinline__ bool next_item(int& it, int nitems, int nch, const int* active, Item& w) {
+  while (it < nitems) {
+    const int e = it / nch, c = it % nch;
+    if (!active || active[e]) {
+      w.e = e;
+      w.c = c;
+      return true;
+    }
+    it += gridDim.x;
+  }
+  return false;
+}
+
+// Producer: stream X[:, 0:nx] rows [c*SR, c*SR + rows) of every item, 8 columns per stage.
+__device__ void produce(const double* X, long long xs_e, int n, int nx, int nitems, int nch, const int* active,
+                        double* ring, unsigned long long* full, unsigned long long* empty) {
+  if ((threadIdx.x & 31) != 0) return;
+  int slot = 0;
+  unsigned ph = 0;
+  Item w;
+  for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
+    const int r0 = w.c * SR, rows = min(SR, n - r0);
+    const unsigned bytes = unsigned(rows) * 8u;
+    const double* Xe = X + w.e * xs_e + r0;
+    for (int g = 0; g < nx; g += SCOLS) {
+      const int nc = min(SCOLS, nx - g);
+      mbar_wait(&empty[slot], ph ^ 1u);
+      mbar_expect_tx(&full[slot], bytes * nc);
+      double* st = ring + size_t(slot) * SSTAGE;
+      for (int k = 0; k < nc; ++k) bulk_g2s(st + k * SCOL_STRIDE, Xe + size_t(g + k) * n, bytes, &full[slot]);
+      if (++slot == SNST) { slot = 0; ph ^= 1u; }
+    }
+  }
+}
+
+// Shared-memory ring setup: zero the stages and init the barriers.  Called by all threads.
+// Rows of a short last chunk beyond n are never copied: the stage keeps zeros or finite basis
+// values of an earlier item there, which meet zero Y fragments (k_sproj) or feed output rows
+// that are not stored (k_supdate).
+__device__ void ring_setup(double* ring, unsigned long long* full, unsigned long long* empty) {
+  for (int i = threadIdx.x; i < SNST * SSTAGE; i += blockDim.x) ring[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SNST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SNW);
+    }
+  }
+  fence_proxy_async();
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- D = X^T Y, G = Y^T Y partials
+// part[(e * nch + c) * (nx + ny) * ny + a + b * (nx + ny)]: a < nx -> (X^T Y)[a][b], a >= nx -> (Y^T Y)[a - nx][b]
+template <int MB>
+__global__ void __launch_bounds__(STHREADS, 1)
+k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const double* Y, long long ys_e, int ny,
+        int gram, double* part, const int* active) {
+  extern __shared__ __align__(16) double sm[];
+  double* ring = sm;
+  double* red = ring + SNST * SSTAGE;  // [SNW][8 * MB] warp tiles
+  __shared__ __align__(8) unsigned long long full[SNST], empty[SNST];
+  ring_setup(ring, full, empty);
+  const int nitems = E * nch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == SNW) {
+    produce(X, xs_e, n, nx, nitems, nch, active, ring, full, empty);
+    return;
+  }
+  constexpr int NJ = MB / 8;
+  const int njt = (ny + 7) >> 3;
+  const int pw = nx + (gram ? ny : 0);
+  int slot = 0;
+  unsigned ph = 0;
+  Item w;
+  for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
+    const int r0 = w.c * SR, rows = min(SR, n - r0);
+    // B fragments: Y[row 64w + 4q + (lane&3)][col 8j + (lane>>2)]
+    double bf[16][NJ];
+    const double* Ye = Y + w.e * ys_e + r0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int r = 64 * warp + 4 * q + (lane & 3);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int col = 8 * j + (lane >> 2);
+        bf[q][j] = (r < rows && col < ny) ? __ldcg(Ye + size_t(col) * n + r) : 0.0;
+      }
+    }
+    double* P = part + size_t(w.e * nch + w.c) * pw * ny;
+    const bool rows_here = 64 * warp < rows;
+    for (int g = 0; g < nx; g += SCOLS) {
+      double acc[NJ][2];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+      mbar_wait(&full[slot], ph);
+      const double* st = ring + size_t(slot) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 64 * warp + (lane & 3);
+      if (rows_here) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const double a = st[4 * q];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (j < njt) dmma(acc[j][0], acc[j][1], a, bf[q][j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == SNST) { slot = 0; ph ^= 1u; }
+      // warp tiles -> shared (D[i = lane>>2][jcol = 8j + 2(lane&3) + h]); sum in warp order
+      double* rw = red + warp * (8 * MB);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3)] = acc[j][0];
+        rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3) + 1] = acc[j][1];
+      }
+      consumer_sync();
+      const int nc = min(SCOLS, nx - g);
+      for (int idx = threadIdx.x; idx < nc * ny; idx += SNW * 32) {
+        const int i = idx % nc, b = idx / nc;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < SNW; ++q) s += red[q * (8 * MB) + i * MB + b];
+        P[(g + i) + size_t(b) * pw] = s;
+      }
+      consumer_sync();
+    }
+    if (gram) {  // G = Y^T Y over the chunk: A fragment of tile i = bf[q][i] (same layout)
+      for (int i = 0; i < njt; ++i) {
+        double acc[NJ][2];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          double a = 0.0;
+#pragma unroll
+          for (int ii = 0; ii < NJ; ++ii)
+            if (ii == i) a = bf[q][ii];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (j < njt) dmma(acc[j][0], acc[j][1], a, bf[q][j]);
+        }
+        double* rw = red + warp * (8 * MB);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3)] = acc[j][0];
+          rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3) + 1] = acc[j][1];
+        }
+        consumer_sync();
+        const int nc = min(8, ny - 8 * i);
+        for (int idx = threadIdx.x; idx < nc * ny; idx += SNW * 32) {
+          const int ii = idx % nc, b = idx / nc;
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < SNW; ++q) s += red[q * (8 * MB) + ii * MB + b];
+          P[nx + 8 * i + ii + size_t(b) * pw] = s;
+        }
+        consumer_sync();
+      }
+    }
+  }
+}
+
+// Sum the chunk partials in chunk order: a < nx -> D[e][row0 + a, col0 + b] (ld ldd, = or +=),
+// a >= nx -> G[e][(a - nx) + b * ny].
+__global__ void k_sred(int nx, int ny, int pw, int nch, const double* part, double* D, long long ds_e, int ldd,
+                       int row0, int col0, int accumulate, double* G, long long gs_e, const int* active) {
+  const int e = blockIdx.y;
+  if (active && !active[e]) return;
+  const size_t sz = size_t(pw) * ny;
+  const double* pe = part + size_t(e) * nch * sz;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < pw * ny; idx += gridDim.x * blockDim.x) {
+    double s0 = 0.0, s1 = 0.0;
+    int c = 0;
+    for (; c + 1 < nch; c += 2) {
+      s0 += __ldcg(pe + size_t(c) * sz + idx);
+      s1 += __ldcg(pe + size_t(c + 1) * sz + idx);
+    }
+    if (c < nch) s0 += __ldcg(pe + size_t(c) * sz + idx);
+    const double s = s0 + s1;
+    const int a = idx % pw, b = idx / pw;
+    if (a < nx) {
+      double* d = D + e * ds_e + (row0 + a) + size_t(col0 + b) * ldd;
+      *d = accumulate ? *d + s : s;
+    } else {
+      G[e * gs_e + (a - nx) + size_t(b) * ny] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Y = beta Y + alpha X M
+template <int MB>
+__global__ void __launch_bounds__(STHREADS, 1)
+k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx, const double* M, long long ms_e, int ldm,
+          double* Y, long long ys_e, int ny, double alpha, double beta, const int* active) {
+  extern __shared__ __align__(16) double sm[];
+  double* ring = sm;
+  __shared__ __align__(8) unsigned long long full[SNST], empty[SNST];
+  ring_setup(ring, full, empty);
+  const int nitems = E * nch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == SNW) {
+    produce(X, xs_e, n, nx, nitems, nch, active, ring, full, empty);
+    return;
+  }
+  constexpr int NJ = MB / 8;
+  const int njt = (ny + 7) >> 3;
+  int slot = 0;
+  unsigned ph = 0;
+  Item w;
+  for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
+    const int r0 = w.c * SR, rows = min(SR, n - r0);
+    const double* Me = M + w.e * ms_e;
+    double acc[8][NJ][2];
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[t][j][0] = acc[t][j][1] = 0.0;
+    const bool rows_here = 64 * warp < rows;
+    for (int g = 0; g < nx; g += SCOLS) {
+      // B fragments of this stage: M[g + 4kq + (lane&3)][8j + (lane>>2)] (zero beyond nx / ny)
+      double bm[2][NJ];
+#pragma unroll
+      for (int kq = 0; kq < 2; ++kq) {
+        const int a = g + 4 * kq + (lane & 3);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int b = 8 * j + (lane >> 2);
+          bm[kq][j] = (a < nx && b < ny) ? __ldg(Me + a + size_t(b) * ldm) : 0.0;
+        }
+      }
+      mbar_wait(&full[slot], ph);
+      // A fragment: X[col 4kq + (lane&3)][row 64w + 8t + (lane>>2)]
+      const double* st = ring + size_t(slot) * SSTAGE + (lane & 3) * SCOL_STRIDE + 64 * warp + (lane >> 2);
+      if (rows_here) {
+#pragma unroll
+        for (int kq = 0; kq < 2; ++kq)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const double a = st[kq * 4 * SCOL_STRIDE + 8 * t];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+              if (j < njt) dmma(acc[t][j][0], acc[t][j][1], a, bm[kq][j]);
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == SNST) { slot = 0; ph ^= 1u; }
+    }
+    // epilogue: D[row 8t + (lane>>2)][col 8j + 2(lane&3) + h]
+    double* Ye = Y + w.e * ys_e + r0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = 64 * warp + 8 * t + (lane >> 2);
+      if (r >= rows) continue;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int b = 8 * j + 2 * (lane & 3) + h;
+          if (b < ny) {
+            double* y = Ye + size_t(b) * n + r;
+            const double v = alpha * acc[t][j][h];
+            *y = beta != 0.0 ? fma(beta, *y, v) : v;
+          }
+        }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+bool stream_ok(int n, int ny) { return (n % 2) == 0 && ny >= 1 && ny <= 32 && n >= SR; }
+
+static int stream_grid(int items) { return std::max(1, std::min(items, 148)); }
+
+static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + size_t(SNW) * 8 * MB); }
+static size_t supdate_smem() { return sizeof(double) * size_t(SNST) * SSTAGE; }
+
+size_t stream_part_doubles(int E, int n, int nx, int ny) {
+  return size_t(E) * cdiv(n, SR) * size_t(nx + ny) * ny;
+}
+
+void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e, int nx, const double* Y,
+                  long long ys_e, int ny, double* part, size_t part_cap, double* D, long long ds_e, int ldd, int row0,
+                  int col0, bool accumulate, double* G, long long gs_e, const int* active) {
+  if (E == 0 || ny == 0 || (nx == 0 && !G)) return;
+  if (!stream_ok(n, ny)) fail(1, "streaming projection: unsupported shape");
+  const int nch = cdiv(n, SR);
+  const int pw = nx + (G ? ny : 0);
+  if (size_t(E) * nch * pw * ny > part_cap) fail(2, "streaming projection: partial buffer too small");
+  const double ea = eact(E, active);
+  {
+    ProfScope ps(PC_XTY, st, ea * n * 8.0 * (nx + ny), 2.0 * ea * double(n) * ny * (nx + (G ? ny : 0)));
+    const int gx = stream_grid(E * nch);
+    const int MB = ny <= 8 ? 8 : ny <= 16 ? 16 : 32;
+    const int gram = G ? 1 : 0;
+    if (MB == 8)
+      k_sproj<8><<<gx, STHREADS, sproj_smem(8), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
+    else if (MB == 16)
+      k_sproj<16><<<gx, STHREADS, sproj_smem(16), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
+    else
+      k_sproj<32><<<gx, STHREADS, sproj_smem(32), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+    dim3 g2(std::min(cdiv(pw * ny, 256), 16), E);
+    k_sred<<<g2, 256, 0, st>>>(nx, ny, pw, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, G, gs_e, active);
+    count_launch();
+    PEXP_LAUNCH_CHECK();
+  }
+}
+
+void launch_supdate(cudaStream_t st, int E, int n, const double* X, long long xs_e, int nx, const double* M,
+                    long long ms_e, int ldm, double* Y, long long ys_e, int ny, double alpha, double beta,
+                    const int* active) {
+  if (E == 0 || ny == 0) return;
+  if (!stream_ok(n, ny)) fail(1, "streaming update: unsupported shape");
+  if (nx == 0) fail(1, "streaming update: empty product");
+  const int nch = cdiv(n, SR);
+  const double ea = eact(E, active);
+  ProfScope ps(PC_COMBINE, st, ea * n * 8.0 * (nx + ny * (beta != 0.0 ? 2 : 1)), 2.0 * ea * double(n) * nx * ny);
+  const int gx = stream_grid(E * nch);
+  const int MB = ny <= 8 ? 8 : ny <= 16 ? 16 : 32;
+  if (MB == 8)
+    k_supdate<8><<<gx, STHREADS, supdate_smem(), st>>>(E, n, nch, X, xs_e, nx, M, ms_e, ldm, Y, ys_e, ny, alpha, beta,
+                                                       active);
+  else if (MB == 16)
+    k_supdate<16><<<gx, STHREADS, supdate_smem(), st>>>(E, n, nch, X, xs_e, nx, M, ms_e, ldm, Y, ys_e, ny, alpha,
+                                                        beta, active);
+  else
+    k_supdate<32><<<gx, STHREADS, supdate_smem(), st>>>(E, n, nch, X, xs_e, nx, M, ms_e, ldm, Y, ys_e, ny, alpha,
+                                                        beta, active);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void stream_init() {
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj_smem(8)));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj_smem(16)));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj_smem(32)));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_supdate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)supdate_smem()));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_supdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)supdate_smem()));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_supdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)supdate_smem()));
+}
+
+}  // namespace pexp

@@ -236,17 +236,17 @@ def test_linear_config2_full_size_all_outputs():
 
 
 @pytest.mark.parametrize("route", ROUTES)
-@pytest.mark.parametrize("s,n,P,restart_blocks", [(20, 700, 4, 0), (20, 700, 4, 3), (40, 900, 3, 0)])
+@pytest.mark.parametrize("s,n,P,restart_blocks", [(20, 700, 4, 0), (20, 700, 4, 6), (40, 900, 3, 0)])
 def test_linear_wide_blocks(s, n, P, restart_blocks, route):
     """Block widths 8 < m <= 32 and m > 32 (a rough 1e-6-noise source keeps every sample:
     m = s): the DMMA projections, the deferred-column in-block QR at m > 32 and nested restarts
     at wide blocks, on both Arnoldi routes."""
     p = synth.generic_linear(n=n, bc="periodic", nu=5e-3, a=1.3, P=P, s=s, T=0.5, seed=7, rank=3, noise=1e-6)
-    out, st = _linear(p, k_max=640, restart_blocks=restart_blocks, route=route, records=True)
+    out, st = _linear(p, k_max=880, restart_blocks=restart_blocks, route=route, records=True)
     ref, info = _oracle_linear(p, dense_max=0, return_info=True)
     assert st["m_j"] == info["m"][0].tolist() == [s] * P
     assert rel(out, ref) < 1e-8, st
-    if restart_blocks == 3:
+    if restart_blocks:
         assert st["restarts"] >= 1, st
 
 
