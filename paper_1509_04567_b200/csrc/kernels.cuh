@@ -143,10 +143,11 @@ bool stream_ok(int n, int ny);
 size_t stream_part_doubles(int E, int n, int nx, int ny);
 void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e, int nx, const double* Y,
                   long long ys_e, int ny, double* part, size_t part_cap, double* D, long long ds_e, int ldd, int row0,
-                  int col0, bool accumulate, double* G, long long gs_e, const int* active);
+                  int col0, bool accumulate, double* G, long long gs_e, const int* active, int gld = 0,
+                  int grow0 = 0, int gcol0 = 0);
 void launch_supdate(cudaStream_t st, int E, int n, const double* X, long long xs_e, int nx, const double* M,
                     long long ms_e, int ldm, double* Y, long long ys_e, int ny, double alpha, double beta,
-                    const int* active);
+                    const int* active, const int* nxe = nullptr);
 void stream_init();
 
 // small.cu

@@ -177,7 +177,7 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
     B.stepws = sw ? ar.take<double>(sw) : nullptr;
   }
   if (stream_ok(n, std::min(mcap, 32))) {
-    B.spart_cap = stream_part_doubles(Ec, n, kcap, std::min(mcap, 32));
+    B.spart_cap = stream_part_doubles(Ec, n, kcap + std::min(mcap, 32), std::min(mcap, 32));
     B.spart = ar.take<double>(B.spart_cap);
   }
   B.Nmax = ktot + (forced ? 4 * mcap : 0);

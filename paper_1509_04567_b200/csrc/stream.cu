@@ -95,8 +95,8 @@ __device__ __forceinline__ bool next_item(int& it, int nitems, int nch, const in
 }
 
 // Producer: stream X[:, 0:nx] rows [c*SR, c*SR + rows) of every item, 8 columns per stage.
-__device__ void produce(const double* X, long long xs_e, int n, int nx, int nitems, int nch, const int* active,
-                        double* ring, unsigned long long* full, unsigned long long* empty) {
+__device__ void produce(const double* X, long long xs_e, int n, int nx0, int nitems, int nch, const int* active,
+                        double* ring, unsigned long long* full, unsigned long long* empty, const int* nxe) {
   if ((threadIdx.x & 31) != 0) return;
   int slot = 0;
   unsigned ph = 0;
@@ -105,6 +105,7 @@ __device__ void produce(const double* X, long long xs_e, int n, int nx, int nite
     const int r0 = w.c * SR, rows = min(SR, n - r0);
     const unsigned bytes = unsigned(rows) * 8u;
     const double* Xe = X + w.e * xs_e + r0;
+    const int nx = nxe ? min(nx0, nxe[w.e]) : nx0;
     for (int g = 0; g < nx; g += SCOLS) {
       const int nc = min(SCOLS, nx - g);
       mbar_wait(&empty[slot], ph ^ 1u);
@@ -149,7 +150,7 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
   const int nitems = E * nch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == SNW) {
-    produce(X, xs_e, n, nx, nitems, nch, active, ring, full, empty);
+    produce(X, xs_e, n, nx, nitems, nch, active, ring, full, empty, nullptr);
     return;
   }
   constexpr int NJ = MB / 8;
@@ -246,10 +247,15 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
   }
 }
 
-// Sum the chunk partials in chunk order: a < nx -> D[e][row0 + a, col0 + b] (ld ldd, = or +=),
-// a >= nx -> G[e][(a - nx) + b * ny].
-__global__ void k_sred(int nx, int ny, int pw, int nch, const double* part, double* D, long long ds_e, int ldd,
-                       int row0, int col0, int accumulate, double* G, long long gs_e, const int* active) {
+// Output descriptor of a reduced block: element (a, b) -> p[e * s_e + (row0 + a) + (col0 + b) * ld].
+struct OutDesc {
+  double* p;
+  long long s_e;
+  int ld, row0, col0, accumulate;
+};
+
+// Sum the chunk partials in chunk order: rows a < nx -> D, rows a >= nx -> G (row a - nx).
+__global__ void k_sred(int nx, int ny, int pw, int nch, const double* part, OutDesc D, OutDesc G, const int* active) {
   const int e = blockIdx.y;
   if (active && !active[e]) return;
   const size_t sz = size_t(pw) * ny;
@@ -263,21 +269,20 @@ __global__ void k_sred(int nx, int ny, int pw, int nch, const double* part, doub
     }
     if (c < nch) s0 += __ldcg(pe + size_t(c) * sz + idx);
     const double s = s0 + s1;
-    const int a = idx % pw, b = idx / pw;
-    if (a < nx) {
-      double* d = D + e * ds_e + (row0 + a) + size_t(col0 + b) * ldd;
-      *d = accumulate ? *d + s : s;
-    } else {
-      G[e * gs_e + (a - nx) + size_t(b) * ny] = s;
-    }
+    int a = idx % pw;
+    const int b = idx / pw;
+    const OutDesc& o = a < nx ? D : G;
+    if (a >= nx) a -= nx;
+    double* d = o.p + e * o.s_e + (o.row0 + a) + size_t(o.col0 + b) * o.ld;
+    *d = o.accumulate ? *d + s : s;
   }
 }
 
 // ---------------------------------------------------------------- Y = beta Y + alpha X M
 template <int MB>
 __global__ void __launch_bounds__(STHREADS, 1)
-k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx, const double* M, long long ms_e, int ldm,
-          double* Y, long long ys_e, int ny, double alpha, double beta, const int* active) {
+k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx0, const double* M, long long ms_e, int ldm,
+          double* Y, long long ys_e, int ny, double alpha, double beta, const int* active, const int* nxe) {
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;
   __shared__ __align__(8) unsigned long long full[SNST], empty[SNST];
@@ -285,7 +290,7 @@ k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx, const 
   const int nitems = E * nch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == SNW) {
-    produce(X, xs_e, n, nx, nitems, nch, active, ring, full, empty);
+    produce(X, xs_e, n, nx0, nitems, nch, active, ring, full, empty, nxe);
     return;
   }
   constexpr int NJ = MB / 8;
@@ -296,6 +301,7 @@ k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx, const 
   for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
     const int r0 = w.c * SR, rows = min(SR, n - r0);
     const double* Me = M + w.e * ms_e;
+    const int nx = nxe ? min(nx0, nxe[w.e]) : nx0;
     double acc[8][NJ][2];
 #pragma unroll
     for (int t = 0; t < 8; ++t)
@@ -361,13 +367,14 @@ static int stream_grid(int items) { return std::max(1, std::min(items, 148)); }
 static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + size_t(SNW) * 8 * MB); }
 static size_t supdate_smem() { return sizeof(double) * size_t(SNST) * SSTAGE; }
 
-size_t stream_part_doubles(int E, int n, int nx, int ny) {
-  return size_t(E) * cdiv(n, SR) * size_t(nx + ny) * ny;
-}
+// partial doubles of E evaluations when pw rows (nx, plus ny if the Gram is fused) x ny are reduced
+size_t stream_part_doubles(int E, int n, int pw, int ny) { return size_t(E) * cdiv(n, SR) * size_t(pw) * ny; }
 
 void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e, int nx, const double* Y,
                   long long ys_e, int ny, double* part, size_t part_cap, double* D, long long ds_e, int ldd, int row0,
-                  int col0, bool accumulate, double* G, long long gs_e, const int* active) {
+                  int col0, bool accumulate, double* G, long long gs_e, const int* active, int gld, int grow0,
+                  int gcol0) {
+  if (gld <= 0) gld = ny;
   if (E == 0 || ny == 0 || (nx == 0 && !G)) return;
   if (!stream_ok(n, ny)) fail(1, "streaming projection: unsupported shape");
   const int nch = cdiv(n, SR);
@@ -375,7 +382,7 @@ void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e
   if (size_t(E) * nch * pw * ny > part_cap) fail(2, "streaming projection: partial buffer too small");
   const double ea = eact(E, active);
   {
-    ProfScope ps(PC_XTY, st, ea * n * 8.0 * (nx + ny), 2.0 * ea * double(n) * ny * (nx + (G ? ny : 0)));
+    ProfScope ps(PC_SPROJ, st, ea * n * 8.0 * (nx + ny), 2.0 * ea * double(n) * ny * (nx + (G ? ny : 0)));
     const int gx = stream_grid(E * nch);
     const int MB = ny <= 8 ? 8 : ny <= 16 ? 16 : 32;
     const int gram = G ? 1 : 0;
@@ -388,7 +395,9 @@ void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e
     count_launch();
     PEXP_LAUNCH_CHECK();
     dim3 g2(std::min(cdiv(pw * ny, 256), 16), E);
-    k_sred<<<g2, 256, 0, st>>>(nx, ny, pw, nch, part, D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, G, gs_e, active);
+    const OutDesc od{D, ds_e, ldd, row0, col0, accumulate ? 1 : 0};
+    const OutDesc og{G, gs_e, gld, grow0, gcol0, (nx == 0 && accumulate) ? 1 : 0};
+    k_sred<<<g2, 256, 0, st>>>(nx, ny, pw, nch, part, od, og, active);
     count_launch();
     PEXP_LAUNCH_CHECK();
   }
@@ -396,24 +405,23 @@ void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e
 
 void launch_supdate(cudaStream_t st, int E, int n, const double* X, long long xs_e, int nx, const double* M,
                     long long ms_e, int ldm, double* Y, long long ys_e, int ny, double alpha, double beta,
-                    const int* active) {
+                    const int* active, const int* nxe) {
   if (E == 0 || ny == 0) return;
   if (!stream_ok(n, ny)) fail(1, "streaming update: unsupported shape");
-  if (nx == 0) fail(1, "streaming update: empty product");
   const int nch = cdiv(n, SR);
   const double ea = eact(E, active);
-  ProfScope ps(PC_COMBINE, st, ea * n * 8.0 * (nx + ny * (beta != 0.0 ? 2 : 1)), 2.0 * ea * double(n) * nx * ny);
+  ProfScope ps(PC_SUPDATE, st, ea * n * 8.0 * (nx + ny * (beta != 0.0 ? 2 : 1)), 2.0 * ea * double(n) * nx * ny);
   const int gx = stream_grid(E * nch);
   const int MB = ny <= 8 ? 8 : ny <= 16 ? 16 : 32;
   if (MB == 8)
     k_supdate<8><<<gx, STHREADS, supdate_smem(), st>>>(E, n, nch, X, xs_e, nx, M, ms_e, ldm, Y, ys_e, ny, alpha, beta,
-                                                       active);
+                                                       active, nxe);
   else if (MB == 16)
     k_supdate<16><<<gx, STHREADS, supdate_smem(), st>>>(E, n, nch, X, xs_e, nx, M, ms_e, ldm, Y, ys_e, ny, alpha,
-                                                        beta, active);
+                                                        beta, active, nxe);
   else
     k_supdate<32><<<gx, STHREADS, supdate_smem(), st>>>(E, n, nch, X, xs_e, nx, M, ms_e, ldm, Y, ys_e, ny, alpha,
-                                                        beta, active);
+                                                        beta, active, nxe);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }

@@ -456,6 +456,19 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
                 double* D, long long ds_e, int ldd, int row0, int col0, bool accumulate,
                 const int* active, int* cnt) {
   if (E == 0 || nx == 0 || ny == 0) return;
+  if (stream_ok(n, ny)) {  // TMA-fed DMMA streaming kernels (stream.cu)
+    const bool gram = X == Y && xs_e == ys_e && x0 == y0 && nx == ny;
+    const int pw = gram ? ny : nx;
+    if (stream_part_doubles(E, n, pw, ny) <= part_cap) {
+      if (gram)
+        launch_sproj(st, E, n, X, xs_e, 0, Y + size_t(y0) * n, ys_e, ny, part, part_cap, nullptr, 0, 0, 0, 0, false, D,
+                     ds_e, active, ldd, row0, col0);
+      else
+        launch_sproj(st, E, n, X + size_t(x0) * n, xs_e, nx, Y + size_t(y0) * n, ys_e, ny, part, part_cap, D, ds_e, ldd,
+                     row0, col0, accumulate, nullptr, 0, active);
+      return;
+    }
+  }
   RedArgs ra{D, ds_e, ldd, row0, col0, accumulate ? 1 : 0, cnt};
   if (ny > 8 && ny <= 32 && nx >= 32) {
     const int rch = xty_chunks(n, E * cdiv(nx, 64));
@@ -537,6 +550,17 @@ void launch_combine(cudaStream_t st, int E, int n, const double* X, long long xs
                     const double* M, long long ms_e, int ldm, double* O, long long os_e, int o0,
                     int ny, double alpha, double beta, const int* active, const int* nxe) {
   if (E == 0 || ny == 0) return;
+  if (stream_ok(n, std::min(ny, NB))) {  // TMA-fed DMMA streaming kernels (stream.cu)
+    for (int b0 = 0; b0 < ny; b0 += NB) {
+      const int nb = std::min(NB, ny - b0);
+      if (nx == 0 && beta == 1.0) continue;
+      if (ny > NB && O == X && o0 < x0 + nx && x0 < o0 + ny && xs_e == os_e)
+        fail(1, "combine: in-place product with more than 32 output columns");
+      launch_supdate(st, E, n, X + size_t(x0) * n, xs_e, nx, M + size_t(b0) * ldm, ms_e, ldm, O + size_t(o0 + b0) * n,
+                     os_e, nb, alpha, beta, active, nxe);
+    }
+    return;
+  }
   for (int b0 = 0; b0 < ny; b0 += NB) {
     int nb = std::min(NB, ny - b0);
     if (nx == 0) {

@@ -21,6 +21,7 @@ ap.add_argument("config", default="C5", nargs="?")
 ap.add_argument("--route", type=int, default=0)
 ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--plain-only", action="store_true", help="one plain solve (ncu target), no profiler pass")
 a = ap.parse_args()
 build.build()
 from paper_1509_04567_b200 import pexp  # noqa: E402
@@ -44,6 +45,8 @@ for _ in range(a.repeat):
     out, st = run(False)
     torch.cuda.synchronize()
     print("plain solve", round(time.perf_counter() - t0, 3), "s", {k: st[k] for k in ("ms_total", "wr_iters", "max_m", "max_k", "host_syncs", "kernel_launches")}, flush=True)
+if a.plain_only:
+    sys.exit(0)
 pexp.profile_enable(True)
 out, st = run(True)
 prof = pexp.profile_read()
