@@ -94,9 +94,20 @@ __device__ __forceinline__ bool next_item(int& it, int nitems, int nch, const in
   return false;
 }
 
-// Producer: stream X[:, 0:nx] rows [c*SR, c*SR + rows) of every item, 8 columns per stage.
-__device__ void produce(const double* X, long long xs_e, int n, int nx0, int nitems, int nch, const int* active,
-                        double* ring, unsigned long long* full, unsigned long long* empty, const int* nxe) {
+// One streamed segment of columns of a work item: columns [0, ncols) of P (per-eval stride s_e),
+// rows [c*SR, c*SR + rows); ncols_e (nullable) caps the count per evaluation.
+struct Seg {
+  const double* P;
+  long long s_e;
+  int ncols;
+  const int* ncols_e;
+  __device__ int count(int e) const { return P ? (ncols_e ? min(ncols, ncols_e[e]) : ncols) : 0; }
+};
+
+// Producer (one lane): for every item, segment a then segment b, 8 columns per stage, each column
+// one bulk copy of the item's rows into the ring.
+__device__ void produce(int n, int nitems, int nch, const int* active, Seg sa, Seg sb, double* ring,
+                        unsigned long long* full, unsigned long long* empty) {
   if ((threadIdx.x & 31) != 0) return;
   int slot = 0;
   unsigned ph = 0;
@@ -104,18 +115,31 @@ __device__ void produce(const double* X, long long xs_e, int n, int nx0, int nit
   for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
     const int r0 = w.c * SR, rows = min(SR, n - r0);
     const unsigned bytes = unsigned(rows) * 8u;
-    const double* Xe = X + w.e * xs_e + r0;
-    const int nx = nxe ? min(nx0, nxe[w.e]) : nx0;
-    for (int g = 0; g < nx; g += SCOLS) {
-      const int nc = min(SCOLS, nx - g);
-      mbar_wait(&empty[slot], ph ^ 1u);
-      mbar_expect_tx(&full[slot], bytes * nc);
-      double* st = ring + size_t(slot) * SSTAGE;
-      for (int k = 0; k < nc; ++k) bulk_g2s(st + k * SCOL_STRIDE, Xe + size_t(g + k) * n, bytes, &full[slot]);
-      if (++slot == SNST) { slot = 0; ph ^= 1u; }
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      const Seg& sg = q == 0 ? sa : sb;
+      const int nx = sg.count(w.e);
+      const double* Xe = sg.P + w.e * sg.s_e + r0;
+      for (int g = 0; g < nx; g += SCOLS) {
+        const int nc = min(SCOLS, nx - g);
+        mbar_wait(&empty[slot], ph ^ 1u);
+        mbar_expect_tx(&full[slot], bytes * nc);
+        double* st = ring + size_t(slot) * SSTAGE;
+        for (int k = 0; k < nc; ++k) bulk_g2s(st + k * SCOL_STRIDE, Xe + size_t(g + k) * n, bytes, &full[slot]);
+        if (++slot == SNST) { slot = 0; ph ^= 1u; }
+      }
     }
   }
 }
+
+// Consumer-side ring position.
+struct RingPos {
+  int slot = 0;
+  unsigned ph = 0;
+  __device__ void advance() {
+    if (++slot == SNST) { slot = 0; ph ^= 1u; }
+  }
+};
 
 // Shared-memory ring setup: zero the stages and init the barriers.  Called by all threads.
 // Rows of a short last chunk beyond n are never copied: the stage keeps zeros or finite basis
@@ -138,6 +162,7 @@ __device__ void ring_setup(double* ring, unsigned long long* full, unsigned long
 
 // ---------------------------------------------------------------- D = X^T Y, G = Y^T Y partials
 // part[(e * nch + c) * (nx + ny) * ny + a + b * (nx + ny)]: a < nx -> (X^T Y)[a][b], a >= nx -> (Y^T Y)[a - nx][b]
+// Ring order per item: the ceil(ny/8) stages of Y (loaded into B fragments), then the X stages.
 template <int MB>
 __global__ void __launch_bounds__(STHREADS, 1)
 k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const double* Y, long long ys_e, int ny,
@@ -150,27 +175,32 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
   const int nitems = E * nch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == SNW) {
-    produce(X, xs_e, n, nx, nitems, nch, active, ring, full, empty, nullptr);
+    produce(n, nitems, nch, active, Seg{Y, ys_e, ny, nullptr}, Seg{X, xs_e, nx, nullptr}, ring, full, empty);
     return;
   }
   constexpr int NJ = MB / 8;
   const int njt = (ny + 7) >> 3;
   const int pw = nx + (gram ? ny : 0);
-  int slot = 0;
-  unsigned ph = 0;
+  RingPos rp;
   Item w;
   for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
     const int r0 = w.c * SR, rows = min(SR, n - r0);
-    // B fragments: Y[row 64w + 4q + (lane&3)][col 8j + (lane>>2)]
+    // B fragments from the Y stages: Y[row 64w + 4q + (lane&3)][col 8j + (lane>>2)]
     double bf[16][NJ];
-    const double* Ye = Y + w.e * ys_e + r0;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int r = 64 * warp + 4 * q + (lane & 3);
+    for (int j = 0; j < NJ; ++j) {
+      if (j < njt) {
+        mbar_wait(&full[rp.slot], rp.ph);
+        const double* st = ring + size_t(rp.slot) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 64 * warp + (lane & 3);
+        const bool colok = 8 * j + (lane >> 2) < ny;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const int col = 8 * j + (lane >> 2);
-        bf[q][j] = (r < rows && col < ny) ? __ldcg(Ye + size_t(col) * n + r) : 0.0;
+        for (int q = 0; q < 16; ++q) bf[q][j] = (colok && 64 * warp + 4 * q + (lane & 3) < rows) ? st[4 * q] : 0.0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rp.slot]);
+        rp.advance();
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) bf[q][j] = 0.0;
       }
     }
     double* P = part + size_t(w.e * nch + w.c) * pw * ny;
@@ -179,8 +209,8 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
       double acc[NJ][2];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-      mbar_wait(&full[slot], ph);
-      const double* st = ring + size_t(slot) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 64 * warp + (lane & 3);
+      mbar_wait(&full[rp.slot], rp.ph);
+      const double* st = ring + size_t(rp.slot) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 64 * warp + (lane & 3);
       if (rows_here) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -191,8 +221,8 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == SNST) { slot = 0; ph ^= 1u; }
+      if (lane == 0) mbar_arrive(&empty[rp.slot]);
+      rp.advance();
       // warp tiles -> shared (D[i = lane>>2][jcol = 8j + 2(lane&3) + h]); sum in warp order
       double* rw = red + warp * (8 * MB);
 #pragma unroll
@@ -212,20 +242,17 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
       consumer_sync();
     }
     if (gram) {  // G = Y^T Y over the chunk: A fragment of tile i = bf[q][i] (same layout)
-      for (int i = 0; i < njt; ++i) {
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        if (i >= njt) break;
         double acc[NJ][2];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          double a = 0.0;
-#pragma unroll
-          for (int ii = 0; ii < NJ; ++ii)
-            if (ii == i) a = bf[q][ii];
+        for (int q = 0; q < 16; ++q)
 #pragma unroll
           for (int j = 0; j < NJ; ++j)
-            if (j < njt) dmma(acc[j][0], acc[j][1], a, bf[q][j]);
-        }
+            if (j < njt) dmma(acc[j][0], acc[j][1], bf[q][i], bf[q][j]);
         double* rw = red + warp * (8 * MB);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
@@ -279,6 +306,7 @@ __global__ void k_sred(int nx, int ny, int pw, int nch, const double* part, OutD
 }
 
 // ---------------------------------------------------------------- Y = beta Y + alpha X M
+// Ring order per item: the X stages, then (beta != 0) the ceil(ny/8) stages of Y's old values.
 template <int MB>
 __global__ void __launch_bounds__(STHREADS, 1)
 k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx0, const double* M, long long ms_e, int ldm,
@@ -290,13 +318,13 @@ k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx0, const
   const int nitems = E * nch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == SNW) {
-    produce(X, xs_e, n, nx0, nitems, nch, active, ring, full, empty, nxe);
+    produce(n, nitems, nch, active, Seg{X, xs_e, nx0, nxe}, Seg{beta != 0.0 ? Y : nullptr, ys_e, ny, nullptr}, ring,
+            full, empty);
     return;
   }
   constexpr int NJ = MB / 8;
   const int njt = (ny + 7) >> 3;
-  int slot = 0;
-  unsigned ph = 0;
+  RingPos rp;
   Item w;
   for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
     const int r0 = w.c * SR, rows = min(SR, n - r0);
@@ -308,21 +336,29 @@ k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx0, const
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[t][j][0] = acc[t][j][1] = 0.0;
     const bool rows_here = 64 * warp < rows;
-    for (int g = 0; g < nx; g += SCOLS) {
-      // B fragments of this stage: M[g + 4kq + (lane&3)][8j + (lane>>2)] (zero beyond nx / ny)
-      double bm[2][NJ];
+    // B fragments M[g + 4kq + (lane&3)][8j + (lane>>2)] (zero beyond nx / ny), one stage ahead
+    double bm[2][NJ], bn[2][NJ];
+    auto load_bm = [&](int g, double (&d)[2][NJ]) {
 #pragma unroll
       for (int kq = 0; kq < 2; ++kq) {
         const int a = g + 4 * kq + (lane & 3);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
           const int b = 8 * j + (lane >> 2);
-          bm[kq][j] = (a < nx && b < ny) ? __ldg(Me + a + size_t(b) * ldm) : 0.0;
+          d[kq][j] = (a < nx && b < ny) ? __ldg(Me + a + size_t(b) * ldm) : 0.0;
         }
       }
-      mbar_wait(&full[slot], ph);
+    };
+    constexpr bool PREF = NJ <= 2;  // register budget: prefetch M one stage ahead below MB = 32
+    if (PREF) load_bm(0, bm);
+    for (int g = 0; g < nx; g += SCOLS) {
+      if (PREF)
+        load_bm(g + SCOLS, bn);
+      else
+        load_bm(g, bm);
+      mbar_wait(&full[rp.slot], rp.ph);
       // A fragment: X[col 4kq + (lane&3)][row 64w + 8t + (lane>>2)]
-      const double* st = ring + size_t(slot) * SSTAGE + (lane & 3) * SCOL_STRIDE + 64 * warp + (lane >> 2);
+      const double* st = ring + size_t(rp.slot) * SSTAGE + (lane & 3) * SCOL_STRIDE + 64 * warp + (lane >> 2);
       if (rows_here) {
 #pragma unroll
         for (int kq = 0; kq < 2; ++kq)
@@ -335,26 +371,42 @@ k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx0, const
           }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == SNST) { slot = 0; ph ^= 1u; }
+      if (lane == 0) mbar_arrive(&empty[rp.slot]);
+      rp.advance();
+      if (PREF)
+#pragma unroll
+        for (int kq = 0; kq < 2; ++kq)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) bm[kq][j] = bn[kq][j];
     }
-    // epilogue: D[row 8t + (lane>>2)][col 8j + 2(lane&3) + h]
+    // epilogue: D[row 8t + (lane>>2)][col 8j + 2(lane&3) + h]; old Y values from the Y stages
     double* Ye = Y + w.e * ys_e + r0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int r = 64 * warp + 8 * t + (lane >> 2);
-      if (r >= rows) continue;
+    for (int j = 0; j < NJ; ++j) {
+      if (j >= njt) break;
+      const double* sy = nullptr;
+      if (beta != 0.0) {
+        mbar_wait(&full[rp.slot], rp.ph);
+        sy = ring + size_t(rp.slot) * SSTAGE + 64 * warp + (lane >> 2);
+      }
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+      for (int t = 0; t < 8; ++t) {
+        const int r = 64 * warp + 8 * t + (lane >> 2);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int b = 8 * j + 2 * (lane & 3) + h;
-          if (b < ny) {
-            double* y = Ye + size_t(b) * n + r;
-            const double v = alpha * acc[t][j][h];
-            *y = beta != 0.0 ? fma(beta, *y, v) : v;
+          const int cb = 2 * (lane & 3) + h, b = 8 * j + cb;
+          if (b < ny && r < rows) {
+            double v = alpha * acc[t][j][h];
+            if (beta != 0.0) v = fma(beta, sy[cb * SCOL_STRIDE + 8 * t], v);
+            Ye[size_t(b) * n + r] = v;
           }
         }
+      }
+      if (beta != 0.0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rp.slot]);
+        rp.advance();
+      }
     }
   }
 }

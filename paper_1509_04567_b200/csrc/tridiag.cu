@@ -184,6 +184,213 @@ __global__ void k_factor(int nf, int n, int periodic, const int* __restrict__ op
   if (bad) atomicExch(err, 1);
 }
 
+// ---------------------------------------------------------------- parallel factorisation
+// One CTA per factor.  The pivot recurrence d_i = T_i - p_i / d_{i-1} (p_i = (-g a_i)(-g c_{i-1}),
+// Thomas LU without pivoting) is a Moebius map of d_{i-1}: in projective coordinates
+// (x, y) -> (T_i x - p_i y, x), d = x / y, i.e. a product of 2x2 matrices.  Per 2048-row tile, each
+// thread composes the matrices of its 8 consecutive rows (normalised by the largest entry; the map
+// is scale-free), a block-wide exclusive scan gives every thread the composed map of the rows before
+// it, applied to the tile's carry-in pivot; each thread then re-runs the exact Thomas recurrence over
+// its 8 rows (so l, 1/d, the superdiagonal and the pivot test are computed exactly as the sequential
+// recurrence does, from a start value accurate to rounding), and the tile's last pivot is the next
+// tile's carry.  The periodic Sherman-Morrison vectors z = T^{-1} u and w' = T^{-T} v / (1 + v^T z)
+// are affine-map scans (forward / backward) like the shift-and-invert solve itself.
+struct Mob {
+  double a, b, c, d;  // [[a, b], [c, d]]
+};
+__device__ __forceinline__ Mob mob_then(const Mob& f, const Mob& t) {  // t * f, normalised
+  Mob r{t.a * f.a + t.b * f.c, t.a * f.b + t.b * f.d, t.c * f.a + t.d * f.c, t.c * f.b + t.d * f.d};
+  const double m = fmax(fmax(fabs(r.a), fabs(r.b)), fmax(fabs(r.c), fabs(r.d)));
+  if (m > 0.0 && isfinite(m)) {
+    const double s = 1.0 / m;
+    r.a *= s; r.b *= s; r.c *= s; r.d *= s;
+  }
+  return r;
+}
+
+// exclusive block scan of Moebius matrices in thread order (composition: later rows on the left)
+__device__ inline Mob block_excl_scan_mob(Mob v, Mob* wsm) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  Mob inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Mob p{__shfl_up_sync(0xffffffffu, inc.a, o), __shfl_up_sync(0xffffffffu, inc.b, o),
+          __shfl_up_sync(0xffffffffu, inc.c, o), __shfl_up_sync(0xffffffffu, inc.d, o)};
+    if (lane >= o) inc = mob_then(p, inc);
+  }
+  Mob exc{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1),
+          __shfl_up_sync(0xffffffffu, inc.c, 1), __shfl_up_sync(0xffffffffu, inc.d, 1)};
+  if (lane == 0) exc = Mob{1.0, 0.0, 0.0, 1.0};
+  __syncthreads();
+  if (lane == 31) wsm[w] = inc;
+  __syncthreads();
+  if (t == 0) {
+    Mob acc{1.0, 0.0, 0.0, 1.0};
+    for (int k = 0; k < PEXP_THREADS / 32; ++k) {
+      const Mob q = wsm[k];
+      wsm[k] = acc;
+      acc = mob_then(acc, q);
+    }
+  }
+  __syncthreads();
+  const Mob pre = wsm[w];
+  __syncthreads();
+  return mob_then(pre, exc);
+}
+
+// One affine first-order recurrence over all n rows, y_g = A(g) y_prev + B(g), in forward
+// (rows ascending) or backward order, tile by tile with a block scan per tile; y written to out.
+template <bool BWD, class FA, class FB>
+__device__ inline void cta_affine_pass(int n, FA fa, FB fb, double* out, Aff* wsm) {
+  const int t = threadIdx.x;
+  const int nchunk = (n + CHUNK - 1) / CHUNK;
+  double carry = 0.0;
+  for (int q = 0; q < nchunk; ++q) {
+    const int ch = BWD ? nchunk - 1 - q : q;
+    const int g0 = ch * CHUNK + t * EPT;
+    double av[EPT], bv[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int g = g0 + k;
+      av[k] = g < n ? fa(g) : 1.0;
+      bv[k] = g < n ? fb(g) : 0.0;
+    }
+    Aff m{1.0, 0.0};
+    if (BWD) {
+#pragma unroll
+      for (int k = EPT - 1; k >= 0; --k) m = after(m, Aff{av[k], bv[k]});
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) m = after(m, Aff{av[k], bv[k]});
+    }
+    Aff tot;
+    const Aff pre = block_excl_scan<BWD>(m, BWD ? PEXP_THREADS - 1 - t : t, wsm, tot);
+    double y = fma(pre.A, carry, pre.B);
+    if (BWD) {
+#pragma unroll
+      for (int k = EPT - 1; k >= 0; --k) {
+        y = fma(av[k], y, bv[k]);
+        if (g0 + k < n) out[g0 + k] = y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        y = fma(av[k], y, bv[k]);
+        if (g0 + k < n) out[g0 + k] = y;
+      }
+    }
+    carry = fma(tot.A, carry, tot.B);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(PEXP_THREADS)
+k_factor_par(int n, int periodic, const int* __restrict__ opidx, const double* __restrict__ gam,
+             const double* __restrict__ sub, const double* __restrict__ diag, const double* __restrict__ sup,
+             double* __restrict__ fl, double* __restrict__ fdinv, double* __restrict__ fsup, double* __restrict__ fz,
+             double* __restrict__ fw, int* __restrict__ err) {
+  __shared__ Mob wm[PEXP_THREADS / 32];
+  __shared__ Aff wsm[PEXP_THREADS / 32 + 1];
+  __shared__ double s_carry;
+  __shared__ int s_bad;
+  const int f = blockIdx.x, t = threadIdx.x;
+  const double g = gam[f];
+  const size_t o = size_t(opidx ? opidx[f] : f) * n, fo = size_t(f) * n;
+  const double *A = sub + o, *B = diag + o, *C = sup + o;
+  double *l = fl + fo, *di = fdinv + fo, *cs = fsup + fo;
+  const double d0 = 1.0 - g * B[0];
+  double alpha = 0.0, beta = 0.0, gs = 0.0;
+  if (periodic) {
+    beta = -g * A[0];       // M[0][n-1]
+    alpha = -g * C[n - 1];  // M[n-1][0]
+    gs = -d0;
+  }
+  const double dfirst = periodic ? d0 - gs : d0;
+  if (t == 0) {
+    s_carry = dfirst;
+    s_bad = !(fabs(dfirst) > 1e-13 * fabs(d0)) || !isfinite(dfirst);
+  }
+  __syncthreads();
+  bool bad = false;
+  auto Tdiag = [&](int i) {
+    double Ti = 1.0 - g * B[i];
+    if (periodic && i == n - 1) Ti -= alpha * beta / gs;
+    return Ti;
+  };
+  const int nchunk = (n + CHUNK - 1) / CHUNK;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int g0 = ch * CHUNK + t * EPT;
+    double Tv[EPT], av[EPT], cp[EPT];  // T_i, -g a_i, -g c_{i-1}
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int i = g0 + k;
+      const bool ok = i >= 1 && i < n;
+      Tv[k] = ok ? Tdiag(i) : 1.0;
+      av[k] = ok ? -g * A[i] : 0.0;
+      cp[k] = ok ? -g * C[i - 1] : 0.0;
+    }
+    Mob m{1.0, 0.0, 0.0, 1.0};  // row 0 and rows >= n: identity (row 0's pivot is the carry-in)
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (g0 + k >= 1 && g0 + k < n) m = mob_then(m, Mob{Tv[k], -av[k] * cp[k], 1.0, 0.0});
+    const Mob pre = block_excl_scan_mob(m, wm);
+    const double c0 = s_carry;  // pivot of the row before this tile (row 0's pivot for tile 0)
+    const double x = pre.a * c0 + pre.b, y = pre.c * c0 + pre.d;
+    double dprev = x / y;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int i = g0 + k;
+      if (i == 0) {
+        l[0] = 0.0;
+        di[0] = 1.0 / dfirst;
+        cs[0] = -g * C[0];
+        dprev = dfirst;
+      } else if (i < n) {
+        const double li = av[k] / dprev;
+        const double d = Tv[k] - li * cp[k];
+        if (!(fabs(d) > 1e-13 * (fabs(Tv[k]) + fabs(li * cp[k]))) || !isfinite(d)) bad = true;
+        l[i] = li;
+        di[i] = 1.0 / d;
+        cs[i] = i < n - 1 ? -g * C[i] : 0.0;
+        dprev = d;
+      }
+    }
+    __syncthreads();                            // every thread has read s_carry
+    if (t == PEXP_THREADS - 1) s_carry = dprev;  // last row of a full tile: the next tile's carry
+    __syncthreads();
+  }
+  if (bad) s_bad = 1;
+  __syncthreads();
+  if (periodic) {
+    double *z = fz + fo, *w = fw + fo;
+    __syncthreads();
+    // z = T^{-1} u, u = (gs, 0, .., 0, alpha): y_i = u_i - l_i y_{i-1}; z_i = d_i^{-1} (y_i - cs_i z_{i+1})
+    cta_affine_pass<false>(
+        n, [&](int i) { return -l[i]; },
+        [&](int i) { return i == 0 ? gs : (i == n - 1 ? alpha : 0.0); }, z, wsm);
+    __syncthreads();
+    cta_affine_pass<true>(
+        n, [&](int i) { return -di[i] * cs[i]; }, [&](int i) { return di[i] * z[i]; }, z, wsm);
+    __syncthreads();
+    // w = T^{-T} v, v = (1, 0, .., 0, beta/gs): U^T q = v, then L^T w = q
+    const double vl = beta / gs;
+    cta_affine_pass<false>(
+        n, [&](int i) { return i == 0 ? 0.0 : -di[i] * cs[i - 1]; },
+        [&](int i) { return di[i] * (i == 0 ? 1.0 : (i == n - 1 ? vl : 0.0)); }, w, wsm);
+    __syncthreads();
+    cta_affine_pass<true>(
+        n, [&](int i) { return i == n - 1 ? 0.0 : -l[i + 1]; }, [&](int i) { return w[i]; }, w, wsm);
+    __syncthreads();
+    const double denom = 1.0 + z[0] + vl * z[n - 1];
+    if (!(fabs(denom) > 0.0) || !isfinite(denom)) bad = true;
+    const double inv = 1.0 / denom;
+    for (int i = t; i < n; i += PEXP_THREADS) w[i] *= inv;
+    if (bad) s_bad = 1;
+    __syncthreads();
+  }
+  if (t == 0 && s_bad) atomicExch(err, 1);
+}
+
 // Grid (ncols, E).  Column c of eval e: rhs at rhs + e*rs_e + (cin0+c)*n, result at
 // out + e*os_e + (cout0+c)*n (may alias rhs only if identical).  fidx[e] selects the factor.
 __global__ void __launch_bounds__(PEXP_THREADS)
@@ -223,8 +430,12 @@ void launch_burgers_rows(cudaStream_t st, int nops, int n, double nu, const doub
 void launch_factor(cudaStream_t st, const Factors& F, int nf, const int* opidx, const double* gam,
                    const Ops& O, int* err) {
   ProfScope ps(PC_FACTOR, st, double(nf) * F.n * 8.0 * (3 + 3 + (F.periodic ? 2 : 0)), 0.0);
-  k_factor<<<cdiv(nf, 64), 64, 0, st>>>(nf, F.n, F.periodic, opidx, gam, O.sub, O.diag, O.sup,
-                                         F.l, F.dinv, F.sup, F.z, F.w, err);
+  if (F.n >= CHUNK)  // long columns: one CTA per factor, block scans (k_factor_par)
+    k_factor_par<<<nf, PEXP_THREADS, 0, st>>>(F.n, F.periodic, opidx, gam, O.sub, O.diag, O.sup, F.l, F.dinv, F.sup,
+                                              F.z, F.w, err);
+  else
+    k_factor<<<cdiv(nf, 64), 64, 0, st>>>(nf, F.n, F.periodic, opidx, gam, O.sub, O.diag, O.sup, F.l, F.dinv, F.sup,
+                                          F.z, F.w, err);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }

@@ -38,6 +38,8 @@ def t(x):
     (5000, "periodic", 1e-3, 1.0, 1 / 640),      # ragged: 2 full 2048-row chunks + tail
     (4096, "dirichlet", 1e-3, 1.0, 1 / 640),
     (1024, "periodic", 1e-4, 2.0, 1 / 160),      # C4 corner: cell Peclet ~20, M not dominant
+    (6144, "periodic", 1e-5, 2.0, 1 / 160),      # parallel (Moebius-scan) factorisation, cell Peclet ~33
+    (65536, "periodic", 1e-3, 0.3, 1 / 2560),    # C5-sized column, 32 tiles of the parallel factorisation
     (7, "dirichlet", 0.3, -1.0, 0.5),            # tiny
 ])
 def test_sai_solve_vs_dense(n, bc, nu, a, gamma):
