@@ -92,6 +92,9 @@ typedef struct {
                              (default 1e-14)                               */
   int32_t hom_group;      /* linear homogeneous legs sharing one block Krylov space
                              (default 8, at most 16)                       */
+  int32_t width_buckets;  /* 0 = default (on): evaluations grouped by retained rank m_j run
+                             with their own block width; -1 = off (every evaluation padded
+                             to max_j m_j).                                 */
 } pexp_options;
 
 /* Per-solve statistics (host memory, caller-owned). */

@@ -14,6 +14,7 @@ struct CallCfg {
   double piv_tol = 1e-14;  // pexp_options.piv_tol
   int route = 0;           // pexp_options.route (0 auto, 1 streaming, 2 fused where it fits)
   int hom_group = 8;       // pexp_options.hom_group
+  int buckets = 1;         // pexp_options.width_buckets (0: pad every evaluation to max m_j)
   int syncs = 0;           // host synchronisations performed by the current call
   int active_hint = -1;    // evaluations still active in the running EBK loop (-1: unknown);
                            // the profiler's algorithmic byte/flop counts use it
@@ -180,6 +181,21 @@ void launch_small_hom(cudaStream_t st, const SPArgs& a, int nslots);
 void launch_expm_batched(cudaStream_t st, int E, int N, const double* A, double* X, double* work,
                          long long work_slot, int* iwork, int nslots);
 void small_init();
+
+// stencil.cu: width buckets of the forced EBK (gather into / scatter out of a chunk)
+struct GatherArgs {
+  const int* perm;
+  int wb, mmax, s, n;
+  const double *gam, *crit, *coef, *U;
+  long long us_e;
+  const int *active, *fidx, *opidx;
+  double *gam_c, *crit_c, *coef_c, *V;
+  long long vs_e;
+  int *active_c, *fidx_c, *opidx_c;
+};
+void launch_bucket_gather(cudaStream_t st, int ec, const GatherArgs& a);
+void launch_bucket_scatter(cudaStream_t st, int ec, const int* perm, size_t cnt, const double* Yt, long long yts,
+                           double* Y, long long ys_e, const int* krec_c, int* krec);
 
 // stencil.cu
 void launch_apply_A(cudaStream_t st, const Ops& O, const int* opidx, int E, int ncols, const double* X,

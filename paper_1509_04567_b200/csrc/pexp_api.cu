@@ -89,6 +89,7 @@ static Opts norm_opts(const pexp_options& o) {
   r.cfg.piv_tol = o.piv_tol > 0 ? o.piv_tol : 1e-14;
   r.cfg.route = o.route;
   r.cfg.hom_group = o.hom_group > 0 ? std::min(o.hom_group, 16) : 8;
+  r.cfg.buckets = o.width_buckets >= 0 ? 1 : 0;
   r.cfg.syncs = 0;
   return r;
 }
@@ -104,6 +105,12 @@ struct EbkBufs {
   double* stepws = nullptr;  // fused Arnoldi step: global V^T W partials (large bases)
   double* spart = nullptr;   // streaming route: per-chunk partials of [V W]^T W
   size_t spart_cap = 0;
+  // width buckets of the forced EBK (ebk_forced_bucketed): permutation [E] and the chunk-slot
+  // copies of the per-evaluation inputs / outputs (nullptr: bucketing not planned)
+  int* perm = nullptr;
+  double *gam_c = nullptr, *crit_c = nullptr, *coef_c = nullptr, *Ytmp = nullptr;
+  int *active_c = nullptr, *fidx_c = nullptr, *opidx_c = nullptr, *krec_c = nullptr;
+  int ycols = 0;
   double* work;
   int* iwork;
   int nslots, Nmax;
@@ -130,7 +137,7 @@ static size_t part_need(int E, int n, int nx, int ny) {
 // kcap: basis columns per evaluation and cycle; ktot: total Krylov dimension over all cycles
 // (ktot > kcap or restart_blocks > 0 allocates the nested-restart state).
 static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int ktot, int mcap, int nout, int s,
-                      bool forced, double* Wt_shared, bool restartable) {
+                      bool forced, double* Wt_shared, bool restartable, int ycols = 0) {
   Ec = std::max(1, std::min(E, Ec));
   B.E = Ec; B.n = n; B.kcap = kcap; B.ktot = ktot; B.mcap = mcap; B.nout = nout; B.s = s;
   B.vs_e = (long long)kcap * n;
@@ -187,6 +194,18 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   B.nslots = std::min(Ec, B.Nmax > 512 ? 148 : 512);
   B.work = ar.take<double>(size_t(B.nslots) * B.work_slot);
   B.iwork = ar.take<int>(size_t(B.nslots) * B.iwork_slot);
+  if (forced && ycols > 0 && E > 1) {  // width buckets
+    B.ycols = ycols;
+    B.perm = ar.take<int>(E);
+    B.gam_c = ar.take<double>(Ec);
+    B.crit_c = ar.take<double>(Ec);
+    B.active_c = ar.take<int>(Ec);
+    B.fidx_c = ar.take<int>(Ec);
+    B.opidx_c = ar.take<int>(Ec);
+    B.krec_c = ar.take<int>(Ec);
+    B.coef_c = ar.take<double>(size_t(Ec) * (s - 1) * 4 * mcap);
+    B.Ytmp = ar.take<double>(size_t(Ec) * ycols * n);
+  }
   if (restartable) {
     B.NA = ar.take<double>(size_t(Ec) * ktot * ktot);
     B.CPL = ar.take<double>(size_t(Ec) * mcap * kcap);
@@ -260,6 +279,7 @@ struct RunInfo {
   int restarts = 0;
   int unconverged = 0;
   double worst_res_ratio = 0.0;
+  int chunks = 0, buckets = 1;
 };
 
 // Where a restart accumulates the outputs of a closed cycle: Y[e*ys_e + j*n] += V_c z_c at
@@ -775,7 +795,7 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   L.Yend = ar.take<double>(size_t(E) * n);
   alloc_svd(ar, L.S, E, n, s);
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
-  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable);
+  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable, 1);
   if (P > 1) {
     const int mh = hom_group_width(c, P), G = cdiv(P - 1, mh), Eg = Bt * G;
     // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
@@ -826,7 +846,7 @@ static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
   L.err = ar.take<int>(4);
   alloc_svd(ar, L.S, E, n, s);
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
-  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, s, s, true, L.S.R, restartable);
+  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, s, s, true, L.S.R, restartable, s);
   const int k1 = std::min(o.kcap, 512);  // scan: single vectors, short spaces, no restart
   alloc_ebk(ar, L.B1, 1, 1, n, k1, k1, 1, s, s, false, nullptr, false);
   if (hom_scan_ok(n, k1)) {
@@ -892,6 +912,95 @@ static RunInfo ebk_forced_chunked(cudaStream_t st, EbkBufs& B, const SvdBufs& S,
   return tot;
 }
 
+// Width buckets: evaluations are grouped by their retained rank m_j rounded up
+// to a multiple of 4, and every bucket runs its own block Arnoldi with that block width instead of
+// padding every evaluation to max_j m_j (the Krylov dimension, bytes and flops grow with the block
+// width).  Buckets with fewer than 16 evaluations merge into the next wider one.  Each chunk
+// gathers its evaluations' inputs into chunk slots, runs the EBK, and scatters the outputs (and the
+// k_j records) back.  The projected solution of an evaluation does not depend on its padding
+// (padding columns carry zero coefficients), only the Krylov space it is found in.
+static std::vector<std::pair<int, std::vector<int>>> width_buckets(const int* me, int E, int mmax) {
+  std::vector<std::vector<int>> cls((mmax + 3) / 4 + 1);
+  for (int e = 0; e < E; ++e) cls[me[e] <= 0 ? 0 : (me[e] + 3) / 4].push_back(e);
+  // zero-rank evaluations (inactive) ride with the narrowest non-empty class
+  std::vector<std::pair<int, std::vector<int>>> out;
+  std::vector<int> carry = cls[0];
+  for (size_t c = 1; c < cls.size(); ++c) {
+    carry.insert(carry.end(), cls[c].begin(), cls[c].end());
+    const bool last = c + 1 == cls.size();
+    if (carry.empty()) continue;
+    int ncarry_active = 0;
+    for (int e : carry) ncarry_active += me[e] > 0;
+    if (ncarry_active >= 16 || last) {
+      out.push_back({std::min(int(4 * c), mmax), carry});
+      carry.clear();
+    }
+  }
+  if (!carry.empty()) {
+    if (out.empty()) out.push_back({std::max(mmax, 1), carry});
+    else out.back().second.insert(out.back().second.end(), carry.begin(), carry.end());
+  }
+  return out;
+}
+
+static RunInfo ebk_forced_bucketed(cudaStream_t st, EbkBufs& B, const SvdBufs& S, const Factors& F, const Ops& O,
+                                   bool periodic, int E, int mmax, const int* me, double h, int s, int out_stride,
+                                   int nout, int o0, double* Y, long long ys_e, int stop_rule, int restart_blocks) {
+  RunInfo tot;
+  const int n = B.n, Ecap = B.E;
+  const int no = o0 == 0 ? nout : 1;
+  if (no > B.ycols) fail(1, "bucketed EBK: output staging too small");
+  auto buckets = width_buckets(me, E, mmax);
+  std::vector<int> perm;
+  for (auto& b : buckets) perm.insert(perm.end(), b.second.begin(), b.second.end());
+  PEXP_CUDA_TRY(cudaMemcpyAsync(B.perm, perm.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
+  host_sync(st);  // pageable source
+  int p0 = 0;
+  for (auto& bk : buckets) {
+    const int wb = bk.first, nb = int(bk.second.size());
+    for (int c0 = 0; c0 < nb; c0 += Ecap, p0 += std::min(Ecap, nb - c0)) {
+      const int ec = std::min(Ecap, nb - c0);
+      GatherArgs ga{};
+      ga.perm = B.perm + p0; ga.wb = wb; ga.mmax = std::max(mmax, 1); ga.s = s; ga.n = n;
+      ga.gam = B.gam; ga.crit = B.crit; ga.coef = B.coef; ga.U = S.U; ga.us_e = (long long)s * n;
+      ga.active = B.active; ga.fidx = B.fidx; ga.opidx = B.opidx;
+      ga.gam_c = B.gam_c; ga.crit_c = B.crit_c; ga.coef_c = B.coef_c; ga.V = B.V; ga.vs_e = B.vs_e;
+      ga.active_c = B.active_c; ga.fidx_c = B.fidx_c; ga.opidx_c = B.opidx_c;
+      launch_bucket_gather(st, ec, ga);
+      EbkBufs Bc = B;
+      Bc.E = ec;
+      Bc.gam = B.gam_c; Bc.crit = B.crit_c; Bc.coef = B.coef_c; Bc.active = B.active_c;
+      Bc.fidx = B.fidx_c; Bc.opidx = B.opidx_c; Bc.krec = B.krec_c;
+      launch_fill_i32(st, Bc.krec, ec, 0);
+      const long long yts = (long long)no * n;
+      RunInfo r = ebk_run(st, Bc, F, O, periodic, wb, 0, h, s - 1, out_stride, nout, stop_rule,
+                          Accum{B.Ytmp, yts, o0, no}, restart_blocks);
+      launch_combine(st, ec, n, Bc.V, Bc.vs_e, 0, std::max(r.max_k, 1), Bc.Z + size_t(o0) * Bc.kcap, Bc.zs_e, Bc.kcap,
+                     B.Ytmp, yts, 0, no, 1.0, r.restarts ? 1.0 : 0.0, nullptr, Bc.kfin);
+      launch_bucket_scatter(st, ec, B.perm + p0, size_t(no) * n, B.Ytmp, yts, Y, ys_e, B.krec_c, B.krec);
+      tot.max_k = std::max(tot.max_k, r.max_k);
+      tot.max_ktot = std::max(tot.max_ktot, r.max_ktot);
+      tot.restarts += r.restarts;
+      tot.unconverged += r.unconverged;
+      tot.worst_res_ratio = std::max(tot.worst_res_ratio, r.worst_res_ratio);
+      ++tot.chunks;
+    }
+  }
+  tot.buckets = int(buckets.size());
+  return tot;
+}
+
+// The forced EBK: width buckets when the retained ranks differ enough to pay for them.
+static RunInfo ebk_forced(cudaStream_t st, EbkBufs& B, const SvdBufs& S, const Factors& F, const Ops& O, bool periodic,
+                          int E, int mmax, const int* me, double h, int s, int out_stride, int nout, int o0, double* Y,
+                          long long ys_e, int stop_rule, int restart_blocks) {
+  if (B.perm && g_cfg.buckets && width_buckets(me, E, mmax).size() > 1)
+    return ebk_forced_bucketed(st, B, S, F, O, periodic, E, mmax, me, h, s, out_stride, nout, o0, Y, ys_e, stop_rule,
+                               restart_blocks);
+  return ebk_forced_chunked(st, B, S, F, O, periodic, E, mmax, h, s, out_stride, nout, o0, Y, ys_e, stop_rule,
+                            restart_blocks);
+}
+
 // ---------------------------------------------------------------- C ABI
 extern "C" {
 
@@ -917,6 +1026,7 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
   if (o.basis_cols < 0 || o.eval_chunk < 0) return PEXP_EINVAL;
   if (o.route < 0 || o.route > 2 || o.defl_tol < 0 || o.piv_tol < 0 || o.hom_group < 0 || o.hom_group > 16)
     return PEXP_EINVAL;
+  if (o.width_buckets < -1 || o.width_buckets > 1) return PEXP_EINVAL;
   pexp_ctx* c = new pexp_ctx;
   c->n = n;
   c->bc = bc;
@@ -1012,8 +1122,8 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     launch_fill_i32(st, L.B.krec, E, 0);
     RunInfo ri{}, rh{};
     if (mmax > 0) {
-      ri = ebk_forced_chunked(st, L.B, L.S, L.F, L.O, periodic, E, mmax, h, s, s - 1, 2, 1, L.Yend, n, o.stop_rule,
-                              o.restart_blocks);
+      ri = ebk_forced(st, L.B, L.S, L.F, L.O, periodic, E, mmax, me.data(), h, s, s - 1, 2, 1, L.Yend, n, o.stop_rule,
+                      o.restart_blocks);
     } else {
       PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
     }
@@ -1144,7 +1254,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
                                                cudaMemcpyDeviceToHost, st));
       launch_fill_i32(st, L.B.krec, E, 0);
       if (mmax > 0) {
-        RunInfo ri = ebk_forced_chunked(st, L.B, L.S, L.F, L.O, true, E, mmax, h, s, 1, s, 0, L.Y, (long long)s * n,
+        RunInfo ri = ebk_forced(st, L.B, L.S, L.F, L.O, true, E, mmax, me.data(), h, s, 1, s, 0, L.Y, (long long)s * n,
                                         o.stop_rule, o.restart_blocks);
         if (ri.unconverged) fail(PEXP_ENOCONV, "Krylov capacity reached (nonhomogeneous, WR iteration " + std::to_string(k + 1) + ")");
         max_k = std::max(max_k, ri.max_ktot);

@@ -260,6 +260,64 @@ __global__ void k_fill_f64(double* p, size_t count, double v) {
     p[i] = v;
 }
 
+// ---------------------------------------------------------------- width buckets (pexp_api.cu)
+// Gather evaluations perm[0..ec) into the slots of one EBK chunk of block width wb: per-eval
+// scalars, the first wb columns of the orthonormal source basis (basis block 0) and the first wb
+// coefficient rows of the cubic spline (layout [s-1][4][w], w = mmax -> wb).
+__global__ void k_bucket_gather(GatherArgs a) {
+  const int i = blockIdx.y, e = a.perm[i];
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      a.gam_c[i] = a.gam[e];
+      a.crit_c[i] = a.crit[e];
+      a.active_c[i] = a.active[e];
+      a.fidx_c[i] = a.fidx[e];
+      a.opidx_c[i] = a.opidx[e];
+    }
+    const int np = (a.s - 1) * 4;
+    for (int idx = threadIdx.x; idx < np * a.wb; idx += blockDim.x) {
+      const int pq = idx / a.wb, c = idx % a.wb;
+      a.coef_c[size_t(i) * np * a.wb + idx] = a.coef[size_t(e) * np * a.mmax + size_t(pq) * a.mmax + c];
+    }
+  }
+  const size_t cnt = size_t(a.wb) * a.n;
+  const double* src = a.U + e * a.us_e;
+  double* dst = a.V + i * a.vs_e;
+  for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < cnt; k += size_t(gridDim.x) * blockDim.x)
+    dst[k] = src[k];
+}
+
+// Outputs of chunk slot i (cnt doubles at Yt + i*yts) back to evaluation perm[i] (Y + e*ys_e),
+// and the slot's Krylov-dimension record.
+__global__ void k_bucket_scatter(const int* perm, size_t cnt, const double* Yt, long long yts, double* Y,
+                                 long long ys_e, const int* krec_c, int* krec) {
+  const int i = blockIdx.y, e = perm[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0 && krec) krec[e] = krec_c[i];
+  const double* src = Yt + i * yts;
+  double* dst = Y + e * ys_e;
+  for (size_t k = size_t(blockIdx.x) * blockDim.x + threadIdx.x; k < cnt; k += size_t(gridDim.x) * blockDim.x)
+    dst[k] = src[k];
+}
+
+void launch_bucket_gather(cudaStream_t st, int ec, const GatherArgs& a) {
+  if (ec == 0) return;
+  ProfScope ps(PC_STENCIL, st, double(ec) * a.wb * a.n * 16.0, 0.0);
+  dim3 grid(std::max(1, std::min(cdiv(long(a.wb) * a.n, 4 * PEXP_THREADS), 64)), ec);
+  k_bucket_gather<<<grid, PEXP_THREADS, 0, st>>>(a);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
+void launch_bucket_scatter(cudaStream_t st, int ec, const int* perm, size_t cnt, const double* Yt, long long yts,
+                           double* Y, long long ys_e, const int* krec_c, int* krec) {
+  if (ec == 0) return;
+  ProfScope ps(PC_STENCIL, st, double(ec) * cnt * 16.0, 0.0);
+  dim3 grid(std::max(1, std::min(cdiv(long(cnt), 4 * PEXP_THREADS), 64)), ec);
+  k_bucket_scatter<<<grid, PEXP_THREADS, 0, st>>>(perm, cnt, Yt, yts, Y, ys_e, krec_c, krec);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
 // ---------------------------------------------------------------- host wrappers
 static int gx(long long n) { return int(std::min<long long>((n + PEXP_THREADS - 1) / PEXP_THREADS, 4096)); }
 static int gx_small(int n, int others) {

@@ -43,14 +43,18 @@ def t(x):
     (7, "dirichlet", 0.3, -1.0, 0.5),            # tiny
 ])
 def test_sai_solve_vs_dense(n, bc, nu, a, gamma):
+    import scipy.sparse as sp
+    from scipy.sparse.linalg import splu
     r = np.random.default_rng(n)
     c = pexp.Context(n, bc, nu, a)
     B = r.standard_normal((5, n))
     X = c.sai_solve(0, gamma, t(B)).cpu().numpy()
-    M = np.eye(n) - gamma * ade_matrix(n, bc, nu, a).toarray()
-    ref = np.linalg.solve(M, B.T).T
+    M = (sp.identity(n, format="csc") - gamma * ade_matrix(n, bc, nu, a)).tocsc()
+    ref = splu(M).solve(B.T.copy()).T           # LAPACK-style sparse LU with pivoting
     assert rel(X, ref) < 1e-12
-    assert np.linalg.norm(M @ X.T - B.T) <= 1e-12 * np.linalg.norm(B)
+    # backward error: residual relative to ||M|| ||X|| (the scale of the rounding in M X)
+    nM = abs(M).sum(axis=1).max()
+    assert np.linalg.norm(M @ X.T - B.T) <= 1e-14 * nM * np.linalg.norm(X) + 1e-13 * np.linalg.norm(B)
 
 
 # ---------------------------------------------------------------- subsystem 3: source SVD
@@ -354,3 +358,20 @@ def test_burgers_config5_full_size_first_iterate():
     assert rel(out, ref) < 1e-8, st
     # mass is conserved by every WR iterate (periodic central differences)
     assert np.abs(out.sum(axis=1) - p.u0.sum()).max() < 1e-9 * np.abs(p.u0).sum()
+
+
+@pytest.mark.parametrize("route", ROUTES)
+def test_linear_width_buckets(route):
+    """Retained ranks that differ across subintervals (a 1e-6-noise source on the second half:
+    m_j = s there, 4 elsewhere): the evaluations run in two width buckets (own block widths,
+    gathered into chunk slots and scattered back); equal to the oracle and to the unbucketed run."""
+    p = synth.generic_linear(n=600, bc="periodic", nu=5e-3, a=1.3, P=32, s=12, T=2.0, seed=5, rank=3)
+    r = np.random.default_rng(9)
+    p.src[0, 16:] += 1e-6 * r.standard_normal(p.src[0, 16:].shape)
+    out, st = _linear(p, k_max=512, route=route, records=True)
+    ref, info = _oracle_linear(p, return_info=True)
+    assert st["m_j"] == info["m"][0].tolist()
+    assert len(set(st["m_j"])) >= 2
+    assert rel(out, ref) < 1e-8, st
+    out2, st2 = _linear(p, k_max=512, route=route, width_buckets=-1)
+    assert rel(out2, ref) < 1e-8, st2
