@@ -973,8 +973,10 @@ static RunInfo ebk_forced_bucketed(cudaStream_t st, EbkBufs& B, const SvdBufs& S
       Bc.fidx = B.fidx_c; Bc.opidx = B.opidx_c; Bc.krec = B.krec_c;
       launch_fill_i32(st, Bc.krec, ec, 0);
       const long long yts = (long long)no * n;
+      // restart cycles keep the column count of the unbucketed run: restart_blocks steps of max m_j
+      const int rb = restart_blocks > 0 ? cdiv(long(restart_blocks) * std::max(mmax, 1), wb) : restart_blocks;
       RunInfo r = ebk_run(st, Bc, F, O, periodic, wb, 0, h, s - 1, out_stride, nout, stop_rule,
-                          Accum{B.Ytmp, yts, o0, no}, restart_blocks);
+                          Accum{B.Ytmp, yts, o0, no}, rb);
       launch_combine(st, ec, n, Bc.V, Bc.vs_e, 0, std::max(r.max_k, 1), Bc.Z + size_t(o0) * Bc.kcap, Bc.zs_e, Bc.kcap,
                      B.Ytmp, yts, 0, no, 1.0, r.restarts ? 1.0 : 0.0, nullptr, Bc.kfin);
       launch_bucket_scatter(st, ec, B.perm + p0, size_t(no) * n, B.Ytmp, yts, Y, ys_e, B.krec_c, B.krec);
