@@ -958,7 +958,7 @@ static RunInfo ebk_forced_bucketed(cudaStream_t st, EbkBufs& B, const SvdBufs& S
   int p0 = 0;
   for (auto& bk : buckets) {
     const int wb = bk.first, nb = int(bk.second.size());
-    for (int c0 = 0; c0 < nb; c0 += Ecap, p0 += std::min(Ecap, nb - c0)) {
+    for (int c0 = 0; c0 < nb; c0 += Ecap) {
       const int ec = std::min(Ecap, nb - c0);
       GatherArgs ga{};
       ga.perm = B.perm + p0; ga.wb = wb; ga.mmax = std::max(mmax, 1); ga.s = s; ga.n = n;
@@ -986,6 +986,7 @@ static RunInfo ebk_forced_bucketed(cudaStream_t st, EbkBufs& B, const SvdBufs& S
       tot.unconverged += r.unconverged;
       tot.worst_res_ratio = std::max(tot.worst_res_ratio, r.worst_res_ratio);
       ++tot.chunks;
+      p0 += ec;
     }
   }
   tot.buckets = int(buckets.size());
