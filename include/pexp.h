@@ -184,7 +184,8 @@ PEXP_API pexp_status pexp_expm_batched(pexp_ctx* ctx, const double* A, int32_t E
  * one-sided SVD, spline), 5 stencil / assembly / superposition, 6 factorisation,
  * 7 fused Arnoldi step (SaI solve + BCGS2 + in-block QR, one cluster per evaluation),
  * 8 Burgers homogeneous scan (persistent), 9 grouped homogeneous legs' projected problem,
- * 10 streaming-route projection [V W]^T W (TMA + DMMA), 11 streaming-route update W -= V H.
+ * 10 streaming-route projection [V W]^T W (TMA + DMMA), 11 streaming-route update W -= V H,
+ * 12 Burgers waveform update after the scan (all subintervals in parallel).
  * pexp_profile_enable(1) clears and starts recording CUDA events around every launch
  * (on the launch stream), with the launch's ALGORITHMIC bytes and flops;
  * pexp_profile_read() synchronises the device, fills per-class sums (ms, bytes, flops,

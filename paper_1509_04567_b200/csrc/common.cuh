@@ -44,7 +44,7 @@ inline void count_launch() { ++g_launches; }
 // launch's shapes), timed with CUDA events on the launch stream.
 enum ProfCat { PC_SOLVE = 0, PC_XTY = 1, PC_COMBINE = 2, PC_SMALL = 3, PC_SVDSMALL = 4, PC_STENCIL = 5,
                PC_FACTOR = 6, PC_ARNOLDI = 7, PC_SCAN = 8, PC_SMALLHOM = 9, PC_SPROJ = 10,
-               PC_SUPDATE = 11, PC_NCAT = 12 };
+               PC_SUPDATE = 11, PC_SCANOUT = 12, PC_NCAT = 13 };
 struct ProfRec {
   cudaEvent_t a, b;
   int cat;

@@ -116,9 +116,13 @@ struct ScanArgs {
   const double *u0, *Y, *Uold;  // u0 [n]; Y, Uold [P][s][n]
   double* Unew;                 // [P][s][n]
   double* delta;                // max |Unew - Uold| (atomic max)
-  double* V;                    // [kcap + 1][n]
+  double* V;                    // [kcap + 1][n]  scratch basis (subintervals not archived)
   double* H;                    // (kcap + 1) x kcap, ld kcap + 1
-  double* Zc;                   // [s][kcap]
+  double* Zc;                   // [P][s][kcap]   projected solutions at the nodes (per subinterval)
+  double* Vpool;                // [pool_cols][n] archived bases (outputs computed after the scan)
+  long long pool_cols;
+  int* koff;                    // [P] pool column offset of subinterval i (-1: not archived)
+  int* kc;                      // [P] converged dimension (-1: outputs written inside the scan)
   double* partA;                // [nw][pw]
   double* partB;                // [nw][pw]
   double* maps;                 // [2][nw][2]
@@ -129,8 +133,8 @@ struct ScanArgs {
 };
 
 // Projected check on the checker CTA: returns max_r residual; writes Zc[r][0..K).
-__device__ static double hom_check(const ScanArgs& a, int K, double gam, double beta, double* z, double* zn,
-                                   double* red, double* psm) {
+__device__ static double hom_check(const ScanArgs& a, double* Zc, int K, double gam, double beta, double* z,
+                                   double* zn, double* red, double* psm) {
   const int ld = a.kcap, ldh = a.kcap + 1;
   const size_t MM = size_t(ld) * ld;
   double* S0 = a.work;
@@ -162,7 +166,7 @@ __device__ static double hom_check(const ScanArgs& a, int K, double gam, double 
     for (int t = threadIdx.x; t < K * K; t += NT) F[t] = S2[(t % K) + size_t(t / K) * ld];
   for (int r = threadIdx.x; r < K; r += NT) z[r] = r == 0 ? beta : 0.0;
   __syncthreads();
-  for (int r = threadIdx.x; r < K; r += NT) a.Zc[r] = z[r];
+  for (int r = threadIdx.x; r < K; r += NT) Zc[r] = z[r];
   const int ng = max(1, min(8, NT / max(K, 1)));  // thread groups per row
   const int jper = (K + ng - 1) / ng;
   for (int q = 1; q < a.s; ++q) {
@@ -183,7 +187,7 @@ __device__ static double hom_check(const ScanArgs& a, int K, double gam, double 
       double v = 0.0;
       for (int g2 = 0; g2 < ng; ++g2) v += zn[g2 * K + rr];
       z[rr] = v;
-      a.Zc[size_t(q) * a.kcap + rr] = v;
+      Zc[size_t(q) * a.kcap + rr] = v;
     }
     __syncthreads();
   }
@@ -192,7 +196,7 @@ __device__ static double hom_check(const ScanArgs& a, int K, double gam, double 
   double maxres = 0.0;
   for (int q = 1 + w; q < a.s; q += NT / 32) {
     double xp = 0.0;
-    for (int r = lane; r < K; r += 32) xp = fma(S1[(K - 1) + size_t(r) * ld], __ldcg(a.Zc + size_t(q) * a.kcap + r), xp);
+    for (int r = lane; r < K; r += 32) xp = fma(S1[(K - 1) + size_t(r) * ld], __ldcg(Zc + size_t(q) * a.kcap + r), xp);
     xp = warp_sum(xp);
     maxres = fmax(maxres, fabs(htail * xp) / gam);
   }
@@ -221,27 +225,24 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   const int rend = min(n, row0 + a.seg);
   double uh[RPT_MAX], xr[RPT_MAX], vr[RPT_MAX];
 
-  // ---- subinterval 0: no homogeneous part; u_{k+1} = u0 + Y, u_hat(T_1) = Y(T_1)
+  // ---- subinterval 0: no homogeneous part; u_hat(T_1) = Y(T_1) (its waveform u0 + Y is written by
+  // k_scan_output after the scan)
   if (!checker) {
-    double mx = 0.0, b2 = 0.0;
+    double b2 = 0.0;
     for (int q = 0; q < rpt; ++q) {
       const int g = row0 + threadIdx.x * rpt + q;
       uh[q] = 0.0;
       if (g >= rend) continue;
-      for (int r = 0; r < s; ++r) {
-        const size_t k = size_t(r) * n + g;
-        const double un = a.u0[g] + a.Y[k];
-        mx = fmax(mx, fabs(un - a.Uold[k]));
-        if (!isfinite(un)) mx = INFINITY;
-        a.Unew[k] = un;
-      }
       uh[q] = a.Y[size_t(s - 1) * n + g];
       b2 = fma(uh[q], uh[q], b2);
     }
-    mx = block_max(mx, red);
-    if (threadIdx.x == 0) atomic_max_nonneg(a.delta, mx);
     b2 = block_sum(b2, red);
     if (threadIdx.x == 0) a.partA[size_t(c) * pw + PBETA] = b2;
+    if (c == 0 && threadIdx.x == 0) {
+      a.kc[0] = 0;
+      a.koff[0] = 0;
+      a.koff[1] = 0;
+    }
   }
   gbar(bar + B_ACNT, bar + B_AGEN, a.nw + 1);
 
@@ -250,6 +251,11 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
     const double beta = sqrt(hv[0]);
     const double gam = a.gam[i];
     const size_t fo = size_t(i) * n;
+    // this subinterval's basis: archived in the pool when it still has room for a full space
+    const int koff = __ldcg(a.koff + i);
+    const bool arch = koff >= 0 && koff + a.kcap + 1 <= a.pool_cols;
+    double* Vi = arch ? a.Vpool + size_t(koff) * n : a.V;
+    double* Zi = a.Zc + size_t(i) * a.s * a.kcap;
     gbar(bar + B_ACNT, bar + B_AGEN, a.nw + 1);  // everyone has read beta before partA is reused
     if (checker) {
       // ---------------------------------------------------------------- checker CTA
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           __syncthreads();
           const int K = s_dec;
           const bool brk = vload(fl + F_BREAK) == K;
-          const double res = hom_check(a, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
+          const double res = hom_check(a, Zi, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
           if (threadIdx.x == 0) {
             int result = 0;
             if (brk || res <= crit) result = K;
@@ -307,11 +313,13 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
       for (int q = 0; q < rpt; ++q) {
         const int g = row0 + threadIdx.x * rpt + q;
         vr[q] = uh[q] * inv;
-        if (g < rend) a.V[g] = vr[q];
+        if (g < rend) Vi[g] = vr[q];
       }
-      int Kc = 0;  // converged dimension (0: beta == 0, no homogeneous part)
+      int Kc = 0;     // converged dimension (0: beta == 0, no homogeneous part)
+      int kused = 0;  // basis columns written (Arnoldi steps performed + 1)
       if (beta > 0.0) {
         for (int k = 0;; ++k) {
+          kused = k + 1;
           // A: forward L-solve maps y_g = -l_g y_{g-1} + b_g over own rows
           Aff m{1.0, 0.0};
           double fdot = 0.0;
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
             }
           }
           const int kk = k + 1;  // columns 0..k
-          seg_dots(a.V, n, row0, rend - row0, kk, xr, rpt, xs, a.partA + size_t(c) * pw, PN);
+          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partA + size_t(c) * pw, PN);
           gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
           // D: h = V^T x; x -= V h; pass-2 dots
           grid_reduce(a.partA, pw, a.nw, 0, kk, hv);
@@ -404,11 +412,11 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
             const int g = row0 + threadIdx.x * rpt + q;
             if (g < rend) {
               double v = xr[q];
-              for (int j = 0; j < kk; ++j) v = fma(-hv[j], a.V[size_t(j) * n + g], v);
+              for (int j = 0; j < kk; ++j) v = fma(-hv[j], Vi[size_t(j) * n + g], v);
               xr[q] = v;
             }
           }
-          seg_dots(a.V, n, row0, rend - row0, kk, xr, rpt, xs, a.partB + size_t(c) * pw, PN);
+          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partB + size_t(c) * pw, PN);
           gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
           // E: second pass, norm, new column
           grid_reduce(a.partB, pw, a.nw, 0, kk, hv2);
@@ -422,9 +430,9 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
             const int g = row0 + threadIdx.x * rpt + q;
             if (g < rend) {
               double v = xr[q];
-              for (int j = 0; j < kk; ++j) v = fma(-hv2[j], a.V[size_t(j) * n + g], v);
+              for (int j = 0; j < kk; ++j) v = fma(-hv2[j], Vi[size_t(j) * n + g], v);
               vr[q] = v * sc;
-              a.V[size_t(kk) * n + g] = vr[q];
+              Vi[size_t(kk) * n + g] = vr[q];
             }
           }
           if (c == 0) {
@@ -444,38 +452,57 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
         if (c == 0 && threadIdx.x == 0) atomicExch(fl + F_ERR, 1);
         Kc = 0;
       }
-      // output: u_hat(t_r) = V Z[r] ; u_{k+1} = u0 + Y + u_hat ; delta ; next u_hat(T_i)
-      for (int t = threadIdx.x; t < s * Kc && Kc > 0 && s * Kc <= KSMALL_MAX; t += NT)
-        hv[t] = __ldcg(a.Zc + size_t(t / Kc) * a.kcap + t % Kc);
-      __syncthreads();
-      double mx = 0.0, b2 = 0.0;
+      // archived: only the end value u_hat(T_i) = Y(T_i) + V z(T_i) here (the waveform at all nodes is
+      // written by k_scan_output after the scan); otherwise the full waveform update in place
       const size_t yo = size_t(i) * s * n;
-      for (int q = 0; q < rpt; ++q) {
-        const int g = row0 + threadIdx.x * rpt + q;
-        uh[q] = 0.0;
-        if (g >= rend) continue;
-        for (int r = 0; r < s; ++r) {
+      double b2 = 0.0;
+      if (arch) {
+        for (int t = threadIdx.x; t < Kc; t += NT) hv[t] = __ldcg(Zi + size_t(s - 1) * a.kcap + t);
+        __syncthreads();
+        for (int q = 0; q < rpt; ++q) {
+          const int g = row0 + threadIdx.x * rpt + q;
+          uh[q] = 0.0;
+          if (g >= rend) continue;
           double w = 0.0;
-          if (s * Kc <= KSMALL_MAX) {
-            for (int j = 0; j < Kc; ++j) w = fma(a.V[size_t(j) * n + g], hv[r * Kc + j], w);
-          } else {
-            for (int j = 0; j < Kc; ++j) w = fma(a.V[size_t(j) * n + g], __ldcg(a.Zc + size_t(r) * a.kcap + j), w);
-          }
-          const size_t kx = yo + size_t(r) * n + g;
-          const double uhr = a.Y[kx] + w;
-          const double un = a.u0[g] + uhr;
-          mx = fmax(mx, fabs(un - a.Uold[kx]));
-          if (!isfinite(un)) mx = INFINITY;
-          a.Unew[kx] = un;
-          if (r == s - 1) uh[q] = uhr;
+          for (int j = 0; j < Kc; ++j) w = fma(Vi[size_t(j) * n + g], hv[j], w);
+          uh[q] = a.Y[yo + size_t(s - 1) * n + g] + w;
+          b2 = fma(uh[q], uh[q], b2);
         }
-        b2 = fma(uh[q], uh[q], b2);
+        b2 = block_sum(b2, red);
+      } else {
+        for (int t = threadIdx.x; t < s * Kc && Kc > 0 && s * Kc <= KSMALL_MAX; t += NT)
+          hv[t] = __ldcg(Zi + size_t(t / Kc) * a.kcap + t % Kc);
+        __syncthreads();
+        double mx = 0.0;
+        for (int q = 0; q < rpt; ++q) {
+          const int g = row0 + threadIdx.x * rpt + q;
+          uh[q] = 0.0;
+          if (g >= rend) continue;
+          for (int r = 0; r < s; ++r) {
+            double w = 0.0;
+            if (s * Kc <= KSMALL_MAX) {
+              for (int j = 0; j < Kc; ++j) w = fma(Vi[size_t(j) * n + g], hv[r * Kc + j], w);
+            } else {
+              for (int j = 0; j < Kc; ++j) w = fma(Vi[size_t(j) * n + g], __ldcg(Zi + size_t(r) * a.kcap + j), w);
+            }
+            const size_t kx = yo + size_t(r) * n + g;
+            const double uhr = a.Y[kx] + w;
+            const double un = a.u0[g] + uhr;
+            mx = fmax(mx, fabs(un - a.Uold[kx]));
+            if (!isfinite(un)) mx = INFINITY;
+            a.Unew[kx] = un;
+            if (r == s - 1) uh[q] = uhr;
+          }
+          b2 = fma(uh[q], uh[q], b2);
+        }
+        mx = block_max(mx, red);
+        b2 = block_sum(b2, red);
+        if (threadIdx.x == 0) atomic_max_nonneg(a.delta, mx);
       }
-      mx = block_max(mx, red);
-      b2 = block_sum(b2, red);
-      if (threadIdx.x == 0) {
-        atomic_max_nonneg(a.delta, mx);
-        a.partA[size_t(c) * pw + PBETA] = b2;
+      if (threadIdx.x == 0) a.partA[size_t(c) * pw + PBETA] = b2;
+      if (c == 0 && threadIdx.x == 0) {
+        a.kc[i] = arch ? Kc : -1;
+        if (i + 1 < a.P) a.koff[i + 1] = arch ? koff + kused + 1 : koff;
       }
     }
     // reset the per-subinterval flags (nobody reads them until after the barrier)
@@ -491,17 +518,73 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   }
 }
 
+// The waveform update of every archived subinterval, after the scan (all subintervals in parallel):
+//   u_{k+1}(t_{i,r}) = u0 + Y_i(t_r) + V_i z_i(t_r),  delta = max |u_{k+1} - u_k|    (Eq.(updateSolution))
+// One thread per row; the node coefficients z_i(t_r) staged in shared memory 32 columns at a time.
+constexpr int OUT_SMAX = 64;
+__global__ void __launch_bounds__(NT) k_scan_output(int s, int n, int kcap, const double* u0, const double* Y,
+                                                    const double* Uold, double* Unew, const double* Vpool,
+                                                    const int* koff, const int* kc, const double* Zc, double* delta) {
+  const int i = blockIdx.y;
+  const int K = kc[i];
+  if (K < 0) return;  // this subinterval's waveform was written inside the scan
+  __shared__ double Zs[OUT_SMAX][33];
+  __shared__ double red[32];
+  const int g = blockIdx.x * NT + threadIdx.x;
+  double acc[OUT_SMAX];
+#pragma unroll
+  for (int r = 0; r < OUT_SMAX; ++r) acc[r] = 0.0;
+  const double* V = Vpool + size_t(koff[i]) * n;
+  const double* Z = Zc + size_t(i) * s * kcap;
+  for (int j0 = 0; j0 < K; j0 += 32) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < s * 32; idx += NT) {
+      const int r = idx / 32, jj = idx % 32;
+      Zs[r][jj] = j0 + jj < K ? __ldcg(Z + size_t(r) * kcap + j0 + jj) : 0.0;
+    }
+    __syncthreads();
+    if (g < n) {
+      const int jn = min(32, K - j0);
+      for (int jj = 0; jj < jn; ++jj) {
+        const double v = V[size_t(j0 + jj) * n + g];
+#pragma unroll
+        for (int r = 0; r < OUT_SMAX; ++r)
+          if (r < s) acc[r] = fma(v, Zs[r][jj], acc[r]);
+      }
+    }
+  }
+  double mx = 0.0;
+  if (g < n) {
+    const double ug = u0[g];
+#pragma unroll
+    for (int r = 0; r < OUT_SMAX; ++r)
+      if (r < s) {
+        const size_t k = (size_t(i) * s + r) * n + g;
+        const double un = ug + Y[k] + acc[r];
+        mx = fmax(mx, fabs(un - Uold[k]));
+        if (!isfinite(un)) mx = INFINITY;
+        Unew[k] = un;
+      }
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) atomic_max_nonneg(delta, mx);
+}
+
 // worker CTAs of the scan: one per 256 rows (at most 147)
 static int scan_workers(int n) { return std::min(147, cdiv(n, NT)); }
 
 bool hom_scan_ok(int n, int kcap) { return kcap <= KSMALL_MAX && n <= 147 * NT * RPT_MAX; }
 
-size_t hom_scan_bytes(int n, int s, int kcap) {
+// archive of the scan's bases (outputs after the scan): on average 96 columns per subinterval;
+// subintervals beyond it write their waveform inside the scan
+static long long scan_pool_cols(int P, int kcap) { return (long long)P * std::min(kcap + 1, 96) + kcap + 1; }
+
+size_t hom_scan_bytes(int n, int s, int kcap, int P) {
   const int nw = scan_workers(n);
   const size_t pw = kcap + 8;
-  return sizeof(double) * (size_t(kcap + 1) * n + size_t(kcap + 1) * kcap + size_t(s) * kcap + 2 * nw * pw +
-                           4 * nw + 10 * size_t(kcap) * kcap) +
-         sizeof(int) * (kcap + F_NFLAGS) + 4 * sizeof(unsigned) + 16 * 256;  // + arena alignment
+  return sizeof(double) * (size_t(kcap + 1) * n + size_t(kcap + 1) * kcap + size_t(P) * s * kcap + 2 * nw * pw +
+                           4 * nw + 10 * size_t(kcap) * kcap + size_t(scan_pool_cols(P, kcap)) * n) +
+         sizeof(int) * (kcap + F_NFLAGS + 2 * P) + 4 * sizeof(unsigned) + 20 * 256;  // + arena alignment
 }
 
 int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
@@ -520,7 +603,12 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   const size_t pw = kcap + 8;
   a.V = ar.take<double>(size_t(kcap + 1) * n);
   a.H = ar.take<double>(size_t(kcap + 1) * kcap);
-  a.Zc = ar.take<double>(size_t(s) * kcap);
+  a.Zc = ar.take<double>(size_t(P) * s * kcap);
+  a.pool_cols = scan_pool_cols(P, kcap);
+  a.Vpool = ar.take<double>(size_t(a.pool_cols) * n);
+  a.koff = ar.take<int>(P);
+  a.kc = ar.take<int>(P);
+  if (s > OUT_SMAX) fail(1, "hom_scan: s > 64");
   a.partA = ar.take<double>(a.nw * pw);
   a.partB = ar.take<double>(a.nw * pw);
   a.maps = ar.take<double>(4 * a.nw);
@@ -534,11 +622,19 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   PEXP_CUDA_TRY(cudaMemsetAsync(a.H, 0, size_t(kcap + 1) * kcap * sizeof(double), st));
   {
     // algorithmic bytes: the waveform pass (Y, Uold read; Unew write) per subinterval
-    ProfScope ps(PC_SCAN, st, double(P) * s * n * 24.0, 0.0);
+    ProfScope ps(PC_SCAN, st, 0.0, 0.0);  // latency-bound chain
     void* args[] = {&a};
     const size_t smem = sizeof(double) * (2 * (KSMALL_MAX + 8) + NT * RPT_MAX + HS_PSM);
     PEXP_CUDA_TRY(cudaFuncSetAttribute(k_hom_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PEXP_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hom_scan, dim3(a.nw + 1), dim3(NT), args, smem, st));
+  }
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+  {
+    // algorithmic: Y, u_k read, u_{k+1} written at every node; the archived bases read once (~32 columns)
+    ProfScope ps(PC_SCANOUT, st, double(P) * s * n * 24.0 + double(P) * 32.0 * n * 8.0, 2.0 * double(P) * s * n * 32.0);
+    k_scan_output<<<dim3(cdiv(n, NT), P), NT, 0, st>>>(s, n, kcap, u0, Y, Uold, Unew, a.Vpool, a.koff, a.kc, a.Zc,
+                                                       delta);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();

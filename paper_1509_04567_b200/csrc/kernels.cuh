@@ -170,7 +170,7 @@ void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, 
 void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax = 0);
 // hom_scan.cu: the Burgers homogeneous scan as one persistent cooperative kernel
 bool hom_scan_ok(int n, int kcap);
-size_t hom_scan_bytes(int n, int s, int kcap);
+size_t hom_scan_bytes(int n, int s, int kcap, int P);
 int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
                     double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
                     double* delta, char* ws, size_t ws_bytes);

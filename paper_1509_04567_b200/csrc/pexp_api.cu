@@ -850,7 +850,7 @@ static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
   const int k1 = std::min(o.kcap, 512);  // scan: single vectors, short spaces, no restart
   alloc_ebk(ar, L.B1, 1, 1, n, k1, k1, 1, s, s, false, nullptr, false);
   if (hom_scan_ok(n, k1)) {
-    L.scan_bytes = hom_scan_bytes(n, s, k1);
+    L.scan_bytes = hom_scan_bytes(n, s, k1, P);
     L.scan_ws = ar.take<char>(L.scan_bytes);
   }
 }

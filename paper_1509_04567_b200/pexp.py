@@ -27,7 +27,8 @@ EXPORTED = ["pexp_create", "pexp_create_batched", "pexp_destroy", "pexp_last_err
             "pexp_workspace_bytes", "pexp_set_workspace", "pexp_solve_linear", "pexp_solve_burgers",
             "pexp_sai_solve", "pexp_source_svd", "pexp_expm_batched", "pexp_profile_enable", "pexp_profile_read"]
 PROFILE_CLASSES = ["sai_solve", "xty", "combine", "small_problem", "small_dense", "stencil", "factor",
-                   "arnoldi_step", "hom_scan", "small_hom", "stream_proj", "stream_update"]
+                   "arnoldi_step", "hom_scan", "small_hom", "stream_proj", "stream_update",
+                   "scan_output"]
 
 
 class Options(C.Structure):
