@@ -118,6 +118,8 @@ typedef struct {
   int32_t* m_j;
   int32_t* k_j;
   double* gamma_j;
+  int32_t* kscan_j;        /* Burgers only (nullable): Krylov dimension of the homogeneous scan
+                              step of subinterval j (index k*P + j; -1 = waveform written in-scan) */
 } pexp_stats;
 
 /* Create a context for one spatial operator A = nu*D2 - a*D1 on n points.

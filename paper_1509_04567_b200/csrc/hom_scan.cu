@@ -589,7 +589,7 @@ size_t hom_scan_bytes(int n, int s, int kcap, int P) {
 
 int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
                     double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
-                    double* delta, char* ws, size_t ws_bytes) {
+                    double* delta, char* ws, size_t ws_bytes, int* kscan_rec) {
   Arena ar{ws, ws_bytes, 0};
   ScanArgs a{};
   a.P = P; a.s = s; a.n = n; a.kcap = kcap; a.periodic = F.periodic;
@@ -642,6 +642,7 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   PEXP_CUDA_TRY(cudaMemcpyAsync(hf, a.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
   host_sync(st);
   if (hf[F_ERR]) fail(4 /* PEXP_ENOCONV */, "Krylov capacity reached (homogeneous scan)");
+  if (kscan_rec) PEXP_CUDA_TRY(cudaMemcpy(kscan_rec, a.kc, P * sizeof(int), cudaMemcpyDeviceToHost));
   return hf[F_KMAX];
 }
 

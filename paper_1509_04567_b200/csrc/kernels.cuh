@@ -173,7 +173,7 @@ bool hom_scan_ok(int n, int kcap);
 size_t hom_scan_bytes(int n, int s, int kcap, int P);
 int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
                     double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
-                    double* delta, char* ws, size_t ws_bytes);
+                    double* delta, char* ws, size_t ws_bytes, int* kscan_rec = nullptr);
 void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double* R, const double* TX, double* CPL,
                            int* Dn, int* Kl, const int* kplast, double* H, long long hs_e, int* live,
                            const int* active);

@@ -1170,10 +1170,10 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     const float ms = ev.ms();
     check_err(st);
     if (st_out) {
-      int32_t *mj = st_out->m_j, *kj = st_out->k_j;
+      int32_t *mj = st_out->m_j, *kj = st_out->k_j, *ksj = st_out->kscan_j;
       double* gj = st_out->gamma_j;
       std::memset(st_out, 0, sizeof(*st_out));
-      st_out->m_j = mj; st_out->k_j = kj; st_out->gamma_j = gj;
+      st_out->m_j = mj; st_out->k_j = kj; st_out->gamma_j = gj; st_out->kscan_j = ksj;
       if (mj) std::copy(me.begin(), me.end(), mj);
       if (kj) {
         PEXP_CUDA_TRY(cudaMemcpy(kj, L.B.krec, E * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1228,6 +1228,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
     int32_t* rec_m = st_out ? st_out->m_j : nullptr;
     int32_t* rec_k = st_out ? st_out->k_j : nullptr;
     double* rec_g = st_out ? st_out->gamma_j : nullptr;
+    int32_t* rec_ks = st_out ? st_out->kscan_j : nullptr;
     std::vector<double> dhist;
     std::vector<int> iota(P);
     for (int j = 0; j < P; ++j) iota[j] = j;
@@ -1272,7 +1273,8 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
         const int k1 = std::min(o.kcap, 512);
         const double defl_s = g_cfg.defl;
         max_k = std::max(max_k, launch_hom_scan(st, L.F, L.B.gam, P, s, n, k1, h, eta, defl_s, u0, L.Y, L.Uk, L.Un,
-                                                L.delta, L.scan_ws, L.scan_bytes));
+                                                L.delta, L.scan_ws, L.scan_bytes,
+                                                rec_ks ? rec_ks + size_t(k) * P : nullptr));
       } else
       for (int i = 0; i < P; ++i) {
         const size_t off = size_t(i) * s * n;
@@ -1313,7 +1315,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
     check_err(st);
     if (st_out) {
       std::memset(st_out, 0, sizeof(*st_out));
-      st_out->m_j = rec_m; st_out->k_j = rec_k; st_out->gamma_j = rec_g;
+      st_out->m_j = rec_m; st_out->k_j = rec_k; st_out->gamma_j = rec_g; st_out->kscan_j = rec_ks;
       for (int q = 0; q < std::min<int>(iters, 64); ++q) st_out->delta_hist[q] = dhist[q];
       st_out->host_syncs = g_cfg.syncs;
       st_out->wr_iters = iters;

@@ -44,10 +44,11 @@ class Stats(C.Structure):
                 ("max_k", C.c_int32), ("restarts", C.c_int32), ("best_residual", C.c_double),
                 ("ms_total", C.c_float), ("evals", C.c_int32), ("kernel_launches", C.c_int32),
                 ("host_syncs", C.c_int32), ("delta_hist", C.c_double * 64),
-                ("m_j", C.POINTER(C.c_int32)), ("k_j", C.POINTER(C.c_int32)), ("gamma_j", C.POINTER(C.c_double))]
+                ("m_j", C.POINTER(C.c_int32)), ("k_j", C.POINTER(C.c_int32)), ("gamma_j", C.POINTER(C.c_double)),
+                ("kscan_j", C.POINTER(C.c_int32))]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("delta_hist", "m_j", "k_j", "gamma_j")}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("delta_hist", "m_j", "k_j", "gamma_j", "kscan_j")}
         d["delta_hist"] = list(self.delta_hist[:min(max(self.wr_iters, 0), 64)])
         return d
 
@@ -179,8 +180,10 @@ class Context:
         st = Stats()
         if records:
             rm, rk, rg = _records(int(max_wr_iters) * P)
+            rs = (C.c_int32 * (int(max_wr_iters) * P))()
             st.m_j, st.k_j, st.gamma_j = (C.cast(rm, C.POINTER(C.c_int32)), C.cast(rk, C.POINTER(C.c_int32)),
                                            C.cast(rg, C.POINTER(C.c_double)))
+            st.kscan_j = C.cast(rs, C.POINTER(C.c_int32))
         self._check(_lib.pexp_solve_burgers(self._h, _dev(u0, "u0"), float(nu), float(T), int(P), float(tol),
                                             int(max_wr_iters), _dev(out, "out"), C.byref(st)))
         d = st.as_dict()
@@ -189,6 +192,7 @@ class Context:
             d["m_j"] = [list(rm[k * P:(k + 1) * P]) for k in range(K)]
             d["k_j"] = [list(rk[k * P:(k + 1) * P]) for k in range(K)]
             d["gamma_j"] = [list(rg[k * P:(k + 1) * P]) for k in range(K)]
+            d["kscan_j"] = [list(rs[k * P:(k + 1) * P]) for k in range(K)]
         return out, d
 
     def sai_solve(self, b: int, gamma: float, rhs: torch.Tensor) -> torch.Tensor:

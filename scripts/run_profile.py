@@ -51,14 +51,15 @@ pexp.profile_enable(True)
 out, st = run(True)
 prof = pexp.profile_read()
 pexp.profile_enable(False)
-res = {"stats": {k: v for k, v in st.items() if k not in ("m_j", "k_j", "gamma_j")},
+res = {"stats": {k: v for k, v in st.items() if k not in ("m_j", "k_j", "gamma_j", "kscan_j")},
        "profile": {k: {"ms": round(v["ms"], 2), "launches": v["launches"],
                        "GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] else None,
                        "TFps": round(v["flops"] / v["ms"] / 1e9, 3) if v["ms"] else None} for k, v in prof.items()}}
 if cfg["kind"] == "burgers":
     res["per_iter"] = [{"m_mean": float(np.mean(m)), "m_max": int(max(m)), "k_mean": float(np.mean(k)),
-                        "k_max": int(max(k)), "gamma_min": float(min(g))}
-                       for m, k, g in zip(st["m_j"], st["k_j"], st["gamma_j"])]
+                        "k_max": int(max(k)), "gamma_min": float(min(g)), "kscan_mean": float(np.mean(ks)),
+                        "kscan_max": int(max(ks))}
+                       for m, k, g, ks in zip(st["m_j"], st["k_j"], st["gamma_j"], st["kscan_j"])]
 else:
     res["m"] = st["m_j"][:64]
     res["k"] = st["k_j"][:64]
