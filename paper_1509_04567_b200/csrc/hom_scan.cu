@@ -106,6 +106,29 @@ __device__ inline void seg_dots(const double* V, int n, int row0, int nrow, int 
   __syncthreads();
 }
 
+// Composition of the affine maps maps[2*idx], maps[2*idx+1] for idx = first, first + step, ...
+// (cnt maps, in that order) applied to 0: the carry into a segment.  One warp: every lane
+// composes a contiguous run of the list (independent loads in flight), then an ordered tree over
+// the lanes.  Result valid in lane 0.
+__device__ inline double warp_carry(const double* maps, int first, int step, int cnt) {
+  const int lane = threadIdx.x & 31;
+  const int q = (cnt + 31) / 32;
+  Aff v{1.0, 0.0};
+  for (int t = 0; t < q; ++t) {
+    const int k = lane * q + t;
+    if (k < cnt) {
+      const int idx = first + k * step;
+      v = after(v, Aff{__ldcg(maps + 2 * idx), __ldcg(maps + 2 * idx + 1)});
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double oa = __shfl_down_sync(0xffffffffu, v.A, o), ob = __shfl_down_sync(0xffffffffu, v.B, o);
+    if ((lane & (2 * o - 1)) == 0 && lane + o < 32) v = after(v, Aff{oa, ob});
+  }
+  return v.B;
+}
+
 }  // namespace
 
 struct ScanArgs {
@@ -353,10 +376,9 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
             break;
           }
           // B: carry from lower segments; y; backward maps x_g = -di_g cs_g x_{g+1} + di_g y_g
-          if (threadIdx.x == 0) {
-            double cy = 0.0;
-            for (int cc = 0; cc < c; ++cc) cy = fma(__ldcg(a.maps + 2 * cc), cy, __ldcg(a.maps + 2 * cc + 1));
-            hv[0] = cy;
+          if (threadIdx.x < 32) {
+            const double cy = warp_carry(a.maps, 0, 1, c);  // segments 0 .. c-1, ascending
+            if (threadIdx.x == 0) hv[0] = cy;
           }
           __syncthreads();
           double y = fma(pre.A, hv[0], pre.B);
@@ -383,11 +405,9 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           }
           gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
           // C: carry from upper segments; x; SM correction; pass-1 dots
-          if (threadIdx.x == 0) {
-            double cx = 0.0;
-            for (int cc = a.nw - 1; cc > c; --cc)
-              cx = fma(__ldcg(a.maps + 2 * a.nw + 2 * cc), cx, __ldcg(a.maps + 2 * a.nw + 2 * cc + 1));
-            hv[0] = cx;
+          if (threadIdx.x < 32) {  // segments nw-1 .. c+1, descending
+            const double cx = warp_carry(a.maps + 2 * a.nw, a.nw - 1, -1, a.nw - 1 - c);
+            if (threadIdx.x == 0) hv[0] = cx;
           }
           if (a.periodic) grid_reduce(a.partA, pw, a.nw, PF, 1, hv2);
           __syncthreads();
