@@ -58,11 +58,13 @@ __device__ inline void gbar(unsigned* cnt, unsigned* gen, unsigned nb) {
   __syncthreads();
 }
 
-// Sum over CTAs of part[c*pw + j] for j < nval, in a fixed order; result to out[j] (smem).
-// Few CTAs (<= 32): one thread per value sums the CTAs in order (independent loads in flight);
-// many CTAs: one warp per value, lanes stride over the CTAs, then a warp tree.
+// Sum over CTAs of part[c*pw + j0 + j] for j < nval, in a fixed order; result to out[j] (smem).
+// The NT threads form ng = NT / nval groups; group q sums CTAs q, q + ng, ... for its value j
+// (independent loads, all in flight), the ng group partials are then summed in group order.  Every
+// CTA computes the identical result.  out must hold >= NT doubles (scratch for the partials).
 __device__ inline void grid_reduce(const double* part, int pw, int ncta, int j0, int nval, double* out) {
-  if (ncta <= 32) {
+  if (nval <= 0) return;
+  if (nval > NT / 2) {  // wide: one thread per value, CTAs in order
     for (int j = threadIdx.x; j < nval; j += NT) {
       double a = 0.0;
       for (int c = 0; c < ncta; ++c) a += __ldcg(part + size_t(c) * pw + j0 + j);
@@ -71,13 +73,19 @@ __device__ inline void grid_reduce(const double* part, int pw, int ncta, int j0,
     __syncthreads();
     return;
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int j = w; j < nval; j += NT / 32) {
-    double a = 0.0;
-    for (int c = lane; c < ncta; c += 32) a += __ldcg(part + size_t(c) * pw + j0 + j);
-    a = warp_sum(a);
-    if (lane == 0) out[j] = a;
-  }
+  const int ng = NT / nval;
+  const int j = threadIdx.x % nval, q = threadIdx.x / nval;
+  double a = 0.0;
+  if (q < ng)
+    for (int c = q; c < ncta; c += ng) a += __ldcg(part + size_t(c) * pw + j0 + j);
+  __syncthreads();  // out may still be read by the caller's previous use
+  if (q < ng) out[q * nval + j] = a;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < nval)
+    for (int g = 0; g < ng; ++g) t += out[g * nval + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < nval) out[threadIdx.x] = t;
   __syncthreads();
 }
 
@@ -422,11 +430,10 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
             }
           }
           const int kk = k + 1;  // columns 0..k
-          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partA + size_t(c) * pw, PN);
+          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partA + size_t(c) * pw, kk);
           gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
           // D: h = V^T x; x -= V h; pass-2 dots
-          grid_reduce(a.partA, pw, a.nw, 0, kk, hv);
-          grid_reduce(a.partA, pw, a.nw, PN, 1, hv + kk);
+          grid_reduce(a.partA, pw, a.nw, 0, kk + 1, hv);  // h = V^T x and ||x||^2 (at kk)
           const double nrm0 = sqrt(hv[kk]);
           for (int q = 0; q < rpt; ++q) {
             const int g = row0 + threadIdx.x * rpt + q;
@@ -436,11 +443,10 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
               xr[q] = v;
             }
           }
-          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partB + size_t(c) * pw, PN);
+          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partB + size_t(c) * pw, kk);
           gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
           // E: second pass, norm, new column
-          grid_reduce(a.partB, pw, a.nw, 0, kk, hv2);
-          grid_reduce(a.partB, pw, a.nw, PN, 1, hv2 + kk);
+          grid_reduce(a.partB, pw, a.nw, 0, kk + 1, hv2);
           double h2n = 0.0;
           for (int j = 0; j < kk; ++j) h2n = fma(hv2[j], hv2[j], h2n);
           const double hn = sqrt(fmax(hv2[kk] - h2n, 0.0));
