@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   const int row0 = c * a.seg;
   const int rend = min(n, row0 + a.seg);
   double uh[RPT_MAX], xr[RPT_MAX], vr[RPT_MAX];
+  int kconv_prev = 0;  // checker: converged dimension of the previous subinterval (thread 0)
 
   // ---- subinterval 0: no homogeneous part; u_hat(T_1) = Y(T_1) (its waveform u0 + Y is written by
   // k_scan_output after the scan)
@@ -294,7 +295,9 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
         const double crit = a.eta * beta / ((s - 1) * a.h);
         double* z = hv;
         double* zn = hv2;
-        int target = min(4, a.kcap - 1), Kprev = -1;
+        // first check just below the previous subinterval's converged dimension (the operators of
+        // neighbouring subintervals are close), then extrapolate the residual decay
+        int target = min(max(4, kconv_prev - 3), a.kcap - 1), Kprev = -1;
         double qprev = -1.0;
         while (true) {
           if (threadIdx.x == 0) {
@@ -315,7 +318,10 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           const double res = hom_check(a, Zi, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
           if (threadIdx.x == 0) {
             int result = 0;
-            if (brk || res <= crit) result = K;
+            if (brk || res <= crit) {
+              result = K;
+              kconv_prev = K;
+            }
             else if (K >= a.kcap - 1) result = -1;
             if (result != 0) {
               __threadfence();
