@@ -6,7 +6,9 @@ Follows Fig. 5 and §2.4:
      J_{k,j} = J(ū_j)                                            (Eq.(piecewiseJac) P:297-301, reading #3)
   2. operator A_j = ν D2 + J_{k,j}; shifted source at the nodes
         ĝ_{j,k}(t) = A u0 + g_k(t) - J_{k,j} û_k(t)
-                   = ν D2 u0 - u_k∘D1 u_k - J_{k,j}(u_k - u0)      (Eq.(sourceParallel), corrected: reading #2)
+                   = ν D2 u0 - u_k∘D1 u_k - J_{k,j}(u_k - u0) + f(t)
+                                                                 (Eq.(sourceParallel) P:312, corrected: reading #2;
+                                                                  forcing f of Eq.(burgersEq), f2 workloads)
   3. nonhomogeneous parts v_{j,k+1} on [T_{j-1}, T_j] by EBK      (Eq.(ivpSubproblem))
   4. homogeneous parts: v_j continued over later subintervals with each subinterval's own
      operator; summed first (linearity), this is the scan
@@ -43,8 +45,9 @@ def wr_gamma(ubar: np.ndarray, D1, dT: float) -> float:
     return g
 
 
-def wr_map(Uk, u0, nu, n, T, P, s, tol, *, eta=1e-12, dense_max=1024, svd_tau_factor=0.01, info=None):
-    """One WR iteration u_k -> u_{k+1} on all nodes; Uk: [P][s][n]."""
+def wr_map(Uk, u0, nu, n, T, P, s, tol, *, eta=1e-12, dense_max=1024, svd_tau_factor=0.01, info=None,
+           f=None):
+    """One WR iteration u_k -> u_{k+1} on all nodes; Uk: [P][s][n]; f: forcing [P][s][n] or None."""
     dT = T / P
     h = dT / (s - 1)
     D1 = d1_matrix(n)
@@ -67,6 +70,8 @@ def wr_map(Uk, u0, nu, n, T, P, s, tol, *, eta=1e-12, dense_max=1024, svd_tau_fa
         for i in range(s):
             u = Ukj[i]
             G[:, i] = A0u0 - u * (D1 @ u) - J @ (u - u0)
+            if f is not None:
+                G[:, i] += f[j, i]
         U, C, _ = truncated_svd(G, svd_tau_factor * tol)
         if info is not None:
             info.setdefault("m", []).append(U.shape[1])
@@ -93,9 +98,10 @@ def wr_map(Uk, u0, nu, n, T, P, s, tol, *, eta=1e-12, dense_max=1024, svd_tau_fa
 
 
 def solve_burgers(n, nu, u0, T, P, s, tol, max_wr_iters=30, wr_tol=1e-6, *, eta=1e-12,
-                  dense_max=1024, svd_tau_factor=0.01, return_info=False, fixed_iters=None):
+                  dense_max=1024, svd_tau_factor=0.01, return_info=False, fixed_iters=None, f=None):
     """Returns out [P][n] = u_K(T_1..T_P) (reading #12) and optionally info
-    {"iters": K, "delta": [...], "U": final waveform [P][s][n]}."""
+    {"iters": K, "delta": [...], "U": final waveform [P][s][n], "out_hist": [u_k(T_1..T_P)]}.
+    f: forcing samples [P][s][n] at the nodes (Eq.(burgersEq)), None for f = 0."""
     u0 = np.asarray(u0, dtype=np.float64)
     Uk = np.broadcast_to(u0, (P, s, n)).copy()      # step 0
     deltas = []
@@ -103,7 +109,8 @@ def solve_burgers(n, nu, u0, T, P, s, tol, max_wr_iters=30, wr_tol=1e-6, *, eta=
     kmax = max_wr_iters if fixed_iters is None else fixed_iters
     for k in range(kmax):
         Un = wr_map(Uk, u0, nu, n, T, P, s, tol, eta=eta, dense_max=dense_max,
-                    svd_tau_factor=svd_tau_factor, info=info)
+                    svd_tau_factor=svd_tau_factor, info=info, f=f)
+        info.setdefault("out_hist", []).append(Un[:, -1, :].copy())
         d = float(np.max(np.abs(Un - Uk)))
         deltas.append(d)
         Uk = Un

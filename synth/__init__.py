@@ -18,3 +18,11 @@ from .configs import (  # noqa: F401
     generic_linear,
     make_config,
 )
+from .paper_workloads import (  # noqa: F401,E402
+    pulse_ade,
+    pulse_exact,
+    sawtooth_burgers,
+    sawtooth_exact,
+    multiscale_burgers,
+    multiscale_exact,
+)

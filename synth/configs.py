@@ -67,7 +67,7 @@ class LinearProblem:
 
 @dataclass
 class BurgersProblem:
-    """u' = nu*D2 u - u∘(D1 u) (PAPER.md:636 with f = 0), periodic."""
+    """u' = nu*D2 u - u∘(D1 u) + f (f = 0 for C3/C5), periodic."""
     name: str
     n: int
     nu: float
@@ -79,6 +79,7 @@ class BurgersProblem:
     max_wr_iters: int = 30
     wr_tol: float = 1e-6
     bc: str = PERIODIC
+    f: Optional[np.ndarray] = None   # [P][s][n] forcing f(x, t_{j,i}) of Eq.(burgersEq) P:636 (None: f = 0)
 
 
 def _fourier(x, k, c, s_):

@@ -67,3 +67,18 @@ def periodic_propagate(n, nu, a, v, t):
     """exp(tA) v for the periodic ADE operator (circulant closed form)."""
     lam = periodic_eigs(n, nu, a)
     return np.real(np.fft.ifft(np.exp(lam * t) * np.fft.fft(v)))
+
+
+def pulse_semidiscrete(x, t, nu, a, n):
+    """Exact solution of the periodic semi-discrete f1 problem (Eq.(ade)/(manusol) P:555-563)
+    u' = (νD2 - aD1)u + f(t), f = -50π²ν cos(10π(x - a t)), u(0) = 1/2 - 1/2 cos(10πx).
+    Single circulant mode k = 10π: u = 1/2 + Re(c(t) e^{ikx}), c' = λc + F e^{-iωt},
+    λ = ν(2cos(kΔx) - 2)/Δx² - i a sin(kΔx)/Δx, F = -50π²ν, ω = k a, c(0) = -1/2:
+        c(t) = e^{λt} c(0) + F (e^{-iωt} - e^{λt}) / (-iω - λ)."""
+    k = 10 * np.pi
+    dx = 1.0 / n
+    lam = nu * (2 * np.cos(k * dx) - 2) / dx ** 2 - 1j * a * np.sin(k * dx) / dx
+    F = -50 * np.pi ** 2 * nu
+    w = k * a
+    c = np.exp(lam * t) * (-0.5) + F * (np.exp(-1j * w * t) - np.exp(lam * t)) / (-1j * w - lam)
+    return 0.5 + np.real(c * np.exp(1j * k * x))
