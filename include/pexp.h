@@ -163,6 +163,17 @@ PEXP_API pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const do
 PEXP_API pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, double T, int32_t P,
                                double tol, int32_t max_wr_iters, double* out, pexp_stats* st);
 
+/* Forced Burgers u' = nu*D2 u - u∘(D1 u) + f(x,t) (Eq.(burgersEq); the paper's
+ * sawtooth and multiscale workloads).  As pexp_solve_burgers, plus
+ *   f   dev [P][s][n]  forcing samples f(x, t_{j,i}) at the sample nodes (header comment),
+ *                      nullable (NULL = unforced).  The sample at T_j appears twice: as
+ *                      f[j-1][s-1] and f[j][0].
+ * The forcing enters the shifted source of Eq.(sourceParallel) P:312 (reading #2) as
+ * g_k(t) = -u_k∘(D1 u_k) + f(t); nothing else changes. */
+PEXP_API pexp_status pexp_solve_burgers_forced(pexp_ctx* ctx, const double* u0, const double* f, double nu,
+                                      double T, int32_t P, double tol, int32_t max_wr_iters,
+                                      double* out, pexp_stats* st);
+
 /* ---- Stage entry points (same kernels as the solves; used by stage-parity tests) ---- */
 
 /* One batch of shift-and-invert solves (subsystem 1): x = (I - gamma*A_b)^{-1} rhs for

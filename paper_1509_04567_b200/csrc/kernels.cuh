@@ -211,7 +211,7 @@ void launch_broadcast_waveform(cudaStream_t st, int P, int s, int n, const doubl
 void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, double dT, double* ubar,
                        double* gam);
 void launch_burgers_source(cudaStream_t st, int P, int s, int n, double nu, const double* u0, const double* U,
-                           const double* ubar, double* G);
+                           const double* ubar, const double* f, double* G);
 void launch_wr_step(cudaStream_t st, int s, int n, const double* u0, const double* Wh, const double* Y,
                     const double* Uold, double* Unew, double* uhat_end, double* delta);
 void launch_superpose(cudaStream_t st, int batch, int P, int n, const double* u0, const double* Yend,

@@ -1200,6 +1200,12 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
 
 pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, double T, int32_t P, double tol,
                                int32_t max_wr_iters, double* out, pexp_stats* st_out) {
+  return pexp_solve_burgers_forced(ctx, u0, nullptr, nu, T, P, tol, max_wr_iters, out, st_out);
+}
+
+pexp_status pexp_solve_burgers_forced(pexp_ctx* ctx, const double* u0, const double* f, double nu, double T,
+                                      int32_t P, double tol, int32_t max_wr_iters, double* out,
+                                      pexp_stats* st_out) {
   if (!ctx) return PEXP_EINVAL;
   if (!u0 || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
   if (ctx->bc != PEXP_BC_PERIODIC || ctx->batch != 1)
@@ -1244,7 +1250,7 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
       PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
       SideFactor sf(ctx, st);
       launch_factor(sf.stream(), L.F, P, L.iota, L.B.gam, L.O, L.err);
-      launch_burgers_source(st, P, s, n, nu, u0, L.Uk, L.ubar, L.G);
+      launch_burgers_source(st, P, s, n, nu, u0, L.Uk, L.ubar, f, L.G);
       std::vector<int> me(E);
       int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, me.data());
       sf.join();

@@ -88,8 +88,9 @@ __global__ void k_gamma(int n, const double* ubar, double dT, double* gam) {
 
 // Shifted WR source at the nodes (Eq.(sourceParallel) PAPER.md:312 with reading #2):
 //   G = nu D2 u0 - u∘D1u - J(ubar)(u - u0),  J(ubar) v = -(D1 ubar)∘v - ubar∘(D1 v)
+// f (nullable): forcing samples f(x, t_{j,i}) of Eq.(burgersEq), [P][s][n]
 __global__ void k_burgers_source(int s, int n, double nu, const double* u0, const double* U, const double* ubar,
-                                 double* G) {
+                                 const double* f, double* G) {
   const int i = blockIdx.y, j = blockIdx.z;
   const double* u = U + (size_t(j) * s + i) * n;
   const double* ub = ubar + size_t(j) * n;
@@ -102,7 +103,9 @@ __global__ void k_burgers_source(int s, int n, double nu, const double* u0, cons
     double d1ub = (ub[rp] - ub[rm]) * inv2dx;
     double v = u[r] - u0[r], vm = u[rm] - u0[rm], vp = u[rp] - u0[rp];
     double d1v = (vp - vm) * inv2dx;
-    g[r] = nu * d2u0 - u[r] * d1u + d1ub * v + ub[r] * d1v;
+    double gv = nu * d2u0 - u[r] * d1u + d1ub * v + ub[r] * d1v;
+    if (f) gv += f[(size_t(j) * s + i) * n + r];
+    g[r] = gv;
   }
 }
 
@@ -397,10 +400,10 @@ void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, do
 }
 
 void launch_burgers_source(cudaStream_t st, int P, int s, int n, double nu, const double* u0, const double* U,
-                           const double* ubar, double* G) {
+                           const double* ubar, const double* f, double* G) {
   dim3 grid(gx_small(n, P * s), s, P);
   { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
-  k_burgers_source<<<grid, PEXP_THREADS, 0, st>>>(s, n, nu, u0, U, ubar, G);
+  k_burgers_source<<<grid, PEXP_THREADS, 0, st>>>(s, n, nu, u0, U, ubar, f, G);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();

@@ -25,6 +25,7 @@ BC = {"periodic": 0, "dirichlet": 1}
 
 EXPORTED = ["pexp_create", "pexp_create_batched", "pexp_destroy", "pexp_last_error", "pexp_sample_times",
             "pexp_workspace_bytes", "pexp_set_workspace", "pexp_solve_linear", "pexp_solve_burgers",
+            "pexp_solve_burgers_forced",
             "pexp_sai_solve", "pexp_source_svd", "pexp_expm_batched", "pexp_profile_enable", "pexp_profile_read"]
 PROFILE_CLASSES = ["sai_solve", "xty", "combine", "small_problem", "small_dense", "stencil", "factor",
                    "arnoldi_step", "hom_scan", "small_hom", "stream_proj", "stream_update",
@@ -76,6 +77,8 @@ _lib.pexp_set_workspace.argtypes = [_P, _P, C.c_size_t]
 _lib.pexp_solve_linear.argtypes = [_P, _P, _P, C.c_double, C.c_int32, C.c_double, _P, C.POINTER(Stats)]
 _lib.pexp_solve_burgers.argtypes = [_P, _P, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_int32, _P,
                                     C.POINTER(Stats)]
+_lib.pexp_solve_burgers_forced.argtypes = [_P, _P, _P, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_int32, _P,
+                                           C.POINTER(Stats)]
 _lib.pexp_sai_solve.argtypes = [_P, C.c_int32, C.c_double, _P, C.c_int32, _P]
 _lib.pexp_source_svd.argtypes = [_P, _P, C.c_int32, C.c_double, C.POINTER(C.c_int32), _P, _P]
 _lib.pexp_expm_batched.argtypes = [_P, _P, C.c_int32, C.c_int32, _P]
@@ -173,8 +176,12 @@ class Context:
         return out, d
 
     def solve_burgers(self, u0: torch.Tensor, nu: float, T: float, P: int, tol: float, max_wr_iters: int = 30,
-                      out: Optional[torch.Tensor] = None, records: bool = False):
+                      out: Optional[torch.Tensor] = None, records: bool = False,
+                      f: Optional[torch.Tensor] = None):
+        """f: forcing samples [P][s][n] at the sample nodes (pexp_solve_burgers_forced), None = unforced."""
         self.ensure_workspace(P, u0.device, kind=1)
+        if f is not None and tuple(f.shape) != (P, self.s, self.n):
+            raise ValueError("f must have shape [P][s][n]")
         if out is None:
             out = torch.empty((P, self.n), dtype=torch.float64, device=u0.device)
         st = Stats()
@@ -184,8 +191,13 @@ class Context:
             st.m_j, st.k_j, st.gamma_j = (C.cast(rm, C.POINTER(C.c_int32)), C.cast(rk, C.POINTER(C.c_int32)),
                                            C.cast(rg, C.POINTER(C.c_double)))
             st.kscan_j = C.cast(rs, C.POINTER(C.c_int32))
-        self._check(_lib.pexp_solve_burgers(self._h, _dev(u0, "u0"), float(nu), float(T), int(P), float(tol),
-                                            int(max_wr_iters), _dev(out, "out"), C.byref(st)))
+        if f is None:
+            self._check(_lib.pexp_solve_burgers(self._h, _dev(u0, "u0"), float(nu), float(T), int(P), float(tol),
+                                                int(max_wr_iters), _dev(out, "out"), C.byref(st)))
+        else:
+            self._check(_lib.pexp_solve_burgers_forced(self._h, _dev(u0, "u0"), _dev(f, "f"), float(nu), float(T),
+                                                       int(P), float(tol), int(max_wr_iters), _dev(out, "out"),
+                                                       C.byref(st)))
         d = st.as_dict()
         if records:
             K = d["wr_iters"]
