@@ -176,6 +176,28 @@ PEXP_API pexp_status pexp_solve_burgers_forced(pexp_ctx* ctx, const double* u0, 
 
 /* ---- Stage entry points (same kernels as the solves; used by stage-parity tests) ---- */
 
+/* Linear solve with its stage results exposed (stage parity of SURVEY §8(c).5).  As
+ * pexp_solve_linear, plus
+ *   vstart dev [batch][P][n], nullable: when given, the nonhomogeneous stage is skipped and the
+ *          homogeneous legs start from v_j(T_j) := vstart[b][j-1] (src may then be NULL);
+ *   vend   dev [batch][P][n], nullable: receives v_j(T_j), j = 1..P, the nonhomogeneous parts at
+ *          their subinterval ends (Eq.(linivpSubproblem));
+ *   legs   dev [batch][G][P][n], nullable, G = ceil((P-1)/hom_group): legs[b][g][i] receives the
+ *          sum over the legs j of group g (j = g*hom_group+1 ...) of exp((T_{i+1}-T_j)A) v_j(T_j)
+ *          for T_{i+1} > T_j (Fig. 2 "Solve homogeneous part"); with hom_group = 1 group g
+ *          holds the single leg j = g+1. */
+PEXP_API pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const double* src,
+                                     const double* vstart, double T, int32_t P, double tol, double* out,
+                                     double* vend, double* legs, pexp_stats* st);
+
+/* One waveform-relaxation map u_k -> u_{k+1} = F(u_k) (Eq.(ivpSubproblem)/(updateSolution)
+ * P:326-335; one pass of Fig. 5's loop body) from a caller-supplied iterate:
+ *   Uk   dev [P][s][n]  u_k at the sample nodes;  Unew dev [P][s][n] receives u_{k+1};
+ *   out  dev [P][n]     u_{k+1}(T_1..T_P);  f nullable (pexp_solve_burgers_forced);
+ *   st->wr_last_delta = max|u_{k+1} - u_k|. */
+PEXP_API pexp_status pexp_wr_map(pexp_ctx* ctx, const double* u0, const double* f, const double* Uk, double nu,
+                        double T, int32_t P, double tol, double* Unew, double* out, pexp_stats* st);
+
 /* One batch of shift-and-invert solves (subsystem 1): x = (I - gamma*A_b)^{-1} rhs for
  * problem b of the context, every column c of rhs dev [ncols][n] -> x dev [ncols][n]. */
 PEXP_API pexp_status pexp_sai_solve(pexp_ctx* ctx, int32_t b, double gamma, const double* rhs,

@@ -1071,8 +1071,14 @@ pexp_status pexp_set_workspace(pexp_ctx* ctx, void* dev_ptr, size_t bytes) {
 
 pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src, double T, int32_t P, double tol,
                               double* out, pexp_stats* st_out) {
+  return pexp_solve_linear_stages(ctx, u0, src, nullptr, T, P, tol, out, nullptr, nullptr, st_out);
+}
+
+pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const double* src, const double* vstart,
+                                     double T, int32_t P, double tol, double* out, double* vend, double* legs,
+                                     pexp_stats* st_out) {
   if (!ctx) return PEXP_EINVAL;
-  if (!u0 || !src || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
+  if (!u0 || (!src && !vstart) || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
   if (!(T > 0) || !std::isfinite(T)) return set_err(ctx, PEXP_EINVAL, "T must be > 0");
   if (P < 1) return set_err(ctx, PEXP_EINVAL, "P must be >= 1");
   if (!(tol >= 1e-14 && tol <= 1e-2)) return set_err(ctx, PEXP_EINVAL, "tol must be in [1e-14, 1e-2]");
@@ -1105,18 +1111,21 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
     SideFactor sf(ctx, st);
     launch_factor(sf.stream(), L.F, 2 * Bt, L.opidx_f, L.gam_f, L.O, L.err);
-    // shifted source G = A u0 + g at the nodes
-    launch_apply_A(st, L.O, L.iota, Bt, 1, u0, n, 0, L.Au0, n, 0, periodic);
-    launch_lin_source(st, Bt, P, s, n, L.Au0, src, L.G);
-    // per-eval maps for the nonhomogeneous batch
-    std::vector<int> fe(E);
-    std::vector<double> ge(E, dT / 10);
-    for (int e = 0; e < E; ++e) fe[e] = e / P;
-    h2d(st, L.B.fidx, fe);
-    h2d(st, L.B.opidx, fe);
-    h2d(st, L.B.gam, ge);
-    std::vector<int> me(E);
-    int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, me.data());
+    std::vector<int> me(E, 0);
+    int mmax = 0;
+    if (!vstart) {
+      // shifted source G = A u0 + g at the nodes
+      launch_apply_A(st, L.O, L.iota, Bt, 1, u0, n, 0, L.Au0, n, 0, periodic);
+      launch_lin_source(st, Bt, P, s, n, L.Au0, src, L.G);
+      // per-eval maps for the nonhomogeneous batch
+      std::vector<int> fe(E);
+      std::vector<double> ge(E, dT / 10);
+      for (int e = 0; e < E; ++e) fe[e] = e / P;
+      h2d(st, L.B.fidx, fe);
+      h2d(st, L.B.opidx, fe);
+      h2d(st, L.B.gam, ge);
+      mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, me.data());
+    }
     sf.join();
     int herr = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1124,12 +1133,15 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
     if (herr) fail(PEXP_EPIVOT, "shift-and-invert factorisation: a pivot is zero relative to its row or non-finite");
     launch_fill_i32(st, L.B.krec, E, 0);
     RunInfo ri{}, rh{};
-    if (mmax > 0) {
+    if (vstart) {  // stage entry: the homogeneous legs start from the caller's v_j(T_j)
+      PEXP_CUDA_TRY(cudaMemcpyAsync(L.Yend, vstart, size_t(E) * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    } else if (mmax > 0) {
       ri = ebk_forced(st, L.B, L.S, L.F, L.O, periodic, E, mmax, me.data(), h, s, s - 1, 2, 1, L.Yend, n, o.stop_rule,
                       o.restart_blocks);
     } else {
       PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
     }
+    if (vend) PEXP_CUDA_TRY(cudaMemcpyAsync(vend, L.Yend, size_t(E) * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     int G = 0;
     if (P > 1) {
       // homogeneous legs, grouped: up to 16 consecutive legs share one block Krylov space
@@ -1163,6 +1175,8 @@ pexp_status pexp_solve_linear(pexp_ctx* ctx, const double* u0, const double* src
       launch_combine(st, Eg, n, Bh.V, Bh.vs_e, 0, std::max(rh.max_k, 1), Bh.Z, Bh.zs_e, Bh.kcap, L.Yh,
                      (long long)P * n, 0, P, 1.0, 0.0, nullptr, Bh.kfin);
     }
+    if (legs && P > 1)
+      PEXP_CUDA_TRY(cudaMemcpyAsync(legs, L.Yh, size_t(Bt) * G * P * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     launch_superpose(st, Bt, P, n, u0, L.Yend, P > 1 ? L.Yh : nullptr, (long long)P * n, n, G, out);
     PEXP_CUDA_TRY(cudaEventRecord(ev.b, st));
     PEXP_CUDA_TRY(cudaEventSynchronize(ev.b));
@@ -1203,9 +1217,25 @@ pexp_status pexp_solve_burgers(pexp_ctx* ctx, const double* u0, double nu, doubl
   return pexp_solve_burgers_forced(ctx, u0, nullptr, nu, T, P, tol, max_wr_iters, out, st_out);
 }
 
+static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f, const double* Uinit, double nu,
+                                double T, int32_t P, double tol, int32_t max_wr_iters, double* out, double* Uout,
+                                pexp_stats* st_out);
+
 pexp_status pexp_solve_burgers_forced(pexp_ctx* ctx, const double* u0, const double* f, double nu, double T,
                                       int32_t P, double tol, int32_t max_wr_iters, double* out,
                                       pexp_stats* st_out) {
+  return burgers_impl(ctx, u0, f, nullptr, nu, T, P, tol, max_wr_iters, out, nullptr, st_out);
+}
+
+pexp_status pexp_wr_map(pexp_ctx* ctx, const double* u0, const double* f, const double* Uk, double nu, double T,
+                        int32_t P, double tol, double* Unew, double* out, pexp_stats* st_out) {
+  if (!Uk || !Unew) return set_err(ctx, PEXP_EINVAL, "null array argument");
+  return burgers_impl(ctx, u0, f, Uk, nu, T, P, tol, 1, out, Unew, st_out);
+}
+
+static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f, const double* Uinit, double nu,
+                                double T, int32_t P, double tol, int32_t max_wr_iters, double* out, double* Uout,
+                                pexp_stats* st_out) {
   if (!ctx) return PEXP_EINVAL;
   if (!u0 || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
   if (ctx->bc != PEXP_BC_PERIODIC || ctx->batch != 1)
@@ -1241,7 +1271,10 @@ pexp_status pexp_solve_burgers_forced(pexp_ctx* ctx, const double* u0, const dou
     h2d(st, L.iota, iota);
     h2d(st, L.B.fidx, iota);
     h2d(st, L.B.opidx, iota);
-    launch_broadcast_waveform(st, P, s, n, u0, L.Uk);
+    if (Uinit)  // stage entry pexp_wr_map: start from the caller's waveform u_k
+      PEXP_CUDA_TRY(cudaMemcpyAsync(L.Uk, Uinit, size_t(P) * s * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    else
+      launch_broadcast_waveform(st, P, s, n, u0, L.Uk);
     int iters = 0, max_m = 0, max_k = 0, restarts = 0;
     double delta = 0.0, delta0 = -1.0;
     for (int k = 0; k < max_wr_iters; ++k) {
@@ -1314,6 +1347,7 @@ pexp_status pexp_solve_burgers_forced(pexp_ctx* ctx, const double* u0, const dou
       if (delta < wr_tol) break;
     }
     launch_copy_end(st, P, s, n, L.Uk, out);
+    if (Uout) PEXP_CUDA_TRY(cudaMemcpyAsync(Uout, L.Uk, size_t(P) * s * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     PEXP_CUDA_TRY(cudaEventRecord(ev.b, st));
     PEXP_CUDA_TRY(cudaEventSynchronize(ev.b));
     ++g_cfg.syncs;

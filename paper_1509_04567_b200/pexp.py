@@ -25,7 +25,7 @@ BC = {"periodic": 0, "dirichlet": 1}
 
 EXPORTED = ["pexp_create", "pexp_create_batched", "pexp_destroy", "pexp_last_error", "pexp_sample_times",
             "pexp_workspace_bytes", "pexp_set_workspace", "pexp_solve_linear", "pexp_solve_burgers",
-            "pexp_solve_burgers_forced",
+            "pexp_solve_burgers_forced", "pexp_solve_linear_stages", "pexp_wr_map",
             "pexp_sai_solve", "pexp_source_svd", "pexp_expm_batched", "pexp_profile_enable", "pexp_profile_read"]
 PROFILE_CLASSES = ["sai_solve", "xty", "combine", "small_problem", "small_dense", "stencil", "factor",
                    "arnoldi_step", "hom_scan", "small_hom", "stream_proj", "stream_update",
@@ -79,6 +79,9 @@ _lib.pexp_solve_burgers.argtypes = [_P, _P, C.c_double, C.c_double, C.c_int32, C
                                     C.POINTER(Stats)]
 _lib.pexp_solve_burgers_forced.argtypes = [_P, _P, _P, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_int32, _P,
                                            C.POINTER(Stats)]
+_lib.pexp_solve_linear_stages.argtypes = [_P, _P, _P, _P, C.c_double, C.c_int32, C.c_double, _P, _P, _P,
+                                          C.POINTER(Stats)]
+_lib.pexp_wr_map.argtypes = [_P, _P, _P, _P, C.c_double, C.c_double, C.c_int32, C.c_double, _P, _P, C.POINTER(Stats)]
 _lib.pexp_sai_solve.argtypes = [_P, C.c_int32, C.c_double, _P, C.c_int32, _P]
 _lib.pexp_source_svd.argtypes = [_P, _P, C.c_int32, C.c_double, C.POINTER(C.c_int32), _P, _P]
 _lib.pexp_expm_batched.argtypes = [_P, _P, C.c_int32, C.c_int32, _P]
@@ -206,6 +209,32 @@ class Context:
             d["gamma_j"] = [list(rg[k * P:(k + 1) * P]) for k in range(K)]
             d["kscan_j"] = [list(rs[k * P:(k + 1) * P]) for k in range(K)]
         return out, d
+
+    def solve_linear_stages(self, u0, src, T, P, tol, vstart=None, hom_group=None):
+        """pexp_solve_linear_stages: returns (out, vend [batch][P][n], legs [batch][G][P][n], stats)."""
+        self.ensure_workspace(P, u0.device)
+        hg = self.opt.hom_group if self.opt.hom_group > 0 else 8
+        G = max(1, -(-(P - 1) // max(1, min(hg, P - 1)))) if P > 1 else 1
+        out = torch.empty((self.batch, P, self.n), dtype=torch.float64, device=u0.device)
+        vend = torch.empty_like(out)
+        legs = torch.zeros((self.batch, G, P, self.n), dtype=torch.float64, device=u0.device)
+        st = Stats()
+        self._check(_lib.pexp_solve_linear_stages(
+            self._h, _dev(u0, "u0"), None if src is None else _dev(src, "src"),
+            None if vstart is None else _dev(vstart, "vstart"), float(T), int(P), float(tol), _dev(out, "out"),
+            _dev(vend, "vend"), _dev(legs, "legs"), C.byref(st)))
+        return out, vend, legs, st.as_dict()
+
+    def wr_map(self, u0, Uk, nu, T, P, tol, f=None):
+        """pexp_wr_map: one WR map u_k -> u_{k+1}; returns (Unew [P][s][n], out [P][n], stats)."""
+        self.ensure_workspace(P, u0.device, kind=1)
+        Unew = torch.empty_like(Uk)
+        out = torch.empty((P, self.n), dtype=torch.float64, device=u0.device)
+        st = Stats()
+        self._check(_lib.pexp_wr_map(self._h, _dev(u0, "u0"), None if f is None else _dev(f, "f"), _dev(Uk, "Uk"),
+                                     float(nu), float(T), int(P), float(tol), _dev(Unew, "Unew"), _dev(out, "out"),
+                                     C.byref(st)))
+        return Unew, out, st.as_dict()
 
     def sai_solve(self, b: int, gamma: float, rhs: torch.Tensor) -> torch.Tensor:
         self.ensure_workspace(1, rhs.device)

@@ -445,3 +445,81 @@ def test_f2_null_forcing_equals_unforced():
     c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s)
     out1, _ = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters, f=t(np.zeros((p.P, p.s, p.n))))
     assert rel(out1.cpu().numpy(), out0) < 1e-12
+
+
+# ---------------------------------------------------------------- stage parity
+
+def _oracle_linear_stages(p, dense_max=1024):
+    """v_j(T_j) (Eq.(linivpSubproblem)) and every homogeneous leg exp((T_i - T_j)A) v_j(T_j)
+    (Fig. 2 line 3) from the oracle's primitives, problem 0 of p."""
+    from oracle.lowrank import truncated_svd, notaknot_taylor
+    from oracle.ebk import ebk_dense, ebk_krylov
+    A = ade_matrix(p.n, p.bc, p.nu[0], p.a[0])
+    dT = p.T / p.P
+    h = dT / (p.s - 1)
+    Au0 = A @ p.u0[0]
+    dense = p.n <= dense_max
+    vend = np.zeros((p.P, p.n))
+    for j in range(p.P):
+        U, C, _ = truncated_svd(Au0[:, None] + p.src[0, j].T, 0.01 * p.tol)
+        if U.shape[1]:
+            coef = notaknot_taylor(C, h)
+            Y = ebk_dense(A, U, coef, h, p.s - 1) if dense else ebk_krylov(A, U, coef, h, p.s - 1, gamma=dT / 10)
+            vend[j] = Y[-1]
+    legs = np.zeros((p.P - 1, p.P, p.n))          # legs[j][i] = leg of v_{j+1} at T_{i+1}, i > j
+    for j in range(p.P - 1):
+        nleg = p.P - 1 - j
+        W = (ebk_dense(A, None, None, dT, nleg, y0=vend[j]) if dense
+             else ebk_krylov(A, None, None, dT, nleg, gamma=p.T / 10, y0=vend[j]))
+        legs[j, j + 1:] = W[1:]
+    return vend, legs
+
+
+@pytest.mark.parametrize("make", [
+    lambda: synth.config2(n=1200, P=8, T=0.125, s=64),
+    lambda: synth.generic_linear(n=777, bc="periodic", nu=5e-3, a=1.3, P=5, s=12, T=0.5, seed=7),
+], ids=["c2-reduced", "generic-periodic"])
+def test_stage_vend_and_homogeneous_legs(make):
+    """Stage parity: (i) v_j(T_j) from the same u0/src, 1e-9; (ii) the homogeneous
+    legs fed the ORACLE's v_j(T_j) (pexp_solve_linear_stages vstart), every leg on its own
+    (hom_group = 1) and as group sums (default grouping), 1e-9 relative to the leg's start norm."""
+    p = make()
+    vend_ref, legs_ref = _oracle_linear_stages(p, dense_max=0)
+    c = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=p.s, k_max=384, hom_group=1)
+    out, vend, _, st = c.solve_linear_stages(t(p.u0), t(p.src), p.T, p.P, p.tol)
+    vend = vend.cpu().numpy()[0]
+    assert rel(vend, vend_ref) < 1e-9, st
+    for j in range(p.P):
+        assert np.linalg.norm(vend[j] - vend_ref[j]) < 1e-9 * np.linalg.norm(vend_ref), j
+    # legs from the oracle's start vectors, one leg per group
+    _, _, legs, st = c.solve_linear_stages(t(p.u0), None, p.T, p.P, p.tol, vstart=t(vend_ref[None]))
+    legs = legs.cpu().numpy()[0]                  # [P-1][P][n]
+    for j in range(p.P - 1):
+        assert np.linalg.norm(legs[j] - legs_ref[j]) < 1e-9 * max(np.linalg.norm(vend_ref[j]), 1e-300), j
+    # default grouping (8 legs share one block Krylov space): group sums
+    c8 = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=p.s, k_max=384)
+    _, _, legs8, st = c8.solve_linear_stages(t(p.u0), None, p.T, p.P, p.tol, vstart=t(vend_ref[None]))
+    legs8 = legs8.cpu().numpy()[0]
+    mh = min(8, p.P - 1)
+    for g in range(legs8.shape[0]):
+        ref = legs_ref[g * mh:(g + 1) * mh].sum(axis=0)
+        assert np.linalg.norm(legs8[g] - ref) < 1e-9 * np.linalg.norm(vend_ref), g
+
+
+@pytest.mark.parametrize("route", ROUTES)
+def test_stage_wr_map_on_steep_iterate(route):
+    """Stage parity: one WR map F(u_k) (Eq.(ivpSubproblem)/(updateSolution) P:326-335) applied to the
+    ORACLE's third iterate of a steepening Burgers run (per-subinterval Jacobians differ, block
+    widths > 1), against oracle.wr.wr_map of the same iterate: 1e-8, and the same delta."""
+    from oracle.wr import wr_map
+    p = synth.config3(n=1024, P=8, s=16, T=0.2, nu=5e-3)
+    _, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True, fixed_iters=3)
+    Uk = info["U"]
+    ref = wr_map(Uk, p.u0, p.nu, p.n, p.T, p.P, p.s, p.tol)
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=512, route=route)
+    Unew, out, st = c.wr_map(t(p.u0), t(Uk), p.nu, p.T, p.P, p.tol)
+    Unew = Unew.cpu().numpy()
+    assert rel(Unew, ref) < 1e-8, st
+    assert rel(out.cpu().numpy(), ref[:, -1, :]) < 1e-8
+    assert abs(st["wr_last_delta"] - np.max(np.abs(ref - Uk))) < 1e-8
+    assert st["max_m"] > 1
