@@ -120,6 +120,11 @@ typedef struct {
   double* gamma_j;
   int32_t* kscan_j;        /* Burgers only (nullable): Krylov dimension of the homogeneous scan
                               step of subinterval j (index k*P + j; -1 = waveform written in-scan) */
+  float ms_nonhom;         /* device time of the nonhomogeneous parts (source assembly, SVD, EBK of
+                              all subintervals at once): the paper's tau_1 with every subinterval
+                              concurrent                                            */
+  float ms_hom;            /* device time of the homogeneous parts and the superposition (linear:
+                              grouped legs; Burgers: the scan + waveform update): tau_2        */
 } pexp_stats;
 
 /* Create a context for one spatial operator A = nu*D2 - a*D1 on n points.

@@ -14,13 +14,20 @@
 // leader: it turns the checker's result into a decision that every worker reads after the next
 // barrier, so all workers leave the Arnoldi loop at the same step.
 //
-// Per Arnoldi step (4 worker barriers):
-//   A: forward L-solve affine maps of own rows -> CTA total; SM dot partial      | barrier
-//   B: carry-in from lower segments, y; backward U-solve maps -> CTA total         | barrier
-//   C: carry-in from upper segments, x; SM correction; CGS pass-1 dot partials      | barrier
-//   D: reduce h; x -= V h; pass-2 dot partials and ||x||^2                          | barrier
-//   E: reduce h2; x -= V h2; ||x|| = sqrt(||x||^2 - ||h2||^2); v_{k+1}; H column; publish
-// Cross-CTA reductions sum the per-CTA partials in a fixed order (identical in every CTA).
+// Per Arnoldi step (3 all-to-all exchanges between the workers, no barrier object):
+//   A: forward L-solve maps of own rows (y affine in the carry-in cy), backward U-solve maps with
+//      the offset kept affine in cy, Sherman-Morrison dot partial                    | exchange 1
+//   B: every CTA composes all segments' maps (one warp): own carries cy, cx; y, x; SM correction;
+//      CGS pass-1 dot partials                                                        | exchange 2
+//   C: h = sum of partials; x -= V h; pass-2 dot partials and ||x||^2                 | exchange 3
+//   D: h2; x -= V h2; ||x|| = sqrt(||x||^2 - ||h2||^2); v_{k+1}; H column; publish
+// An exchange is a stamped all-gather through L2: every CTA stores its row of values into one of
+// three rotating slots whose entries hold a sentinel (all-ones NaN pattern) until written; every
+// CTA polls all rows (independent loads, all in flight) and sums them in a fixed order, so all
+// CTAs hold bitwise identical results after ONE L2 round trip.  A CTA re-arms a slot's own row
+// right after the gather two exchanges later (nobody can still be reading it, and the re-arm is
+// fenced before its next publish).  The CTA's rows of the basis live in shared memory (the first
+// vcap columns; later ones in L2), so the Gram-Schmidt passes never leave the SM.
 #include <cstdlib>
 #include "kernels.cuh"
 #include "dense.cuh"
@@ -33,6 +40,11 @@ namespace {
 constexpr int RPT_MAX = 4;   // rows per thread
 constexpr int NT = PEXP_THREADS;
 constexpr int HS_PSM = 12288;  // checker's shared scratch (doubles) for the LU panel / permutation
+constexpr int XG_DOUBLES = 148 * 8;  // gathered rows of exchange 1
+// dynamic shared memory (doubles): hv, hv2, xs, then [xg | Vs] (workers) or the LU scratch (checker)
+constexpr int SCAN_SMEM_DOUBLES = 26400;  // 206 KB dynamic (+ ~19 KB static of the dense helpers) of the 227 KB per CTA
+constexpr int VS_DOUBLES = SCAN_SMEM_DOUBLES - 2 * (KSMALL_MAX + 8) - NT * RPT_MAX - XG_DOUBLES;
+static_assert(XG_DOUBLES + VS_DOUBLES >= HS_PSM, "checker scratch must fit");
 
 enum { F_STEPS = 0, F_RESULT = 1, F_DECISION = 2, F_KMAX = 3, F_ERR = 4, F_BREAK = 5, F_NFLAGS = 8 };
 enum { B_WCNT = 0, B_WGEN = 1, B_ACNT = 2, B_AGEN = 3 };
@@ -89,11 +101,165 @@ __device__ inline void grid_reduce(const double* part, int pw, int ncta, int j0,
   __syncthreads();
 }
 
-// Partial dots of the CTA's segment: out[j] = V_j[seg] . x[seg] (j < kk), out[pn] = ||x[seg]||^2.
-// x (rpt rows per thread, row l = threadIdx.x * rpt + q) is staged in shared memory; one warp
-// per column, lanes over consecutive rows (coalesced V reads).
-__device__ inline void seg_dots(const double* V, int n, int row0, int nrow, int kk, const double* xr, int rpt,
-                                double* xs, double* out, int pn) {
+struct Aff3 {  // x -> A x + B0 + B1 cy  (offset affine in the forward carry-in cy)
+  double A, B0, B1;
+};
+__device__ __forceinline__ Aff3 after3(Aff3 first, Aff3 then) {
+  return {then.A * first.A, fma(then.A, first.B0, then.B0), fma(then.A, first.B1, then.B1)};
+}
+
+// Exclusive scan of Aff3 maps in REVERSE thread order (rank = NT - 1 - threadIdx.x), as
+// block_excl_scan<true> of scan.cuh.
+__device__ __forceinline__ Aff3 block_excl_scan3_rev(Aff3 v, int rank, Aff3* wsm, Aff3& total) {
+  const int lane = rank & 31, w = rank >> 5;
+  Aff3 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double pa = __shfl_down_sync(0xffffffffu, inc.A, o), p0 = __shfl_down_sync(0xffffffffu, inc.B0, o),
+                 p1 = __shfl_down_sync(0xffffffffu, inc.B1, o);
+    if (lane >= o) inc = after3(Aff3{pa, p0, p1}, inc);
+  }
+  const double ea = __shfl_down_sync(0xffffffffu, inc.A, 1), e0 = __shfl_down_sync(0xffffffffu, inc.B0, 1),
+               e1 = __shfl_down_sync(0xffffffffu, inc.B1, 1);
+  const Aff3 exc = lane == 0 ? Aff3{1.0, 0.0, 0.0} : Aff3{ea, e0, e1};
+  __syncthreads();
+  if (lane == 31) wsm[w] = inc;
+  __syncthreads();
+  if (rank == 0) {
+    Aff3 acc{1.0, 0.0, 0.0};
+    for (int k = 0; k < NT / 32; ++k) {
+      const Aff3 t = wsm[k];
+      wsm[k] = acc;
+      acc = after3(acc, t);
+    }
+    wsm[NT / 32] = acc;
+  }
+  __syncthreads();
+  const Aff3 pre = wsm[w];
+  total = wsm[NT / 32];
+  return after3(pre, exc);
+}
+
+// ---- stamped all-gather exchange (header comment)
+__device__ __forceinline__ double ld_poll(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool is_sentinel(double v) { return __double_as_longlong(v) == -1LL; }
+__device__ __forceinline__ double sentinel() { return __longlong_as_double(-1LL); }
+
+struct Xch {
+  double* base;  // [3][nw][pw]
+  int nw, pw, c;
+  int e = 0;               // exchange counter (identical in every worker)
+  int lastn[3] = {0, 0, 0};  // values this CTA stored in each slot's row
+  __device__ double* row(int slot, int cta) const { return base + (size_t(slot) * nw + cta) * pw; }
+};
+
+// Publish this CTA's nval values (shared memory src) in the current slot.  All threads call it.
+__device__ inline void xch_publish(Xch& X, const double* src, int nval) {
+  const int slot = X.e % 3;
+  double* r = X.row(slot, X.c);
+  for (int j = threadIdx.x; j < nval; j += NT) __stcg(r + j, src[j]);
+  X.lastn[slot] = nval;
+}
+
+// After the gather of exchange e: re-arm the own row of slot (e + 2) % 3 and advance.
+__device__ inline void xch_finish(Xch& X) {
+  const int rs = (X.e + 2) % 3;
+  double* r = X.row(rs, X.c);
+  const int ln = X.lastn[rs];
+  for (int j = threadIdx.x; j < ln; j += NT) __stcg(r + j, sentinel());
+  X.lastn[rs] = 0;
+  __threadfence();
+  __syncthreads();
+  ++X.e;
+}
+
+// Gather: out[cta * nval + j] for every CTA (nval small).  out in shared memory.
+__device__ inline void xch_gather(Xch& X, int nval, double* out) {
+  const int slot = X.e % 3;
+  const int total = X.nw * nval;
+  for (int i0 = threadIdx.x; i0 < total; i0 += 4 * NT) {
+    double v[4];
+    const double* p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * NT;
+      p[u] = X.row(slot, (i < total ? i : 0) / nval) + (i < total ? i : 0) % nval;
+      if (i < total) v[u] = ld_poll(p[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * NT;
+      if (i < total) {
+        while (is_sentinel(v[u])) v[u] = ld_poll(p[u]);
+        out[i] = v[u];
+      }
+    }
+  }
+  xch_finish(X);
+}
+
+// Reduce: out[j] = sum over CTAs (fixed order: ng interleaved groups, then the groups in order) of
+// value j, j < nval.  out (shared memory) must hold >= max(NT, nval) doubles.
+__device__ inline void xch_reduce(Xch& X, int nval, double* out) {
+  const int slot = X.e % 3;
+  __syncthreads();  // out may be the publish source or still be read by the caller
+  if (nval > NT / 2) {  // wide: one thread per value, CTAs in order
+    for (int j = threadIdx.x; j < nval; j += NT) {
+      double a = 0.0;
+      for (int c0 = 0; c0 < X.nw; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + u < X.nw) v[u] = ld_poll(X.row(slot, c0 + u) + j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + u < X.nw) {
+            while (is_sentinel(v[u])) v[u] = ld_poll(X.row(slot, c0 + u) + j);
+            a += v[u];
+          }
+      }
+      out[j] = a;
+    }
+    xch_finish(X);
+    return;
+  }
+  const int ng = NT / nval;
+  const int j = threadIdx.x % nval, q = threadIdx.x / nval;
+  double a = 0.0;
+  if (q < ng) {
+    for (int c0 = q; c0 < X.nw; c0 += 8 * ng) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u * ng < X.nw) v[u] = ld_poll(X.row(slot, c0 + u * ng) + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u * ng < X.nw) {
+          while (is_sentinel(v[u])) v[u] = ld_poll(X.row(slot, c0 + u * ng) + j);
+          a += v[u];
+        }
+    }
+  }
+  __syncthreads();  // out may still be read by the caller's previous use
+  if (q < ng) out[q * nval + j] = a;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < nval)
+    for (int g = 0; g < ng; ++g) t += out[g * nval + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < nval) out[threadIdx.x] = t;
+  xch_finish(X);
+}
+
+// Partial dots of the CTA's segment against basis columns 0..kk-1 (the first vcap from shared
+// memory Vs, column stride segp; later ones from global Vg, column stride n) and ||x||^2:
+// out[j] = V_j[seg] . x[seg] (j < kk), out[kk] = ||x[seg]||^2.  x staged in xs.
+__device__ inline void seg_dots2(const double* Vs, int segp, int vcap, const double* Vg, int n, int row0, int nrow,
+                                 int kk, const double* xr, int rpt, double* xs, double* out) {
   for (int q = 0; q < rpt; ++q) {
     const int l = threadIdx.x * rpt + q;
     if (l < nrow) xs[l] = xr[q];
@@ -101,40 +267,22 @@ __device__ inline void seg_dots(const double* V, int n, int row0, int nrow, int 
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int j = w; j <= kk; j += NT / 32) {
-    double p = 0.0;
+    double p0 = 0.0, p1 = 0.0;
     if (j < kk) {
-      const double* v = V + size_t(j) * n + row0;
-      for (int l = lane; l < nrow; l += 32) p = fma(v[l], xs[l], p);
+      const double* v = j < vcap ? Vs + size_t(j) * segp : Vg + size_t(j) * n + row0;
+      int l = lane;
+      for (; l + 32 < nrow; l += 64) {
+        p0 = fma(v[l], xs[l], p0);
+        p1 = fma(v[l + 32], xs[l + 32], p1);
+      }
+      if (l < nrow) p0 = fma(v[l], xs[l], p0);
     } else {
-      for (int l = lane; l < nrow; l += 32) p = fma(xs[l], xs[l], p);
+      for (int l = lane; l < nrow; l += 32) p0 = fma(xs[l], xs[l], p0);
     }
-    p = warp_sum(p);
-    if (lane == 0) out[j < kk ? j : pn] = p;
+    const double p = warp_sum(p0 + p1);
+    if (lane == 0) out[j] = p;
   }
   __syncthreads();
-}
-
-// Composition of the affine maps maps[2*idx], maps[2*idx+1] for idx = first, first + step, ...
-// (cnt maps, in that order) applied to 0: the carry into a segment.  One warp: every lane
-// composes a contiguous run of the list (independent loads in flight), then an ordered tree over
-// the lanes.  Result valid in lane 0.
-__device__ inline double warp_carry(const double* maps, int first, int step, int cnt) {
-  const int lane = threadIdx.x & 31;
-  const int q = (cnt + 31) / 32;
-  Aff v{1.0, 0.0};
-  for (int t = 0; t < q; ++t) {
-    const int k = lane * q + t;
-    if (k < cnt) {
-      const int idx = first + k * step;
-      v = after(v, Aff{__ldcg(maps + 2 * idx), __ldcg(maps + 2 * idx + 1)});
-    }
-  }
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double oa = __shfl_down_sync(0xffffffffu, v.A, o), ob = __shfl_down_sync(0xffffffffu, v.B, o);
-    if ((lane & (2 * o - 1)) == 0 && lane + o < 32) v = after(v, Aff{oa, ob});
-  }
-  return v.B;
 }
 
 }  // namespace
@@ -157,6 +305,8 @@ struct ScanArgs {
   double* partA;                // [nw][pw]
   double* partB;                // [nw][pw]
   double* maps;                 // [2][nw][2]
+  double* xch;                  // [3][nw][kcap + 8] exchange slots (sentinel-initialised)
+  int vcap, segp;               // basis columns resident in shared memory; their column stride
   double* work;                 // checker: 10 kcap^2
   int* iwork;                   // checker: kcap
   unsigned* bar;                // [4]
@@ -244,6 +394,9 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   double* hv = dyn;
   double* hv2 = dyn + KSMALL_MAX + 8;
   double* xs = hv2 + KSMALL_MAX + 8;
+  double* xg = xs + NT * RPT_MAX;     // workers: gathered exchange-1 rows [nw][8]; checker: LU scratch from here
+  double* Vs = xg + XG_DOUBLES;       // workers: the CTA's rows of the first vcap basis columns
+  __shared__ Aff3 wsm3[NT / 32 + 1];
   const int c = blockIdx.x;
   const bool checker = c == a.nw;
   const int n = a.n, s = a.s, rpt = a.rpt;
@@ -256,12 +409,14 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   const int rend = min(n, row0 + a.seg);
   double uh[RPT_MAX], xr[RPT_MAX], vr[RPT_MAX];
   int kconv_prev = 0;  // checker: converged dimension of the previous subinterval (thread 0)
+  Xch X;
+  X.base = a.xch; X.nw = a.nw; X.pw = a.kcap + 8; X.c = c;
 
   // ---- subinterval 0: no homogeneous part; u_hat(T_1) = Y(T_1) (its waveform u0 + Y is written by
   // k_scan_output after the scan)
   if (!checker) {
     double b2 = 0.0;
-    for (int q = 0; q < rpt; ++q) {
+    _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
       const int g = row0 + threadIdx.x * rpt + q;
       uh[q] = 0.0;
       if (g >= rend) continue;
@@ -347,124 +502,205 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
     } else {
       // ---------------------------------------------------------------- workers
       const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
-      for (int q = 0; q < rpt; ++q) {
+      // this subinterval's factor rows of the CTA's segment, in registers for all Arnoldi steps
+      double f_l[RPT_MAX], f_di[RPT_MAX], f_a[RPT_MAX], f_z[RPT_MAX], f_w[RPT_MAX];
+      _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
         const int g = row0 + threadIdx.x * rpt + q;
+        const bool ok = g < rend;
+        f_l[q] = ok ? a.fl[fo + g] : 0.0;
+        f_di[q] = ok ? a.fdinv[fo + g] : 0.0;
+        f_a[q] = ok ? -f_di[q] * a.fsup[fo + g] : 1.0;
+        f_z[q] = ok && a.periodic ? a.fz[fo + g] : 0.0;
+        f_w[q] = ok && a.periodic ? a.fw[fo + g] : 0.0;
         vr[q] = uh[q] * inv;
-        if (g < rend) Vi[g] = vr[q];
+        if (ok) {
+          Vi[g] = vr[q];
+          if (0 < a.vcap) Vs[threadIdx.x * rpt + q] = vr[q];
+        }
       }
+      __syncthreads();
       int Kc = 0;     // converged dimension (0: beta == 0, no homogeneous part)
       int kused = 0;  // basis columns written (Arnoldi steps performed + 1)
       if (beta > 0.0) {
         for (int k = 0;; ++k) {
           kused = k + 1;
-          // A: forward L-solve maps y_g = -l_g y_{g-1} + b_g over own rows
+          // A: y_g = -l_g y_{g-1} + b_g over own rows as y_g = ya_g cy + yb_g (cy: carry from the lower
+          // segments); x_g = a_g x_{g+1} + di_g y_g composed over own rows with the offset affine in cy
+          int dec_pref = 0;
+          if (c == 0 && threadIdx.x == 0) dec_pref = vload(fl + F_RESULT);  // in flight during the scans
           Aff m{1.0, 0.0};
           double fdot = 0.0;
-          for (int q = 0; q < rpt; ++q) {
+          _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
             const int g = row0 + threadIdx.x * rpt + q;
             if (g < rend) {
-              m = after(m, Aff{-a.fl[fo + g], vr[q]});
-              if (a.periodic) fdot = fma(a.fw[fo + g], vr[q], fdot);
+              m = after(m, Aff{-f_l[q], vr[q]});
+              fdot = fma(f_w[q], vr[q], fdot);
             }
           }
           Aff tot;
           const Aff pre = block_excl_scan<false>(m, threadIdx.x, wsm, tot);
+          double ya[RPT_MAX], yb[RPT_MAX];
+          {
+            double al = pre.A, be = pre.B;
+            _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
+              const int g = row0 + threadIdx.x * rpt + q;
+              if (g < rend) {
+                al = -f_l[q] * al;
+                be = fma(-f_l[q], be, vr[q]);
+              }
+              ya[q] = al;
+              yb[q] = be;
+            }
+          }
+          Aff3 mb{1.0, 0.0, 0.0};
+          _Pragma("unroll") for (int q = RPT_MAX - 1; q >= 0; --q) if (q < rpt) {
+            const int g = row0 + threadIdx.x * rpt + q;
+            if (g < rend) mb = after3(mb, Aff3{f_a[q], f_di[q] * yb[q], f_di[q] * ya[q]});
+          }
+          Aff3 totb;
+          const Aff3 preb = block_excl_scan3_rev(mb, NT - 1 - threadIdx.x, wsm3, totb);
           if (a.periodic) fdot = block_sum(fdot, red);
           if (threadIdx.x == 0) {
-            a.maps[2 * c] = tot.A;
-            a.maps[2 * c + 1] = tot.B;
-            a.partA[size_t(c) * pw + PF] = fdot;
+            double d = 0.0;
             if (c == 0) {  // leader: decision for this step
-              int d = vload(fl + F_RESULT);
-              if (d == 0 && (k >= a.kcap - 1 || vload(fl + F_BREAK) > 0)) {  // no room / invariant space
-                while ((d = vload(fl + F_RESULT)) == 0) __nanosleep(64);
+              int dd = dec_pref;
+              if (dd == 0 && (k >= a.kcap - 1 || vload(fl + F_BREAK) > 0)) {  // no room / invariant space
+                while ((dd = vload(fl + F_RESULT)) == 0) __nanosleep(64);
               }
-              fl[F_DECISION] = d;
+              d = double(dd);
             }
+            xs[0] = tot.A; xs[1] = tot.B; xs[2] = totb.A; xs[3] = totb.B0; xs[4] = totb.B1; xs[5] = fdot;
+            xs[6] = d; xs[7] = 0.0;
           }
-          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
-          if (threadIdx.x == 0) s_dec = vload(fl + F_DECISION);
           __syncthreads();
-          if (s_dec != 0) {
-            Kc = s_dec;
+          xch_publish(X, xs, 8);
+          xch_gather(X, 8, xg);
+          const int dec = int(xg[6]);
+          if (dec != 0) {
+            Kc = dec;
             break;
           }
-          // B: carry from lower segments; y; backward maps x_g = -di_g cs_g x_{g+1} + di_g y_g
+          // B: all segments' maps composed by warp 0 (every CTA identically): own carries and the SM dot
           if (threadIdx.x < 32) {
-            const double cy = warp_carry(a.maps, 0, 1, c);  // segments 0 .. c-1, ascending
-            if (threadIdx.x == 0) hv[0] = cy;
+            const int lane = threadIdx.x;
+            const int per = (a.nw + 31) / 32;
+            // forward: cy at the start of each of the lane's segments
+            Aff run{1.0, 0.0};
+            for (int u = 0; u < per; ++u) {
+              const int cc = lane * per + u;
+              if (cc < a.nw) run = after(run, Aff{xg[cc * 8 + 0], xg[cc * 8 + 1]});
+            }
+            Aff inc = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const double pa = __shfl_up_sync(0xffffffffu, inc.A, o), pb = __shfl_up_sync(0xffffffffu, inc.B, o);
+              if (lane >= o) inc = after(Aff{pa, pb}, inc);
+            }
+            double cyl = __shfl_up_sync(0xffffffffu, inc.B, 1);  // carry into the lane's first segment
+            if (lane == 0) cyl = 0.0;
+            // backward maps x_first = A x_in + (B0 + B1 cy) of the lane's segments, composed descending
+            Aff runb{1.0, 0.0};
+            double cys[8];
+            {
+              double cyv = cyl;
+              for (int u = 0; u < per; ++u) {
+                const int cc = lane * per + u;
+                cys[u] = cyv;
+                if (cc < a.nw) cyv = fma(xg[cc * 8 + 0], cyv, xg[cc * 8 + 1]);
+              }
+            }
+            for (int u = per - 1; u >= 0; --u) {
+              const int cc = lane * per + u;
+              if (cc < a.nw) runb = after(runb, Aff{xg[cc * 8 + 2], fma(xg[cc * 8 + 4], cys[u], xg[cc * 8 + 3])});
+            }
+            Aff incb = runb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const double pa = __shfl_down_sync(0xffffffffu, incb.A, o), pb = __shfl_down_sync(0xffffffffu, incb.B, o);
+              if (lane + o < 32) incb = after(Aff{pa, pb}, incb);
+            }
+            double cxl = __shfl_down_sync(0xffffffffu, incb.B, 1);  // x entering the lane's LAST segment from above
+            if (lane == 31) cxl = 0.0;
+            // own segment: walk down from the lane's last segment to c
+            const int lo = c / per;
+            if (lane == lo) {
+              double cxv = cxl;
+              for (int u = per - 1; u > c - lo * per; --u) {
+                const int cc = lane * per + u;
+                if (cc < a.nw) cxv = fma(xg[cc * 8 + 2], cxv, fma(xg[cc * 8 + 4], cys[u], xg[cc * 8 + 3]));
+              }
+              hv[0] = cys[c - lo * per];
+              hv[1] = cxv;
+            }
+            double fs = 0.0;
+            for (int u = 0; u < per; ++u) {
+              const int cc = lane * per + u;
+              if (cc < a.nw) fs += xg[cc * 8 + 5];
+            }
+            fs = warp_sum(fs);
+            if (lane == 0) hv[2] = fs;
           }
           __syncthreads();
-          double y = fma(pre.A, hv[0], pre.B);
-          for (int q = 0; q < rpt; ++q) {
-            const int g = row0 + threadIdx.x * rpt + q;
-            if (g < rend) {
-              y = fma(-a.fl[fo + g], y, vr[q]);
-              xr[q] = y;
+          const double cy = hv[0], cx = hv[1], fsm = a.periodic ? hv[2] : 0.0;
+          {
+            double x = fma(preb.A, cx, fma(preb.B1, cy, preb.B0));
+            _Pragma("unroll") for (int q = RPT_MAX - 1; q >= 0; --q) if (q < rpt) {
+              const int g = row0 + threadIdx.x * rpt + q;
+              if (g < rend) {
+                const double y = fma(ya[q], cy, yb[q]);
+                x = fma(f_a[q], x, f_di[q] * y);
+                xr[q] = fma(-fsm, f_z[q], x);
+              }
             }
           }
-          Aff mb{1.0, 0.0};
-          for (int q = rpt - 1; q >= 0; --q) {
-            const int g = row0 + threadIdx.x * rpt + q;
-            if (g < rend) {
-              const double dv = a.fdinv[fo + g];
-              mb = after(mb, Aff{-dv * a.fsup[fo + g], dv * xr[q]});
-            }
-          }
-          Aff totb;
-          const Aff preb = block_excl_scan<true>(mb, NT - 1 - threadIdx.x, wsm, totb);
-          if (threadIdx.x == 0) {
-            a.maps[2 * a.nw + 2 * c] = totb.A;
-            a.maps[2 * a.nw + 2 * c + 1] = totb.B;
-          }
-          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
-          // C: carry from upper segments; x; SM correction; pass-1 dots
-          if (threadIdx.x < 32) {  // segments nw-1 .. c+1, descending
-            const double cx = warp_carry(a.maps + 2 * a.nw, a.nw - 1, -1, a.nw - 1 - c);
-            if (threadIdx.x == 0) hv[0] = cx;
-          }
-          if (a.periodic) grid_reduce(a.partA, pw, a.nw, PF, 1, hv2);
-          __syncthreads();
-          const double fsm = a.periodic ? hv2[0] : 0.0;
-          double x = fma(preb.A, hv[0], preb.B);
-          for (int q = rpt - 1; q >= 0; --q) {
-            const int g = row0 + threadIdx.x * rpt + q;
-            if (g < rend) {
-              const double dv = a.fdinv[fo + g];
-              x = fma(-dv * a.fsup[fo + g], x, dv * xr[q]);
-              xr[q] = a.periodic ? fma(-fsm, a.fz[fo + g], x) : x;
-            }
-          }
+          __syncthreads();  // hv free again
           const int kk = k + 1;  // columns 0..k
-          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partA + size_t(c) * pw, kk);
-          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
-          // D: h = V^T x; x -= V h; pass-2 dots
-          grid_reduce(a.partA, pw, a.nw, 0, kk + 1, hv);  // h = V^T x and ||x||^2 (at kk)
+          seg_dots2(Vs, a.segp, a.vcap, Vi, n, row0, rend - row0, kk, xr, rpt, xs, hv2);
+          xch_publish(X, hv2, kk + 1);
+          // C: h = V^T x; x -= V h; pass-2 dots
+          xch_reduce(X, kk + 1, hv);  // h = V^T x and ||x||^2 (at kk)
           const double nrm0 = sqrt(hv[kk]);
-          for (int q = 0; q < rpt; ++q) {
+          _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
             const int g = row0 + threadIdx.x * rpt + q;
             if (g < rend) {
-              double v = xr[q];
-              for (int j = 0; j < kk; ++j) v = fma(-hv[j], Vi[size_t(j) * n + g], v);
-              xr[q] = v;
+              const int l = threadIdx.x * rpt + q;
+              double v0 = xr[q], v1 = 0.0;
+              const int ks = min(kk, a.vcap);
+              int j = 0;
+              for (; j + 1 < ks; j += 2) {
+                v0 = fma(-hv[j], Vs[size_t(j) * a.segp + l], v0);
+                v1 = fma(-hv[j + 1], Vs[size_t(j + 1) * a.segp + l], v1);
+              }
+              if (j < ks) v0 = fma(-hv[j], Vs[size_t(j) * a.segp + l], v0);
+              for (j = ks; j < kk; ++j) v0 = fma(-hv[j], Vi[size_t(j) * n + g], v0);
+              xr[q] = v0 + v1;
             }
           }
-          seg_dots(Vi, n, row0, rend - row0, kk, xr, rpt, xs, a.partB + size_t(c) * pw, kk);
-          gbar(bar + B_WCNT, bar + B_WGEN, a.nw);
-          // E: second pass, norm, new column
-          grid_reduce(a.partB, pw, a.nw, 0, kk + 1, hv2);
+          seg_dots2(Vs, a.segp, a.vcap, Vi, n, row0, rend - row0, kk, xr, rpt, xs, hv2);
+          xch_publish(X, hv2, kk + 1);
+          // D: second pass, norm, new column
+          xch_reduce(X, kk + 1, hv2);
           double h2n = 0.0;
           for (int j = 0; j < kk; ++j) h2n = fma(hv2[j], hv2[j], h2n);
           const double hn = sqrt(fmax(hv2[kk] - h2n, 0.0));
           const bool brk = !(hn > a.defl * nrm0);
           const double sc = brk ? 0.0 : 1.0 / hn;
-          for (int q = 0; q < rpt; ++q) {
+          _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
             const int g = row0 + threadIdx.x * rpt + q;
             if (g < rend) {
-              double v = xr[q];
-              for (int j = 0; j < kk; ++j) v = fma(-hv2[j], Vi[size_t(j) * n + g], v);
-              vr[q] = v * sc;
+              const int l = threadIdx.x * rpt + q;
+              double v0 = xr[q], v1 = 0.0;
+              const int ks = min(kk, a.vcap);
+              int j = 0;
+              for (; j + 1 < ks; j += 2) {
+                v0 = fma(-hv2[j], Vs[size_t(j) * a.segp + l], v0);
+                v1 = fma(-hv2[j + 1], Vs[size_t(j + 1) * a.segp + l], v1);
+              }
+              if (j < ks) v0 = fma(-hv2[j], Vs[size_t(j) * a.segp + l], v0);
+              for (j = ks; j < kk; ++j) v0 = fma(-hv2[j], Vi[size_t(j) * n + g], v0);
+              vr[q] = (v0 + v1) * sc;
               Vi[size_t(kk) * n + g] = vr[q];
+              if (kk < a.vcap) Vs[size_t(kk) * a.segp + l] = vr[q];
             }
           }
           if (c == 0) {
@@ -478,6 +714,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
               atomicExch(fl + F_STEPS, kk);
             }
           }
+          __syncthreads();  // hv, hv2, Vs column kk complete before the next step reads them
         }
       }
       if (Kc < 0) {
@@ -491,7 +728,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
       if (arch) {
         for (int t = threadIdx.x; t < Kc; t += NT) hv[t] = __ldcg(Zi + size_t(s - 1) * a.kcap + t);
         __syncthreads();
-        for (int q = 0; q < rpt; ++q) {
+        _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
           const int g = row0 + threadIdx.x * rpt + q;
           uh[q] = 0.0;
           if (g >= rend) continue;
@@ -506,7 +743,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           hv[t] = __ldcg(Zi + size_t(t / Kc) * a.kcap + t % Kc);
         __syncthreads();
         double mx = 0.0;
-        for (int q = 0; q < rpt; ++q) {
+        _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
           const int g = row0 + threadIdx.x * rpt + q;
           uh[q] = 0.0;
           if (g >= rend) continue;
@@ -614,7 +851,7 @@ static long long scan_pool_cols(int P, int kcap) { return (long long)P * std::mi
 size_t hom_scan_bytes(int n, int s, int kcap, int P) {
   const int nw = scan_workers(n);
   const size_t pw = kcap + 8;
-  return sizeof(double) * (size_t(kcap + 1) * n + size_t(kcap + 1) * kcap + size_t(P) * s * kcap + 2 * nw * pw +
+  return sizeof(double) * (size_t(kcap + 1) * n + size_t(kcap + 1) * kcap + size_t(P) * s * kcap + 5 * nw * pw +
                            4 * nw + 10 * size_t(kcap) * kcap + size_t(scan_pool_cols(P, kcap)) * n) +
          sizeof(int) * (kcap + F_NFLAGS + 2 * P) + 4 * sizeof(unsigned) + 20 * 256;  // + arena alignment
 }
@@ -644,6 +881,9 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   a.partA = ar.take<double>(a.nw * pw);
   a.partB = ar.take<double>(a.nw * pw);
   a.maps = ar.take<double>(4 * a.nw);
+  a.xch = ar.take<double>(3 * size_t(a.nw) * pw);
+  a.segp = a.seg;
+  a.vcap = std::min(VS_DOUBLES / a.segp, kcap + 1);
   a.work = ar.take<double>(10 * size_t(kcap) * kcap);
   a.iwork = ar.take<int>(kcap);
   a.flags = ar.take<int>(F_NFLAGS);
@@ -651,12 +891,13 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   if (ar.off > ws_bytes) fail(2, "hom_scan workspace too small");
   PEXP_CUDA_TRY(cudaMemsetAsync(a.flags, 0, F_NFLAGS * sizeof(int), st));
   PEXP_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), st));
+  PEXP_CUDA_TRY(cudaMemsetAsync(a.xch, 0xFF, 3 * size_t(a.nw) * pw * sizeof(double), st));  // sentinel
   PEXP_CUDA_TRY(cudaMemsetAsync(a.H, 0, size_t(kcap + 1) * kcap * sizeof(double), st));
   {
     // algorithmic bytes: the waveform pass (Y, Uold read; Unew write) per subinterval
     ProfScope ps(PC_SCAN, st, 0.0, 0.0);  // latency-bound chain
     void* args[] = {&a};
-    const size_t smem = sizeof(double) * (2 * (KSMALL_MAX + 8) + NT * RPT_MAX + HS_PSM);
+    const size_t smem = sizeof(double) * SCAN_SMEM_DOUBLES;
     PEXP_CUDA_TRY(cudaFuncSetAttribute(k_hom_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PEXP_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hom_scan, dim3(a.nw + 1), dim3(NT), args, smem, st));
   }

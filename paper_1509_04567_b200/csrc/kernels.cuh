@@ -125,7 +125,7 @@ void launch_factor(cudaStream_t st, const Factors& F, int nf, const int* opidx, 
                    const Ops& O, int* err);
 void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E, int ncols,
                       const double* rhs, long long rs_e, int cin0, double* out, long long os_e, int cout0,
-                      const int* active);
+                      const int* active, double* out2 = nullptr, long long o2s_e = 0);  // out2: raw copy of x
 
 // tsmm.cu
 int xty_chunks(int n, int E);
@@ -158,7 +158,7 @@ void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long
                        const double* norm0, long long ns_e, int ldn, double defl, double* Rinv, const double* Rprev,
                        long long rps_e, int ldrp, double* Rout, long long rs_e, int ldr, int* live,
                        long long ls_e, const int* active, bool pivoted, double dtol = 0.0,
-                       double* norm0_out = nullptr);
+                       double* norm0_out = nullptr, int* maskB = nullptr, int* maskC = nullptr);
 void launch_defer_corr(cudaStream_t st, int E, int N, const double* Gb, long long gs_e, const int* cls, long long cs_e,
                        double* Mc, const int* active, bool plus_identity = false);
 void launch_onesided_svd(cudaStream_t st, int E, int s, const double* C, const int* kk, double tau, double* Qs,

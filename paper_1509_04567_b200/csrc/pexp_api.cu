@@ -7,6 +7,7 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -100,6 +101,7 @@ struct EbkBufs {
   long long vs_e = 0, hs_e = 0, zs_e = 0;
   double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p, *R0, *critc;
   int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc, *krec;
+  int *maskB, *maskC;  // in-block QR: evaluations that need stage B / stage C (written by k_block_chol)
   double* part;
   size_t part_cap;
   double* stepws = nullptr;  // fused Arnoldi step: global V^T W partials (large bases)
@@ -175,6 +177,8 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   B.critc = ar.take<double>(size_t(Ec) * mcap);
   B.horc = ar.take<int>(size_t(Ec) * mcap);
   B.live = ar.take<int>(size_t(Ec) * kcap);
+  B.maskB = ar.take<int>(Ec);
+  B.maskC = ar.take<int>(Ec);
   // the SVD stage (all E, s x s products) shares the partial-sum buffer with the chunks
   B.part_cap = std::max(part_need(Ec, n, std::max(kcap, s), forced ? std::max(mcap, s) : mcap),
                         forced ? part_need(E, n, s, s) : size_t(0));
@@ -231,12 +235,14 @@ static EbkBufs chunk_view(const EbkBufs& B, int c0, int Ec, int mb) {
 // Gram -> k_block_chol -> W <- W Rinv.  norm0 (nullable) = pre-orthogonalisation norms for
 // the deflation test; dtol > 0 defers nearly dependent columns (class 2, passed through raw).
 static void chol_combine_block(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0, const double* n0,
-                               long long n0s, int n0ld, double dtol, double defl, double* n0out, const int* active) {
+                               long long n0s, int n0ld, double dtol, double defl, double* n0out, const int* active,
+                               bool masks = false) {
   const long long ws_e = B.vs_e;
   launch_xty(st, E, n, B.V, ws_e, c0, m, B.V, ws_e, c0, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0, false,
              active, B.xcnt);
   launch_block_chol(st, E, m, B.G1, (long long)m * m, m, n0, n0s, n0ld, defl, B.Rinv, nullptr, 0, 0, nullptr, 0, 0,
-                    B.live + c0, B.kcap, active, true, dtol, n0out);
+                    B.live + c0, B.kcap, active, true, dtol, n0out, masks ? B.maskB : nullptr,
+                    masks ? B.maskC : nullptr);
   if (m <= 32) {
     launch_combine(st, E, n, B.V, ws_e, c0, m, B.Rinv, (long long)m * m, m, B.V, ws_e, c0, m, 1.0, 0.0, active);
   } else {
@@ -251,10 +257,23 @@ static void chol_combine_block(cudaStream_t st, EbkBufs& B, int E, int n, int m,
 // the first BCGS pass): stage A accepts well-separated columns (scaled pivot > 1e-8), defers
 // nearly dependent ones; stage B re-orthogonalises deferred columns explicitly (CGS2); stage C
 // accepts or deflates them relative to their pre-orthogonalisation norms norm0.
+// Stage B runs only for the evaluations whose stage A deferred a column (device-side mask written
+// by k_block_chol: the other evaluations' work items exit at once).  With reorth_follows (the call
+// inside an Arnoldi step, where BCGS pass 2 and its CholQR follow) stage C is likewise masked to
+// the evaluations whose stage A did not accept every column with scaled pivots >= 1e-2 -- the rule
+// of the fused step (arnoldi.cu).  The masked launches are charged no algorithmic bytes.
 static void inblock_qr(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0, const double* norm0, long long n0s,
-                       int n0ld, double defl, const int* active) {
+                       int n0ld, double defl, const int* active, bool reorth_follows = false) {
   const long long ws_e = B.vs_e;
-  chol_combine_block(st, B, E, n, m, c0, norm0, n0s, n0ld, 1e-8, defl, B.n0p, active);
+  const int* act0 = active;
+  chol_combine_block(st, B, E, n, m, c0, norm0, n0s, n0ld, 1e-8, defl, B.n0p, active, true);
+  // (wide blocks m > 32 go out of place through Wt2 and copy every evaluation back: no masks there)
+  const bool mask_ok = m <= 32;
+  const int hint = g_cfg.active_hint;
+  if (mask_ok) {
+    g_cfg.active_hint = 0;
+    active = B.maskB;
+  }
   for (int rep = 0; rep < 2; ++rep) {
     launch_xty(st, E, n, B.V, ws_e, c0, m, B.V, ws_e, c0, m, B.part, B.part_cap, B.G1, (long long)m * m, m, 0, 0, false,
                active, B.xcnt);
@@ -270,7 +289,10 @@ static void inblock_qr(cudaStream_t st, EbkBufs& B, int E, int n, int m, int c0,
                                       cudaMemcpyDeviceToDevice, st));
     }
   }
-  chol_combine_block(st, B, E, n, m, c0, B.n0p, m, 0, 0.0, defl, nullptr, active);
+  const bool maskc = mask_ok && reorth_follows;
+  if (!maskc) g_cfg.active_hint = hint;
+  chol_combine_block(st, B, E, n, m, c0, B.n0p, m, 0, 0.0, defl, nullptr, maskc ? B.maskC : act0);
+  g_cfg.active_hint = hint;
 }
 
 struct RunInfo {
@@ -457,16 +479,14 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       sa.hs_g = B.stepws;
       launch_arnoldi_step(st, sa);
     } else if (B.spart && m <= 32) {  // streaming route: TMA-fed DMMA products (stream.cu)
-    launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
-    PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.Wt, size_t(m) * n * sizeof(double), B.V + size_t(nv) * n,
-                                    ws_e * sizeof(double), size_t(m) * n * sizeof(double), E,
-                                    cudaMemcpyDeviceToDevice, st));
+    // W0 = (I - gamma A)^{-1} V_b into the basis (columns [nv, nv+m)) and, raw, into Wt
+    launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active, B.Wt, (long long)m * n);
     // BCGS pass 1: H[0:nv, block b] = V^T W0 and the W0 Gram (deflation reference) in one pass
     launch_sproj(st, E, n, B.V, ws_e, nv, B.V + size_t(nv) * n, ws_e, m, B.spart, B.spart_cap, B.H, B.hs_e, kcap, 0,
                  b * m, false, B.G0, (long long)m * m, B.active);
     launch_supdate(st, E, n, B.V, ws_e, nv, B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.V + size_t(nv) * n, ws_e, m,
                    -1.0, 1.0, B.active);
-    inblock_qr(st, B, E, n, m, nv, B.G0, (long long)m * m, m, defl, B.active);
+    inblock_qr(st, B, E, n, m, nv, B.G0, (long long)m * m, m, defl, B.active, true);
     // BCGS pass 2 + CholQR
     launch_sproj(st, E, n, B.V, ws_e, nv, B.V + size_t(nv) * n, ws_e, m, B.spart, B.spart_cap, B.T,
                  (long long)kcap * B.mcap, nv, 0, 0, false, nullptr, 0, B.active);
@@ -477,12 +497,9 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
                b * m, false, B.active, B.xcnt);
     } else {
     // W = (I - gamma A)^{-1} V_b  -> columns [nv, nv+m)
-    launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active);
-    // keep the raw image W0 = (I - gamma A)^{-1} V_b: the subdiagonal block of H is computed
-    // directly as Q^T W0 at the end (exact to eps, independent of the in-block QR route)
-    PEXP_CUDA_TRY(cudaMemcpy2DAsync(B.Wt, size_t(m) * n * sizeof(double), B.V + size_t(nv) * n,
-                                    ws_e * sizeof(double), size_t(m) * n * sizeof(double), E,
-                                    cudaMemcpyDeviceToDevice, st));
+    // keep the raw image W0 = (I - gamma A)^{-1} V_b (second output Wt): the subdiagonal block of H
+    // is computed directly as Q^T W0 at the end (exact to eps, independent of the in-block QR route)
+    launch_sai_solve(st, F, B.fidx, E, m, B.V, ws_e, b * m, B.V, ws_e, nv, B.active, B.Wt, (long long)m * n);
     // norms of W0 (deflation reference)
     launch_xty(st, E, n, B.V, ws_e, nv, m, B.V, ws_e, nv, m, B.part, B.part_cap, B.G0, (long long)m * m, m, 0, 0,
                false, B.active, B.xcnt);
@@ -491,7 +508,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
                false, B.active, B.xcnt);
     launch_combine(st, E, n, B.V, ws_e, 0, nv, B.H + size_t(b) * m * kcap, B.hs_e, kcap, B.V, ws_e, nv, m, -1.0, 1.0,
                    B.active);
-    inblock_qr(st, B, E, n, m, nv, B.G0, (long long)m * m, m, defl, B.active);
+    inblock_qr(st, B, E, n, m, nv, B.G0, (long long)m * m, m, defl, B.active, true);
     // BCGS pass 2 (re-orthogonalisation against V) + CholQR of the nearly orthonormal block
     launch_xty(st, E, n, B.V, ws_e, 0, nv, B.V, ws_e, nv, m, B.part, B.part_cap, B.T, (long long)kcap * B.mcap, nv,
                0, 0, false, B.active, B.xcnt);
@@ -1142,6 +1159,8 @@ pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const doub
       PEXP_CUDA_TRY(cudaMemsetAsync(L.Yend, 0, size_t(E) * n * sizeof(double), st));
     }
     if (vend) PEXP_CUDA_TRY(cudaMemcpyAsync(vend, L.Yend, size_t(E) * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    EventPair evh;  // homogeneous legs + superposition (tau_2)
+    PEXP_CUDA_TRY(cudaEventRecord(evh.a, st));
     int G = 0;
     if (P > 1) {
       // homogeneous legs, grouped: up to 16 consecutive legs share one block Krylov space
@@ -1178,6 +1197,7 @@ pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const doub
     if (legs && P > 1)
       PEXP_CUDA_TRY(cudaMemcpyAsync(legs, L.Yh, size_t(Bt) * G * P * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     launch_superpose(st, Bt, P, n, u0, L.Yend, P > 1 ? L.Yh : nullptr, (long long)P * n, n, G, out);
+    PEXP_CUDA_TRY(cudaEventRecord(evh.b, st));
     PEXP_CUDA_TRY(cudaEventRecord(ev.b, st));
     PEXP_CUDA_TRY(cudaEventSynchronize(ev.b));
     ++g_cfg.syncs;
@@ -1199,6 +1219,8 @@ pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const doub
       st_out->restarts = ri.restarts;
       st_out->best_residual = std::max(ri.worst_res_ratio, rh.worst_res_ratio);
       st_out->ms_total = ms;
+      st_out->ms_hom = evh.ms();
+      st_out->ms_nonhom = ms - st_out->ms_hom;
       st_out->evals = E;
       st_out->kernel_launches = (int)g_launches;
       st_out->host_syncs = g_cfg.syncs;
@@ -1266,6 +1288,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
     double* rec_g = st_out ? st_out->gamma_j : nullptr;
     int32_t* rec_ks = st_out ? st_out->kscan_j : nullptr;
     std::vector<double> dhist;
+    std::vector<std::unique_ptr<EventPair>> scan_ev;  // homogeneous scan + waveform update per iteration
     std::vector<int> iota(P);
     for (int j = 0; j < P; ++j) iota[j] = j;
     h2d(st, L.iota, iota);
@@ -1308,6 +1331,8 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       if (rec_k) PEXP_CUDA_TRY(cudaMemcpyAsync(rec_k + size_t(k) * P, L.B.krec, P * sizeof(int),
                                                cudaMemcpyDeviceToHost, st));
       PEXP_CUDA_TRY(cudaMemsetAsync(L.delta, 0, sizeof(double), st));
+      scan_ev.emplace_back(new EventPair);
+      PEXP_CUDA_TRY(cudaEventRecord(scan_ev.back()->a, st));
       if (L.scan_ws) {  // persistent cooperative scan; host-driven fallback beyond its row capacity
         const int k1 = std::min(o.kcap, 512);
         const double defl_s = g_cfg.defl;
@@ -1336,6 +1361,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
                        1.0, 0.0, nullptr, B1.kfin);
         launch_wr_step(st, s, n, u0, L.Wh, L.Y + off, L.Uk + off, L.Un + off, L.uhat, L.delta);
       }
+      PEXP_CUDA_TRY(cudaEventRecord(scan_ev.back()->b, st));
       PEXP_CUDA_TRY(cudaMemcpyAsync(&delta, L.delta, sizeof(double), cudaMemcpyDeviceToHost, st));
       host_sync(st);
       std::swap(L.Uk, L.Un);
@@ -1364,6 +1390,8 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       st_out->max_k = max_k;
       st_out->restarts = restarts;
       st_out->ms_total = ms;
+      for (auto& e : scan_ev) st_out->ms_hom += e->ms();
+      st_out->ms_nonhom = ms - st_out->ms_hom;
       st_out->evals = P * iters;
       st_out->kernel_launches = (int)g_launches;
     }
@@ -1394,7 +1422,7 @@ pexp_status pexp_sai_solve(pexp_ctx* ctx, int32_t b, double gamma, const double*
     launch_ade_rows(st, 1, n, ctx->bc == PEXP_BC_DIRICHLET, L.nu_d, L.a_d, O1.sub, O1.diag, O1.sup);
     PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
     launch_factor(st, L.F, 1, L.opidx_f, L.gam_f, O1, L.err);
-    launch_sai_solve(st, L.F, nullptr, 1, ncols, rhs, 0, 0, x, 0, 0, nullptr);
+    launch_sai_solve(st, L.F, nullptr, 1, ncols, rhs, 0, 0, x, 0, 0, nullptr, nullptr, 0);
     int herr = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&herr, L.err, sizeof(int), cudaMemcpyDeviceToHost, st));
     host_sync(st);

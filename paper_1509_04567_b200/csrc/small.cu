@@ -219,9 +219,12 @@ __global__ void __launch_bounds__(PEXP_THREADS)
 k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm0, long long ns_e,
              int ldn, double defl, double* Rinv, const double* Rprev, long long rps_e, int ldrp, double* Rout,
              long long rs_e, int ldr, int* live, long long ls_e, const int* active, int pivoted, double piv_tol,
-             double dtol, double* norm0_out) {
+             double dtol, double* norm0_out, int* maskB, int* maskC) {
   const int e = blockIdx.x;
-  if (active && !active[e]) return;
+  if (active && !active[e]) {
+    if (maskB && threadIdx.x == 0) { maskB[e] = 0; maskC[e] = 0; }
+    return;
+  }
   extern __shared__ double dsm[];
   double (*S)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm);                       // scaled Gram / Schur
   double (*X)[MAXS + 1] = reinterpret_cast<double (*)[MAXS + 1]>(dsm + MAXS * (MAXS + 1));   // work
@@ -229,7 +232,7 @@ k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm
   __shared__ double Lp[MAXS][MAXS + 1];  // Lp[a][t]: permuted lower factor (position a, pivot t)
   __shared__ int dead[MAXS], perm[MAXS], used[MAXS];
   __shared__ int s_np, s_j;
-  __shared__ double s_piv;
+  __shared__ double s_piv, s_pmin;
   const double* Ge = G + e * gs_e;
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     double g = Ge[k + size_t(k) * ldg];
@@ -245,7 +248,7 @@ k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm
     S[i][j] = d[i] * d[j] * 0.5 * (Ge[i + size_t(j) * ldg] + Ge[j + size_t(i) * ldg]);
     Lp[i][j] = 0.0;
   }
-  if (threadIdx.x == 0) s_np = 0;
+  if (threadIdx.x == 0) { s_np = 0; s_pmin = INFINITY; }
   __syncthreads();
   for (int t = 0; t < N; ++t) {
     if (threadIdx.x == 0) {
@@ -265,6 +268,7 @@ k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm
         used[jb] = 1;
         perm[t] = jb;
         s_piv = sqrt(best);
+        s_pmin = fmin(s_pmin, best);
         s_np = t + 1;
       }
     }
@@ -298,6 +302,13 @@ k_block_chol(int N, const double* G, long long gs_e, int ldg, const double* norm
   }
   __syncthreads();
   const int nd = s_nd;
+  // masks of the follow-up stages of the in-block QR (pexp_api.cu inblock_qr): stage B (explicit
+  // CGS2 of deferred columns) only when something was deferred; stage C (second CholQR) unless
+  // every column was accepted with scaled pivots >= 1e-2 (same rule as the fused Arnoldi step)
+  if (maskB && threadIdx.x == 0) {
+    maskB[e] = nd > 0;
+    maskC[e] = !(nd == 0 && np == N && s_pmin >= 1e-2);
+  }
   // Rp[t][a] (upper, t <= a, t < np) = Lp[perm[a]][t];  X = Rp^{-1} on the leading np x np block
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     for (int k = 0; k < N; ++k) X[k][j] = 0.0;
@@ -1032,12 +1043,13 @@ void launch_sym_eig_select(cudaStream_t st, int E, int s, const double* G, doubl
 void launch_block_chol(cudaStream_t st, int E, int N, const double* G, long long gs_e, int ldg,
                        const double* norm0, long long ns_e, int ldn, double defl, double* Rinv, const double* Rprev,
                        long long rps_e, int ldrp, double* Rout, long long rs_e, int ldr, int* live,
-                       long long ls_e, const int* active, bool pivoted, double dtol, double* norm0_out) {
+                       long long ls_e, const int* active, bool pivoted, double dtol, double* norm0_out, int* maskB,
+                       int* maskC) {
   if (N > MAXS) fail(1, "block width > 64 not supported");
   ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
   k_block_chol<<<E, PEXP_THREADS, SM2, st>>>(N, G, gs_e, ldg, norm0, ns_e, ldn, defl, Rinv, Rprev, rps_e, ldrp,
                                             Rout, rs_e, ldr, live, ls_e, active, pivoted ? 1 : 0, g_cfg.piv_tol, dtol,
-                                            norm0_out);
+                                            norm0_out, maskB, maskC);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }

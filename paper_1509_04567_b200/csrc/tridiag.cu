@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(PEXP_THREADS)
 k_sai_solve(int n, int periodic, const int* fidx, const double* fl, const double* fdinv,
             const double* fsup, const double* fz, const double* fw, const double* rhs,
             long long rs_e, int cin0, double* out, long long os_e, int cout0,
-            const int* active) {
+            const int* active, double* out2, long long o2s_e) {
   const int c = blockIdx.x, e = blockIdx.y;
   if (active && !active[e]) return;
   __shared__ double s0[PEXP_THREADS * SPAD];
@@ -406,8 +406,8 @@ k_sai_solve(int n, int periodic, const int* fidx, const double* fl, const double
   __shared__ double red[32];
   const size_t fo = size_t(fidx ? fidx[e] : e) * n;
   cta_sai_solve(n, periodic, fl + fo, fdinv + fo, fsup + fo, periodic ? fz + fo : nullptr, periodic ? fw + fo : nullptr,
-                rhs + e * rs_e + size_t(cin0 + c) * n, out + e * os_e + size_t(cout0 + c) * n, nullptr, s0, s1, wsm,
-                red);
+                rhs + e * rs_e + size_t(cin0 + c) * n, out + e * os_e + size_t(cout0 + c) * n,
+                out2 ? out2 + e * o2s_e + size_t(c) * n : nullptr, s0, s1, wsm, red);
 }
 
 // ---------------------------------------------------------------- host wrappers
@@ -442,7 +442,7 @@ void launch_factor(cudaStream_t st, const Factors& F, int nf, const int* opidx, 
 
 void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E, int ncols,
                       const double* rhs, long long rs_e, int cin0, double* out, long long os_e,
-                      int cout0, const int* active) {
+                      int cout0, const int* active, double* out2, long long o2s_e) {
   if (E == 0 || ncols == 0) return;
   // algorithmic: read rhs + write x per column, factors once per distinct factor (<= E)
   const double ea = eact(E, active);
@@ -450,7 +450,7 @@ void launch_sai_solve(cudaStream_t st, const Factors& F, const int* fidx, int E,
                ea * ncols * F.n * (F.periodic ? 8.0 : 6.0));
   dim3 grid(ncols, E);
   k_sai_solve<<<grid, PEXP_THREADS, 0, st>>>(F.n, F.periodic, fidx, F.l, F.dinv, F.sup, F.z, F.w,
-                                              rhs, rs_e, cin0, out, os_e, cout0, active);
+                                              rhs, rs_e, cin0, out, os_e, cout0, active, out2, o2s_e);
   count_launch();
   PEXP_LAUNCH_CHECK();
 }
