@@ -125,6 +125,11 @@ typedef struct {
                               concurrent                                            */
   float ms_hom;            /* device time of the homogeneous parts and the superposition (linear:
                               grouped legs; Burgers: the scan + waveform update): tau_2        */
+  double scan_steps;       /* Burgers: Arnoldi steps the homogeneous scan performed (all subintervals
+                              and iterations), projected-problem checks of its checker CTA, and
+                              SM cycles that CTA spent in them (diagnostics)   */
+  double scan_checks;
+  double scan_check_cycles;
 } pexp_stats;
 
 /* Create a context for one spatial operator A = nu*D2 - a*D1 on n points.

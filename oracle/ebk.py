@@ -35,7 +35,7 @@ def ebk_dense(A, U, coef, h, npieces, y0=None):
     n = A.shape[0]
     Ad = A.toarray() if sp.issparse(A) else np.asarray(A)
     Uc = U if U is not None else np.zeros((n, 0))
-    F0, B = phi_blocks(Ad, Uc, h)
+    F0, B = phi_blocks(Ad, Uc, h, nq=coef.shape[1] if (coef is not None and Uc.shape[1]) else 4)
     z0 = np.zeros(n) if y0 is None else y0
     return chain(F0, B, coef if Uc.shape[1] else None, h, z0, npieces)
 
@@ -54,8 +54,9 @@ def ebk_krylov(A, U, coef, h, npieces, gamma, y0=None, eta=1e-12, kmax=900,
             Z = np.zeros((npieces + 1, n))
             return (Z, {"k": 0}) if return_info else Z
         # criterion scale: max over nodes of ||U p(τ_i)|| = ||c_{i,0}|| (U orthonormal)
-        nodes = np.concatenate([coef[:, 0, :], (coef[-1, 0] + coef[-1, 1] * h + coef[-1, 2] * h * h / 2
-                                                 + coef[-1, 3] * h ** 3 / 6)[None]])
+        import math
+        last = sum(coef[-1, q] * h ** q / math.factorial(q) for q in range(coef.shape[1]))   # p at the end node
+        nodes = np.concatenate([coef[:, 0, :], last[None]])
         tgt = eta * (scale if scale is not None else np.max(np.linalg.norm(nodes, axis=1)))
     else:
         beta = np.linalg.norm(y0)
@@ -95,7 +96,7 @@ def ebk_krylov(A, U, coef, h, npieces, gamma, y0=None, eta=1e-12, kmax=900,
         Ahat = (np.eye(k) - Hinv) / gamma
         if forced:
             E = np.zeros((k, m)); E[:m, :m] = np.eye(m)
-            F0, B = phi_blocks(Ahat, E, h)
+            F0, B = phi_blocks(Ahat, E, h, nq=coef.shape[1])
             Z = chain(F0, B, coef, h, np.zeros(k), npieces)
         else:
             F0, B = phi_blocks(Ahat, np.zeros((k, 0)), h)

@@ -56,6 +56,31 @@ def notaknot_taylor(Y: np.ndarray, h: float) -> np.ndarray:
     return out
 
 
+def cheb_taylor(Y: np.ndarray, dT: float, npieces: int) -> np.ndarray:
+    """Higher-order p(t) on Chebyshev nodes ("Chebyshev nodes ... other types of
+    p(t) are possible", DESIGN.md §3 reading #23).
+
+    Each row of Y [m][s] holds the values at the Chebyshev-Lobatto nodes
+    τ_i = (dT/2)(1 - cos(π i/(s-1))), i = 0..s-1, of the subinterval [0, dT].  p is THE polynomial
+    of degree s-1 through them.  It is returned as its exact Taylor re-expansion about the uniform
+    piece starts σ_i = i·dT/npieces (a polynomial of degree s-1 equals its s-term Taylor series):
+        out[i][q] = p^{(q)}(σ_i),  shape [npieces][s][m],
+        p(σ_i + σ) = Σ_{q<s} out[i][q] σ^q/q!.
+    Interpolation, differentiation and evaluation in the Chebyshev basis are library primitives
+    (numpy.polynomial.chebyshev: chebfit on s points with degree s-1 is interpolation)."""
+    from numpy.polynomial import chebyshev as Ch
+    Y = np.atleast_2d(Y)
+    m, s = Y.shape
+    x = -np.cos(np.pi * np.arange(s) / (s - 1))              # nodes mapped to [-1, 1]
+    c = Ch.chebfit(x, Y.T, s - 1)                             # [s][m] Chebyshev coefficients
+    xs = 2.0 * (np.arange(npieces) * (dT / npieces)) / dT - 1.0
+    out = np.zeros((npieces, s, m))
+    for q in range(s):
+        cq = c if q == 0 else Ch.chebder(c, m=q, scl=2.0 / dT, axis=0)   # d^q/dτ^q
+        out[:, q, :] = Ch.chebval(xs, cq).T if cq.shape[0] > 0 else 0.0
+    return out
+
+
 def eval_taylor(coef: np.ndarray, h: float, tau: float) -> np.ndarray:
     """Evaluate the piecewise cubic at local time tau in [0, (s-1)h]."""
     npieces = coef.shape[0]

@@ -14,14 +14,16 @@ from __future__ import annotations
 import numpy as np
 
 from .operators import ade_matrix
-from .lowrank import truncated_svd, notaknot_taylor
+from .lowrank import truncated_svd, notaknot_taylor, cheb_taylor
 from .ebk import ebk_dense, ebk_krylov
 
 
 def solve_linear(n, bc, nu, a, u0, src, T, P, s, tol, *, eta=1e-12, dense_max=1024,
-                 i_max=None, svd_tau_factor=0.01, return_info=False):
+                 i_max=None, svd_tau_factor=0.01, return_info=False, node_rule=0):
     """u0: [batch][n]; src: [batch][P][s][n] (g at the nodes of synth.node_times);
-    nu, a: [batch].  Returns out [batch][P'][n], P' = P or i_max."""
+    nu, a: [batch].  Returns out [batch][P'][n], P' = P or i_max.
+    node_rule 0: uniform nodes, not-a-knot cubic p(t) (readings #8, #9); node_rule 1 (row f3):
+    Chebyshev-Lobatto nodes, p(t) = the degree-(s-1) interpolant (reading #23)."""
     u0 = np.atleast_2d(u0)
     batch = u0.shape[0]
     nu = np.broadcast_to(np.asarray(nu, dtype=np.float64), (batch,))
@@ -47,7 +49,7 @@ def solve_linear(n, bc, nu, a, u0, src, T, P, s, tol, *, eta=1e-12, dense_max=10
             if U.shape[1] == 0:
                 vend[j] = 0.0
                 continue
-            coef = notaknot_taylor(C, h)
+            coef = notaknot_taylor(C, h) if node_rule == 0 else cheb_taylor(C, dT, s - 1)
             if dense:                               # step 4
                 Y = ebk_dense(A, U, coef, h, s - 1)
             else:

@@ -46,7 +46,9 @@ constexpr int SCAN_SMEM_DOUBLES = 26400;  // 206 KB dynamic (+ ~19 KB static of 
 constexpr int VS_DOUBLES = SCAN_SMEM_DOUBLES - 2 * (KSMALL_MAX + 8) - NT * RPT_MAX - XG_DOUBLES;
 static_assert(XG_DOUBLES + VS_DOUBLES >= HS_PSM, "checker scratch must fit");
 
-enum { F_STEPS = 0, F_RESULT = 1, F_DECISION = 2, F_KMAX = 3, F_ERR = 4, F_BREAK = 5, F_NFLAGS = 8 };
+enum { F_STEPS = 0, F_RESULT = 1, F_DECISION = 2, F_KMAX = 3, F_ERR = 4, F_BREAK = 5,
+       F_NSTEPS = 8, F_NCHECK = 9, F_CHKCYC = 10,  // diagnostics: Arnoldi steps, checks, checker kilo-cycles
+       F_NFLAGS = 12 };
 enum { B_WCNT = 0, B_WGEN = 1, B_ACNT = 2, B_AGEN = 3 };
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
@@ -470,8 +472,11 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           __syncthreads();
           const int K = s_dec;
           const bool brk = vload(fl + F_BREAK) == K;
+          const long long tc0 = clock64();
           const double res = hom_check(a, Zi, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
           if (threadIdx.x == 0) {
+            fl[F_NCHECK] += 1;
+            fl[F_CHKCYC] += int((clock64() - tc0) >> 10);
             int result = 0;
             if (brk || res <= crit) {
               result = K;
@@ -770,6 +775,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
       }
       if (threadIdx.x == 0) a.partA[size_t(c) * pw + PBETA] = b2;
       if (c == 0 && threadIdx.x == 0) {
+        fl[F_NSTEPS] += kused;
         a.kc[i] = arch ? Kc : -1;
         if (i + 1 < a.P) a.koff[i + 1] = arch ? koff + kused + 1 : koff;
       }
@@ -858,7 +864,7 @@ size_t hom_scan_bytes(int n, int s, int kcap, int P) {
 
 int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
                     double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
-                    double* delta, char* ws, size_t ws_bytes, int* kscan_rec) {
+                    double* delta, char* ws, size_t ws_bytes, int* kscan_rec, double* diag) {
   Arena ar{ws, ws_bytes, 0};
   ScanArgs a{};
   a.P = P; a.s = s; a.n = n; a.kcap = kcap; a.periodic = F.periodic;
@@ -916,6 +922,11 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   host_sync(st);
   if (hf[F_ERR]) fail(4 /* PEXP_ENOCONV */, "Krylov capacity reached (homogeneous scan)");
   if (kscan_rec) PEXP_CUDA_TRY(cudaMemcpy(kscan_rec, a.kc, P * sizeof(int), cudaMemcpyDeviceToHost));
+  if (diag) {
+    diag[0] += hf[F_NSTEPS];
+    diag[1] += hf[F_NCHECK];
+    diag[2] += double(hf[F_CHKCYC]) * 1024.0;
+  }
   return hf[F_KMAX];
 }
 

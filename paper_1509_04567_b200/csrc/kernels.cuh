@@ -16,6 +16,8 @@ struct CallCfg {
   int hom_group = 8;       // pexp_options.hom_group
   int buckets = 1;         // pexp_options.width_buckets (0: pad every evaluation to max m_j)
   int syncs = 0;           // host synchronisations performed by the current call
+  int nq = 4;              // Taylor terms per polynomial piece of p(t): 4 (cubic spline) or 12 (node_rule 1)
+  int node_rule = 0;       // pexp_options.node_rule
   int active_hint = -1;    // evaluations still active in the running EBK loop (-1: unknown);
                            // the profiler's algorithmic byte/flop counts use it
 };
@@ -52,7 +54,8 @@ struct SPArgs {
   const int* npieces;            // [E] or nullptr
   int npieces_const;
   int out_stride, nout;          // store z at nodes q*out_stride, q < nout
-  const double* coef;            // forced: [E][s-1][4][m]
+  const double* coef;            // forced: [E][s-1][nq][m]
+  int nq;                        // Taylor terms per piece (4: cubic spline; 12: Chebyshev interpolant pieces)
   int s;
   const double* beta;            // homogeneous: [E] start-vector norms
   const double* crit;            // [E] residual targets
@@ -167,13 +170,18 @@ void launch_build_final(cudaStream_t st, int E, int s, int mmax, const int* kk, 
                         const double* sig, const double* Cs, const int* m, double* Msel, double* Cfin, int* fill);
 void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, const double* Cfin, double h,
                    double eta, double* coef, double* crit);
+// node_rule 1: coef[e][i][q][c] = sum_k Dmat[i][q][k] Cfin[e][c][k] (Taylor coefficients of the degree-(s-1)
+// interpolant through the Chebyshev-Lobatto nodes, at the s-1 uniform piece starts), crit as launch_spline
+void launch_poly_coef(cudaStream_t st, int E, int s, int mmax, int nq, const double* Dmat, const double* Cfin,
+                      double eta, double* coef, double* crit);
 void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax = 0);
 // hom_scan.cu: the Burgers homogeneous scan as one persistent cooperative kernel
 bool hom_scan_ok(int n, int kcap);
 size_t hom_scan_bytes(int n, int s, int kcap, int P);
 int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P, int s, int n, int kcap, double h,
                     double eta, double defl, const double* u0, const double* Y, const double* Uold, double* Unew,
-                    double* delta, char* ws, size_t ws_bytes, int* kscan_rec = nullptr);
+                    double* delta, char* ws, size_t ws_bytes, int* kscan_rec = nullptr,
+                    double* diag = nullptr);  // diag[3] += Arnoldi steps, checks, checker cycles
 void launch_restart_finish(cudaStream_t st, int E, int m, int kcap, const double* R, const double* TX, double* CPL,
                            int* Dn, int* Kl, const int* kplast, double* H, long long hs_e, int* live,
                            const int* active);

@@ -1288,6 +1288,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
     double* rec_g = st_out ? st_out->gamma_j : nullptr;
     int32_t* rec_ks = st_out ? st_out->kscan_j : nullptr;
     std::vector<double> dhist;
+    double scan_diag[3] = {0.0, 0.0, 0.0};
     std::vector<std::unique_ptr<EventPair>> scan_ev;  // homogeneous scan + waveform update per iteration
     std::vector<int> iota(P);
     for (int j = 0; j < P; ++j) iota[j] = j;
@@ -1338,7 +1339,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
         const double defl_s = g_cfg.defl;
         max_k = std::max(max_k, launch_hom_scan(st, L.F, L.B.gam, P, s, n, k1, h, eta, defl_s, u0, L.Y, L.Uk, L.Un,
                                                 L.delta, L.scan_ws, L.scan_bytes,
-                                                rec_ks ? rec_ks + size_t(k) * P : nullptr));
+                                                rec_ks ? rec_ks + size_t(k) * P : nullptr, scan_diag));
       } else
       for (int i = 0; i < P; ++i) {
         const size_t off = size_t(i) * s * n;
@@ -1391,6 +1392,9 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       st_out->restarts = restarts;
       st_out->ms_total = ms;
       for (auto& e : scan_ev) st_out->ms_hom += e->ms();
+      st_out->scan_steps = scan_diag[0];
+      st_out->scan_checks = scan_diag[1];
+      st_out->scan_check_cycles = scan_diag[2];
       st_out->ms_nonhom = ms - st_out->ms_hom;
       st_out->evals = P * iters;
       st_out->kernel_launches = (int)g_launches;

@@ -46,7 +46,8 @@ class Stats(C.Structure):
                 ("ms_total", C.c_float), ("evals", C.c_int32), ("kernel_launches", C.c_int32),
                 ("host_syncs", C.c_int32), ("delta_hist", C.c_double * 64),
                 ("m_j", C.POINTER(C.c_int32)), ("k_j", C.POINTER(C.c_int32)), ("gamma_j", C.POINTER(C.c_double)),
-                ("kscan_j", C.POINTER(C.c_int32)), ("ms_nonhom", C.c_float), ("ms_hom", C.c_float)]
+                ("kscan_j", C.POINTER(C.c_int32)), ("ms_nonhom", C.c_float), ("ms_hom", C.c_float),
+                ("scan_steps", C.c_double), ("scan_checks", C.c_double), ("scan_check_cycles", C.c_double)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("delta_hist", "m_j", "k_j", "gamma_j", "kscan_j")}

@@ -44,7 +44,7 @@ for _ in range(a.repeat):
     t0 = time.perf_counter()
     out, st = run(False)
     torch.cuda.synchronize()
-    print("plain solve", round(time.perf_counter() - t0, 3), "s", {k: st[k] for k in ("ms_total", "wr_iters", "max_m", "max_k", "host_syncs", "kernel_launches")}, flush=True)
+    print("plain solve", round(time.perf_counter() - t0, 3), "s", {k: st[k] for k in ("ms_total", "ms_hom", "wr_iters", "max_m", "max_k", "host_syncs", "kernel_launches", "scan_steps", "scan_checks", "scan_check_cycles")}, flush=True)
 if a.plain_only:
     sys.exit(0)
 pexp.profile_enable(True)

@@ -36,11 +36,15 @@ def grid_x(n: int, bc: str) -> np.ndarray:
     raise ValueError(bc)
 
 
-def node_times(T: float, P: int, s: int) -> np.ndarray:
-    """[P][s] sample times t_{j,i} = j*dT + i*(dT/(s-1))."""
+def node_times(T: float, P: int, s: int, node_rule: int = 0) -> np.ndarray:
+    """[P][s] sample times.  node_rule 0 (default): uniform, t_{j,i} = j*dT + i*(dT/(s-1));
+    node_rule 1: Chebyshev-Lobatto points of each subinterval ("Chebyshev nodes",
+    endpoints included as in P:64), t_{j,i} = j*dT + (dT/2)(1 - cos(pi i/(s-1)))."""
     dT = T / P
     j = np.arange(P, dtype=np.float64)[:, None]
     i = np.arange(s, dtype=np.float64)[None, :]
+    if node_rule == 1:
+        return j * dT + 0.5 * dT * (1.0 - np.cos(np.pi * i / (s - 1)))
     return j * dT + i * (dT / (s - 1))
 
 
@@ -86,7 +90,7 @@ def _fourier(x, k, c, s_):
     return c * np.cos(2 * np.pi * k * x) + s_ * np.sin(2 * np.pi * k * x)
 
 
-def config1(n=256, P=8, s=32, T=1.0, tol=1e-8, seed=1) -> LinearProblem:
+def config1(n=256, P=8, s=32, T=1.0, tol=1e-8, seed=1, node_rule=0) -> LinearProblem:
     """C1: periodic ADE, a=1, nu=1e-2; 4-mode u0 (k distinct in 1..8), rank-3 source."""
     r = _rng(seed)
     x = grid_x(n, PERIODIC)
@@ -96,7 +100,7 @@ def config1(n=256, P=8, s=32, T=1.0, tol=1e-8, seed=1) -> LinearProblem:
     kap = r.integers(1, 9, size=3)
     ga, de = r.standard_normal(3), r.standard_normal(3)
     w = r.uniform(1.0, 5.0, size=3)
-    t = node_times(T, P, s)
+    t = node_times(T, P, s, node_rule)
     modes = np.stack([_fourier(x, kap[q], ga[q], de[q]) for q in range(3)])   # [3][n]
     temp = np.stack([np.sin(2 * np.pi * w[q] * t) for q in range(3)])        # [3][P][s]
     src = np.einsum("rps,rn->psn", temp, modes)
@@ -175,7 +179,7 @@ def _bump(x, c, w):
 
 
 def generic_linear(n=256, bc=PERIODIC, nu=1e-2, a=1.0, P=4, s=16, T=0.5, tol=1e-8,
-                   rank=3, seed=11, noise=0.0) -> LinearProblem:
+                   rank=3, seed=11, noise=0.0, node_rule=0) -> LinearProblem:
     """Non-Fourier data (periodic Gaussian bumps): the Krylov space is NOT invariant,
     so the block Arnoldi runs deep."""
     r = _rng(seed)
@@ -183,7 +187,7 @@ def generic_linear(n=256, bc=PERIODIC, nu=1e-2, a=1.0, P=4, s=16, T=0.5, tol=1e-
     u0 = _bump(x, r.uniform(0.2, 0.8), r.uniform(0.05, 0.1))
     if bc == DIRICHLET:
         u0 = u0 * np.sin(np.pi * x)
-    t = node_times(T, P, s)
+    t = node_times(T, P, s, node_rule)
     modes = np.stack([r.standard_normal() * _bump(x, r.uniform(0, 1), r.uniform(0.03, 0.1))
                       for _ in range(rank)])
     w = r.uniform(1.0, 5.0, size=rank)

@@ -42,7 +42,7 @@ def pulse_exact(x, t, a=1.0):
     return 0.5 - 0.5 * np.cos(10 * np.pi * (x - a * t))
 
 
-def pulse_ade(P=2, dT=0.5, n=1000, s=64, tol=1e-4, nu=1e-2, a=1.0, T=None) -> LinearProblem:
+def pulse_ade(P=2, dT=0.5, n=1000, s=64, tol=1e-4, nu=1e-2, a=1.0, T=None, node_rule=0) -> LinearProblem:
     """f1 workload: Eq.(ade) u_t + a u_x = ν u_xx + f with the five-pulse solution Eq.(manusol).
 
     f = u_t + a u_x - ν u_xx of the exact solution (continuous source):
@@ -53,7 +53,7 @@ def pulse_ade(P=2, dT=0.5, n=1000, s=64, tol=1e-4, nu=1e-2, a=1.0, T=None) -> Li
     x, so only the spline error of sin(10πt) changes, ~1e-8 relative)."""
     T = P * dT if T is None else T
     x = grid_x(n, PERIODIC)
-    t = node_times(T, P, s)                                        # [P][s]
+    t = node_times(T, P, s, node_rule)                             # [P][s]
     th = 10 * np.pi * (x[None, None, :] - a * t[:, :, None])
     src = -50 * np.pi ** 2 * nu * np.cos(th)
     u0 = pulse_exact(x, 0.0, a)
