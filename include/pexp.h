@@ -29,7 +29,9 @@
  *     NUL-terminated message owned by the context (valid until the next call on it).
  *   - Grids (reading #15): periodic x_i = i/n, dx = 1/n; Dirichlet x_i = (i+1)/(n+1),
  *     dx = 1/(n+1), zero boundary values.  Sample nodes (reading #9): with dT = T/P,
- *     t_{j,i} = j*dT + i*(dT/(s-1)), j = 0..P-1, i = 0..s-1 (endpoints included).
+ *     t_{j,i} = j*dT + i*(dT/(s-1)), j = 0..P-1, i = 0..s-1 (endpoints included); with
+ *     pexp_options.node_rule = 1 the Chebyshev-Lobatto points of each subinterval instead.
+ *     pexp_sample_times returns the nodes of the context's rule.
  */
 #ifndef PEXP_H
 #define PEXP_H
@@ -65,7 +67,11 @@ typedef enum { PEXP_BC_PERIODIC = 0, PEXP_BC_DIRICHLET = 1 } pexp_bc;
 /* Method options.  A zero-initialised struct means "defaults". */
 typedef struct {
   int32_t s;              /* source samples per subinterval, >= 4 (default 32)           */
-  int32_t node_rule;      /* 0 = uniform incl. endpoints (only value supported)         */
+  int32_t node_rule;      /* 0 = uniform nodes incl. endpoints, p(t) = not-a-knot cubic spline (default);
+                             1 = Chebyshev-Lobatto nodes t_{j,i} = j*dT + (dT/2)(1 - cos(pi i/(s-1)))
+                             (P:451), p(t) = the degree-(s-1) interpolant through them, integrated
+                             through its 12-term Taylor polynomials on s-1 uniform pieces (DESIGN.md
+                             §3 #23).  Linear solves only; needs k_max + 12 s <= 1024          */
   double svd_tau_factor;  /* truncation tau_svd = factor*tol relative to sigma_1 (0.01)  */
   double stop_factor;     /* Krylov stop eta = factor*tol (default 0.1; DESIGN.md §3 #6)  */
   int32_t restart_blocks; /* restart a Krylov cycle after this many block steps (P:451:

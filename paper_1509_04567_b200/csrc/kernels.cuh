@@ -193,7 +193,7 @@ void small_init();
 // stencil.cu: width buckets of the forced EBK (gather into / scatter out of a chunk)
 struct GatherArgs {
   const int* perm;
-  int wb, mmax, s, n;
+  int wb, mmax, s, n, nq;
   const double *gam, *crit, *coef, *U;
   long long us_e;
   const int *active, *fidx, *opidx;

@@ -67,10 +67,13 @@ static void h2d(cudaStream_t st, T* dst, const std::vector<T>& v) {
 }
 
 // ---------------------------------------------------------------- options
+// node_rule 1: p(t) = the degree-(s-1) interpolant through the Chebyshev-Lobatto
+// nodes, integrated through its Taylor polynomials of NQ_CHEB terms on the s-1 uniform pieces
+constexpr int NQ_CHEB = 12;
 struct Opts {
   int s;
   double tau_f, eta_f;
-  int restart_blocks, kcap, stop_rule, kcyc, chunk;
+  int restart_blocks, kcap, stop_rule, kcyc, chunk, nq, node_rule;
   cudaStream_t st;
   CallCfg cfg;
 };
@@ -92,12 +95,16 @@ static Opts norm_opts(const pexp_options& o) {
   r.cfg.hom_group = o.hom_group > 0 ? std::min(o.hom_group, 16) : 8;
   r.cfg.buckets = o.width_buckets >= 0 ? 1 : 0;
   r.cfg.syncs = 0;
+  r.node_rule = o.node_rule;
+  r.nq = o.node_rule == 1 ? NQ_CHEB : 4;
+  r.cfg.nq = r.nq;
+  r.cfg.node_rule = r.node_rule;
   return r;
 }
 
 // ---------------------------------------------------------------- EBK buffers
 struct EbkBufs {
-  int E = 0, n = 0, kcap = 0, ktot = 0, mcap = 0, nout = 0, s = 0, groups = 1;
+  int E = 0, n = 0, kcap = 0, ktot = 0, mcap = 0, nout = 0, s = 0, groups = 1, nq = 4;
   long long vs_e = 0, hs_e = 0, zs_e = 0;
   double *V, *H, *Z, *Gt, *Wt, *Wt2, *T, *G0, *G1, *Rinv, *Rtmp, *res, *gam, *crit, *beta, *coef, *n0p, *R0, *critc;
   int *live, *active, *conv, *kfin, *npieces, *count, *fidx, *opidx, *xcnt, *horc, *krec;
@@ -139,8 +146,9 @@ static size_t part_need(int E, int n, int nx, int ny) {
 // kcap: basis columns per evaluation and cycle; ktot: total Krylov dimension over all cycles
 // (ktot > kcap or restart_blocks > 0 allocates the nested-restart state).
 static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int ktot, int mcap, int nout, int s,
-                      bool forced, double* Wt_shared, bool restartable, int ycols = 0) {
+                      bool forced, double* Wt_shared, bool restartable, int ycols = 0, int nq = 4) {
   Ec = std::max(1, std::min(E, Ec));
+  B.nq = nq;
   B.E = Ec; B.n = n; B.kcap = kcap; B.ktot = ktot; B.mcap = mcap; B.nout = nout; B.s = s;
   B.vs_e = (long long)kcap * n;
   B.hs_e = (long long)kcap * kcap;
@@ -150,7 +158,7 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   B.gam = ar.take<double>(E);
   B.crit = ar.take<double>(E);
   B.beta = ar.take<double>(size_t(E) * mcap);
-  B.coef = forced ? ar.take<double>(size_t(E) * (s - 1) * 4 * mcap) : nullptr;
+  B.coef = forced ? ar.take<double>(size_t(E) * (s - 1) * nq * mcap) : nullptr;
   B.active = ar.take<int>(E);
   B.conv = ar.take<int>(E);
   B.kfin = ar.take<int>(E);
@@ -182,6 +190,8 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
   // the SVD stage (all E, s x s products) shares the partial-sum buffer with the chunks
   B.part_cap = std::max(part_need(Ec, n, std::max(kcap, s), forced ? std::max(mcap, s) : mcap),
                         forced ? part_need(E, n, s, s) : size_t(0));
+  if (forced && stream_ok(n, 32))  // SVD-stage products with up to s columns through the streaming kernels
+    B.part_cap = std::max(B.part_cap, stream_part_doubles(E, n, s, std::min(s, 32)));
   B.part = ar.take<double>(B.part_cap);
   {
     const size_t sw = arnoldi_scratch_doubles(Ec, kcap, mcap);
@@ -191,7 +201,7 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
     B.spart_cap = stream_part_doubles(Ec, n, kcap + std::min(mcap, 32), std::min(mcap, 32));
     B.spart = ar.take<double>(B.spart_cap);
   }
-  B.Nmax = ktot + (forced ? 4 * mcap : 0);
+  B.Nmax = ktot + (forced ? nq * mcap : 0);
   B.work_slot = 10LL * B.Nmax * B.Nmax;
   B.iwork_slot = B.Nmax;
   // one workspace slot per resident cluster; large projected problems get one per SM
@@ -207,7 +217,7 @@ static void alloc_ebk(Arena& ar, EbkBufs& B, int E, int Ec, int n, int kcap, int
     B.fidx_c = ar.take<int>(Ec);
     B.opidx_c = ar.take<int>(Ec);
     B.krec_c = ar.take<int>(Ec);
-    B.coef_c = ar.take<double>(size_t(Ec) * (s - 1) * 4 * mcap);
+    B.coef_c = ar.take<double>(size_t(Ec) * (s - 1) * nq * mcap);
     B.Ytmp = ar.take<double>(size_t(Ec) * ycols * n);
   }
   if (restartable) {
@@ -227,7 +237,7 @@ static EbkBufs chunk_view(const EbkBufs& B, int c0, int Ec, int mb) {
   C.res += c0; C.gam += c0; C.crit += c0; C.active += c0; C.conv += c0; C.kfin += c0;
   C.npieces += c0; C.fidx += c0; C.opidx += c0; C.xcnt += c0; C.krec += c0;
   C.beta += c0;  // kind-1 layout (forced chunks do not read beta)
-  if (C.coef) C.coef += size_t(c0) * (B.s - 1) * 4 * mb;
+  if (C.coef) C.coef += size_t(c0) * (B.s - 1) * B.nq * mb;
   return C;
 }
 
@@ -345,7 +355,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   a.npieces = kind == 1 ? B.npieces : nullptr;
   a.npieces_const = npieces_const;
   a.out_stride = out_stride; a.nout = nout;
-  a.coef = B.coef; a.s = B.s;
+  a.coef = B.coef; a.s = B.s; a.nq = B.nq;
   a.beta = B.beta; a.crit = B.crit;
   a.Gt = B.Gt; a.gts_e = (long long)m * m;
   a.Z = B.Z; a.zs_e = B.zs_e;
@@ -546,7 +556,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
 
 // ---------------------------------------------------------------- source SVD stage
 struct SvdBufs {
-  double *U, *R, *Gs, *lam, *Msel, *sigma1, *Cb, *Qs, *Cs, *sig, *Cfin, *Rinv, *Kinv;
+  double *U, *R, *Gs, *lam, *Msel, *sigma1, *Cb, *Qs, *Cs, *sig, *Cfin, *Rinv, *Kinv, *Dmat;
   int *off, *me, *fill;
 };
 
@@ -564,6 +574,7 @@ static void alloc_svd(Arena& ar, SvdBufs& S, int E, int n, int s) {
   S.Cfin = ar.take<double>(size_t(E) * s * s);
   S.Rinv = ar.take<double>(size_t(E) * s * s);
   S.Kinv = ar.take<double>(size_t(s) * s);
+  S.Dmat = ar.take<double>(size_t(s - 1) * NQ_CHEB * s);
   S.off = ar.take<int>(E);
   S.me = ar.take<int>(E);
   S.fill = ar.take<int>(size_t(E) * s);
@@ -592,6 +603,46 @@ static std::vector<double> notaknot_inverse(int s) {
       }
   }
   return I;
+}
+
+// node_rule 1 ("Chebyshev nodes", "other types of p(t) possible"; DESIGN.md §3 #23):
+// the linear map from the s values at the Chebyshev-Lobatto nodes tau_k = (dT/2)(1 - cos(pi k/(s-1)))
+// to the Taylor coefficients p^{(q)}(sigma_i), q < nq, of THE degree-(s-1) interpolant p at the uniform
+// piece starts sigma_i = i dT/(s-1):  D[(i*nq + q)*s + k].  Host, once per solve, in long double:
+// Chebyshev coefficients by the discrete cosine formula, derivatives by the coefficient recurrence
+// d_{j-1} = d_{j+1} + 2 j c_j (scaled by 2/dT), values by the three-term recurrence.
+static std::vector<double> cheb_taylor_matrix(int s, int nq, double dT) {
+  typedef long double ld;
+  const int N = s - 1;
+  const ld pi = acosl(-1.0L);
+  std::vector<double> D(size_t(N) * nq * s, 0.0);
+  std::vector<ld> c(N + 1), d(N + 2), Tj(N + 1);
+  for (int k = 0; k <= N; ++k) {
+    // plain Chebyshev coefficients of the cardinal polynomial of node k: x_k = -cos(pi k/N)
+    const ld wk = (k == 0 || k == N) ? 0.5L : 1.0L;
+    for (int j = 0; j <= N; ++j) {
+      const ld wj = (j == 0 || j == N) ? 0.5L : 1.0L;
+      c[j] = wj * (2.0L / N) * wk * cosl(pi * ld(j) * ld(N - k) / ld(N));
+    }
+    for (int q = 0; q < nq; ++q) {
+      if (q > 0) {  // c <- coefficients of dp/dtau
+        std::fill(d.begin(), d.end(), 0.0L);
+        for (int j = N; j >= 1; --j) d[j - 1] = d[j + 1] + 2.0L * j * c[j];
+        d[0] *= 0.5L;
+        for (int j = 0; j <= N; ++j) c[j] = d[j] * (2.0L / ld(dT));
+      }
+      for (int i = 0; i < N; ++i) {
+        const ld x = 2.0L * ld(i) / ld(N) - 1.0L;
+        Tj[0] = 1.0L;
+        if (N >= 1) Tj[1] = x;
+        for (int j = 2; j <= N; ++j) Tj[j] = 2.0L * x * Tj[j - 1] - Tj[j - 2];
+        ld v = 0.0L;
+        for (int j = N; j >= 0; --j) v += c[j] * Tj[j];
+        D[(size_t(i) * nq + q) * s + k] = double(v);
+      }
+    }
+  }
+  return D;
 }
 
 // Two-pass Gram SVD (subsystem 3) of E sample matrices G [E][s][n]; writes V block 0
@@ -680,9 +731,15 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
       PEXP_CUDA_TRY(cudaMemcpyAsync(S.U, Fr, size_t(E) * gs_e * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
   }
-  std::vector<double> Ki = notaknot_inverse(s);
-  h2d(st, S.Kinv, Ki);
-  launch_spline(st, E, s, mb, S.Kinv, S.Cfin, h, eta, B->coef, B->crit);
+  if (g_cfg.node_rule == 1) {
+    std::vector<double> Dm = cheb_taylor_matrix(s, g_cfg.nq, h * (s - 1));
+    h2d(st, S.Dmat, Dm);
+    launch_poly_coef(st, E, s, mb, g_cfg.nq, S.Dmat, S.Cfin, eta, B->coef, B->crit);
+  } else {
+    std::vector<double> Ki = notaknot_inverse(s);
+    h2d(st, S.Kinv, Ki);
+    launch_spline(st, E, s, mb, S.Kinv, S.Cfin, h, eta, B->coef, B->crit);
+  }
   k_active_from_m<<<cdiv(E, 256), 256, 0, st>>>(E, S.me, B->active);
   count_launch();
   PEXP_LAUNCH_CHECK();
@@ -812,7 +869,7 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
   L.Yend = ar.take<double>(size_t(E) * n);
   alloc_svd(ar, L.S, E, n, s);
   const bool restartable = o.restart_blocks > 0 || o.kcyc < o.kcap;
-  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable, 1);
+  alloc_ebk(ar, L.B, E, o.chunk, n, o.kcyc, o.kcap, s, 2, s, true, L.S.R, restartable, 1, o.nq);
   if (P > 1) {
     const int mh = hom_group_width(c, P), G = cdiv(P - 1, mh), Eg = Bt * G;
     // a group of mh legs needs a wider space than one forced evaluation (measured on C2:
@@ -978,7 +1035,7 @@ static RunInfo ebk_forced_bucketed(cudaStream_t st, EbkBufs& B, const SvdBufs& S
     for (int c0 = 0; c0 < nb; c0 += Ecap) {
       const int ec = std::min(Ecap, nb - c0);
       GatherArgs ga{};
-      ga.perm = B.perm + p0; ga.wb = wb; ga.mmax = std::max(mmax, 1); ga.s = s; ga.n = n;
+      ga.perm = B.perm + p0; ga.wb = wb; ga.mmax = std::max(mmax, 1); ga.s = s; ga.n = n; ga.nq = B.nq;
       ga.gam = B.gam; ga.crit = B.crit; ga.coef = B.coef; ga.U = S.U; ga.us_e = (long long)s * n;
       ga.active = B.active; ga.fidx = B.fidx; ga.opidx = B.opidx;
       ga.gam_c = B.gam_c; ga.crit_c = B.crit_c; ga.coef_c = B.coef_c; ga.V = B.V; ga.vs_e = B.vs_e;
@@ -1040,8 +1097,10 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
   pexp_options o{};
   if (opt) o = *opt;
   if (o.s != 0 && (o.s < 4 || o.s > 64)) return PEXP_EINVAL;
-  if (o.node_rule != 0) return PEXP_EINVAL;
+  if (o.node_rule < 0 || o.node_rule > 1) return PEXP_EINVAL;
   if (o.k_max < 0 || o.k_max > KSMALL_MAX - 64) return PEXP_EINVAL;
+  // projected-problem capacity: K + nq*m <= KSMALL_MAX with m <= s (node_rule 1: nq = 12)
+  if (o.node_rule == 1 && (o.k_max > 0 ? o.k_max : 256) + NQ_CHEB * (o.s > 0 ? o.s : 32) > KSMALL_MAX) return PEXP_EINVAL;
   if (o.stop_rule < 0 || o.stop_rule > 1) return PEXP_EINVAL;
   if (o.basis_cols < 0 || o.eval_chunk < 0) return PEXP_EINVAL;
   if (o.route < 0 || o.route > 2 || o.defl_tol < 0 || o.piv_tol < 0 || o.hom_group < 0 || o.hom_group > 16)
@@ -1066,8 +1125,11 @@ pexp_status pexp_sample_times(const pexp_ctx* ctx, double T, int32_t P, double* 
   if (!ctx || !t_host || !(T > 0) || P < 1) return PEXP_EINVAL;
   Opts o = norm_opts(ctx->opt);
   const double dT = T / P;
+  const double pi = std::acos(-1.0);
   for (int j = 0; j < P; ++j)
-    for (int i = 0; i < o.s; ++i) t_host[size_t(j) * o.s + i] = j * dT + i * (dT / (o.s - 1));
+    for (int i = 0; i < o.s; ++i)
+      t_host[size_t(j) * o.s + i] = o.node_rule == 1 ? j * dT + 0.5 * dT * (1.0 - std::cos(pi * i / (o.s - 1)))
+                                                     : j * dT + i * (dT / (o.s - 1));
   return PEXP_OK;
 }
 
@@ -1262,6 +1324,8 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
   if (!u0 || !out) return set_err(ctx, PEXP_EINVAL, "null array argument");
   if (ctx->bc != PEXP_BC_PERIODIC || ctx->batch != 1)
     return set_err(ctx, PEXP_EINVAL, "Burgers requires a periodic context with batch 1");
+  if (ctx->opt.node_rule != 0)
+    return set_err(ctx, PEXP_EINVAL, "Burgers requires uniform sample nodes (node_rule 0)");
   if (!(nu > 0) || !std::isfinite(nu)) return set_err(ctx, PEXP_EINVAL, "nu must be > 0");
   if (!(T > 0)) return set_err(ctx, PEXP_EINVAL, "T must be > 0");
   if (P < 1) return set_err(ctx, PEXP_EINVAL, "P must be >= 1");

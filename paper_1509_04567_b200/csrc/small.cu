@@ -508,6 +508,36 @@ __global__ void k_build_final(int s, int mmax, const int* kk_arr, const double* 
     fill[e * mmax + c] = !(c < kk && sig[size_t(e) * s + c] > 0.0);
 }
 
+// ---------------------------------------------------------------- Chebyshev interpolant pieces
+// node_rule 1: coef_e[i][q][c] = sum_k Dmat[(i*nq + q)*s + k] * Cfin_e[c][k]  (Cfin col-major mmax x s:
+// the coefficient rows at the Chebyshev-Lobatto nodes);  crit[e] = eta * max_k ||Cfin[:, k]||.
+__global__ void k_poly_coef(int s, int mmax, int nq, const double* Dmat, const double* Cfin, double eta,
+                            double* coef, double* crit) {
+  const int e = blockIdx.x;
+  extern __shared__ double sm[];
+  double* Y = sm;  // [s][mmax] (as stored)
+  __shared__ double red[32];
+  const double* Ce = Cfin + size_t(e) * mmax * s;
+  for (int idx = threadIdx.x; idx < mmax * s; idx += blockDim.x) Y[idx] = Ce[idx];
+  __syncthreads();
+  double* ce = coef + size_t(e) * (s - 1) * nq * mmax;
+  for (int idx = threadIdx.x; idx < (s - 1) * nq * mmax; idx += blockDim.x) {
+    const int c = idx % mmax, iq = idx / mmax;
+    const double* Dr = Dmat + size_t(iq) * s;
+    double a = 0.0;
+    for (int k = 0; k < s; ++k) a = fma(Dr[k], Y[c + k * mmax], a);
+    ce[idx] = a;
+  }
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < s; k += blockDim.x) {
+    double a = 0.0;
+    for (int c = 0; c < mmax; ++c) a += Y[c + k * mmax] * Y[c + k * mmax];
+    mx = fmax(mx, sqrt(a));
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) crit[e] = eta * mx;
+}
+
 // ---------------------------------------------------------------- not-a-knot spline
 // Kinv: inverse of the s x s not-a-knot second-derivative system (host-computed, depends
 // only on s).  Cfin_e: mmax x s samples.  coef_e: [s-1][4][mmax] Taylor coefficients
@@ -608,7 +638,8 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPAr
     const int D = a.Dn ? a.Dn[e] : 0;
     const int Kl = a.Kl ? a.Kl[e] : 0;
     const int Dz = D + Kp;
-    const int Nn = Dz + (forced ? 4 * m : 0);
+    const int nq = a.nq;
+    const int Nn = Dz + (forced ? nq * m : 0);
     double* NAe = a.NA ? a.NA + e * a.nas_e : nullptr;
     const double* CPe = a.CPL ? a.CPL + e * a.cpls_e : nullptr;
     // Hs -> S0, Hinv -> S1
@@ -640,7 +671,7 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPAr
         }
       }
       // polynomial chain: unscaled identity blocks (the h^q factors are applied in the chain)
-      if (forced && i >= Dz && j - i == m && i < Dz + 3 * m) S2[i + size_t(j) * ld] = 1.0;
+      if (forced && i >= Dz && j - i == m && i < Dz + (nq - 1) * m) S2[i + size_t(j) * ld] = 1.0;
       else S2[i + size_t(j) * ld] = a.h * v;
     }
     if (wr && g.rank == 0) {  // TX = (1/gamma) H_tail X, X = last-block rows of H^{-1}
@@ -678,14 +709,14 @@ __global__ void __launch_bounds__(PEXP_THREADS, SMALL_MINB) k_small_problem(SPAr
       double* Fo = WK;                      // [np][Dz] forcing of every piece
       double* Rg = WK + size_t(np) * Dz;    // [mt][Kp]
       double* Ze = a.Z + e * a.zs_e;
-      const double* cf = forced ? a.coef + size_t(e) * (a.s - 1) * 4 * m : nullptr;
+      const double* cf = forced ? a.coef + size_t(e) * (a.s - 1) * nq * m : nullptr;
       for (int t = threadIdx.x + g.rank * blockDim.x; t < a.nout * a.kcap; t += blockDim.x * g.size) Ze[t] = 0.0;
       if (forced)
         for (int t = threadIdx.x; t < nr * np; t += blockDim.x) {
           const int r = r0 + t % nr, i = t / nr;
-          const double* ci = cf + size_t(i) * 4 * m;
+          const double* ci = cf + size_t(i) * nq * m;
           double v = 0.0, hq = 1.0;
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < nq; ++q) {
             const double* B = S2 + size_t(Dz + q * m) * ld;
             double acc = 0.0;
             for (int c = 0; c < m; ++c) acc = fma(B[r + size_t(c) * ld], ci[q * m + c], acc);
@@ -1080,11 +1111,19 @@ void launch_spline(cudaStream_t st, int E, int s, int mmax, const double* Kinv, 
   PEXP_LAUNCH_CHECK();
 }
 
+void launch_poly_coef(cudaStream_t st, int E, int s, int mmax, int nq, const double* Dmat, const double* Cfin,
+                      double eta, double* coef, double* crit) {
+  ProfScope ps(PC_SVDSMALL, st, 0.0, 0.0);
+  k_poly_coef<<<E, PEXP_THREADS, size_t(mmax) * s * sizeof(double), st>>>(s, mmax, nq, Dmat, Cfin, eta, coef, crit);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
 void launch_small_problem(cudaStream_t st, const SPArgs& a, int nslots, int Dmax) {
   if (Dmax + a.K + a.m > KSMALL_MAX) fail(1, "Krylov dimension exceeds the small-problem capacity");
   size_t smem = SP_DYN;
   {
-  const double N = Dmax + a.K + (a.kind == 0 ? 4.0 * a.m : 0.0);
+  const double N = Dmax + a.K + (a.kind == 0 ? double(a.nq) * a.m : 0.0);
   ProfScope ps(PC_SMALL, st, 0.0, eact(a.E, a.active) * (22.0 * N * N * N + 2.0 * a.K * a.K * a.K));
   const int ncl = std::min(a.E, nslots);
   launch_clustered(k_small_problem, ncl, cluster_size_for(ncl), smem, st, a);

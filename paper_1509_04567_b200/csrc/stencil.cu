@@ -266,7 +266,7 @@ __global__ void k_fill_f64(double* p, size_t count, double v) {
 // ---------------------------------------------------------------- width buckets (pexp_api.cu)
 // Gather evaluations perm[0..ec) into the slots of one EBK chunk of block width wb: per-eval
 // scalars, the first wb columns of the orthonormal source basis (basis block 0) and the first wb
-// coefficient rows of the cubic spline (layout [s-1][4][w], w = mmax -> wb).
+// coefficient rows of the piecewise polynomial p(t) (layout [s-1][nq][w], w = mmax -> wb).
 __global__ void k_bucket_gather(GatherArgs a) {
   const int i = blockIdx.y, e = a.perm[i];
   if (blockIdx.x == 0) {
@@ -277,7 +277,7 @@ __global__ void k_bucket_gather(GatherArgs a) {
       a.fidx_c[i] = a.fidx[e];
       a.opidx_c[i] = a.opidx[e];
     }
-    const int np = (a.s - 1) * 4;
+    const int np = (a.s - 1) * a.nq;
     for (int idx = threadIdx.x; idx < np * a.wb; idx += blockDim.x) {
       const int pq = idx / a.wb, c = idx % a.wb;
       a.coef_c[size_t(i) * np * a.wb + idx] = a.coef[size_t(e) * np * a.mmax + size_t(pq) * a.mmax + c];

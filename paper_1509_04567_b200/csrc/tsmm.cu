@@ -456,6 +456,17 @@ void launch_xty(cudaStream_t st, int E, int n, const double* X, long long xs_e, 
                 double* D, long long ds_e, int ldd, int row0, int col0, bool accumulate,
                 const int* active, int* cnt) {
   if (E == 0 || nx == 0 || ny == 0) return;
+  if (ny > 32 && ny <= 64 && stream_ok(n, 32) && stream_part_doubles(E, n, nx, 32) <= part_cap) {
+    // wide right-hand blocks (the s = 64 source Grams of the SVD stage): two passes of the streaming
+    // kernel over 32-column halves of Y (X is streamed twice; still ~3x faster than the register-tiled
+    // square-Gram kernel on long columns)
+    for (int h0 = 0; h0 < ny; h0 += 32) {
+      const int nh = std::min(32, ny - h0);
+      launch_sproj(st, E, n, X + size_t(x0) * n, xs_e, nx, Y + size_t(y0 + h0) * n, ys_e, nh, part, part_cap, D, ds_e,
+                   ldd, row0, col0 + h0, accumulate, nullptr, 0, active);
+    }
+    return;
+  }
   if (stream_ok(n, ny)) {  // TMA-fed DMMA streaming kernels (stream.cu)
     const bool gram = X == Y && xs_e == ys_e && x0 == y0 && nx == ny;
     const int pw = gram ? ny : nx;

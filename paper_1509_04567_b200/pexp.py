@@ -116,7 +116,7 @@ class Context:
                  svd_tau_factor: float = 0.01, stop_factor: float = 0.1, restart_blocks: int = 20,
                  stream: Optional[torch.cuda.Stream] = None, stop_rule: int = 0, basis_cols: int = 0,
                  eval_chunk: int = 0, route: int = 0, defl_tol: float = 0.0, piv_tol: float = 0.0,
-                 hom_group: int = 0, width_buckets: int = 0):
+                 hom_group: int = 0, width_buckets: int = 0, node_rule: int = 0):
         self.n, self.bc, self.s = int(n), bc, int(s)
         self._stream = stream
         nu = [float(v) for v in (nu if hasattr(nu, "__len__") else [nu])]
@@ -125,7 +125,7 @@ class Context:
             a = a * len(nu)
         self.batch = len(nu)
         handle = stream.cuda_stream if stream is not None else None  # None = legacy default stream
-        self.opt = Options(self.s, 0, svd_tau_factor, stop_factor, restart_blocks, k_max, handle, stop_rule,
+        self.opt = Options(self.s, int(node_rule), svd_tau_factor, stop_factor, restart_blocks, k_max, handle, stop_rule,
                            basis_cols, eval_chunk, route, defl_tol, piv_tol, hom_group, width_buckets)
         self._h = _P()
         arr = C.c_double * self.batch

@@ -69,6 +69,17 @@ def test_sample_times_match_synth_convention(P):
     np.testing.assert_array_equal(t, synth.node_times(0.9, 5, 7))
 
 
+def test_sample_times_chebyshev_rule(P):
+    """node_rule = 1 (row f3): Chebyshev-Lobatto nodes of each subinterval, endpoints included."""
+    c = P.Context(50, "periodic", 1e-2, 1.0, s=9, node_rule=1)
+    t = c.sample_times(0.9, 5).numpy()
+    np.testing.assert_allclose(t, synth.node_times(0.9, 5, 9, node_rule=1), rtol=0, atol=2e-16)
+    with pytest.raises(P.PexpError):
+        P.Context(50, "periodic", 1e-2, 1.0, s=64, k_max=512, node_rule=1)   # K + 12 s > capacity
+    with pytest.raises(P.PexpError):
+        P.Context(50, "periodic", 1e-2, 1.0, node_rule=2)
+
+
 def test_workspace_query_and_solve_without_workspace(P):
     c = P.Context(128, "periodic", 1e-2, 1.0, s=8)
     assert c.workspace_bytes(4, 0) > 0

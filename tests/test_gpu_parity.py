@@ -524,3 +524,43 @@ def test_stage_wr_map_on_steep_iterate(route):
     assert rel(out.cpu().numpy(), ref[:, -1, :]) < 1e-8
     assert abs(st["wr_last_delta"] - np.max(np.abs(ref - Uk))) < 1e-8
     assert st["max_m"] > 1
+
+
+# ---------------------------------------------------------------- f3: Chebyshev nodes, higher-order p(t)
+
+@pytest.mark.parametrize("route", ROUTES)
+@pytest.mark.parametrize("make", [
+    lambda: synth.config1(node_rule=1),
+    lambda: synth.generic_linear(n=777, bc="periodic", nu=5e-3, a=1.3, P=5, s=12, T=0.5, seed=7, node_rule=1),
+    lambda: synth.generic_linear(n=600, bc="dirichlet", nu=1e-3, a=1.0, P=5, s=20, T=0.5, seed=7, node_rule=1),
+], ids=["c1", "generic-periodic", "generic-dirichlet"])
+def test_f3_chebyshev_nodes(make, route):
+    """f3 (P:451 Chebyshev nodes; higher-order p(t)): pexp_options.node_rule = 1 against the oracle's
+    node_rule = 1 (degree-(s-1) interpolant, exact re-expansion) to 1e-8."""
+    p = make()
+    out, st = _linear(p, route=route, node_rule=1)
+    ref = _oracle_linear(p, node_rule=1)
+    assert rel(out, ref) < 1e-8, st
+
+
+def test_f3_pulse_reaches_exact_source_solution():
+    """The f1 pulse problem sampled at 32 Chebyshev nodes per subinterval: the CUDA path equals the
+    closed-form semi-discrete solution with the EXACT source to 1e-9 (uniform nodes + cubic spline
+    stop at the 4e-5 interpolation floor), and the oracle to 1e-8."""
+    from tests.closed_forms import pulse_semidiscrete
+    p = synth.pulse_ade(P=4, s=32, tol=1e-8, node_rule=1)
+    out, st = _linear(p, node_rule=1)
+    x = synth.grid_x(p.n, p.bc)
+    Ti = (np.arange(p.P) + 1) * p.T / p.P
+    ref = np.stack([pulse_semidiscrete(x, ti, p.nu[0], p.a[0], p.n) for ti in Ti])
+    assert rel(out[0], ref) < 1e-9, st
+    out0, _ = _linear(synth.pulse_ade(P=4, s=32, tol=1e-8), k_max=256)
+    assert rel(out0[0], ref) > 1e-6          # the cubic-spline floor the variant removes
+    assert rel(out, _oracle_linear(p, node_rule=1)) < 1e-8
+
+
+def test_f3_sample_times_and_burgers_rejected():
+    c = pexp.Context(64, "periodic", 1e-2, 0.0, s=9, node_rule=1)
+    np.testing.assert_allclose(c.sample_times(0.9, 3).numpy(), synth.node_times(0.9, 3, 9, node_rule=1), atol=1e-15)
+    with pytest.raises(pexp.PexpError):
+        c.solve_burgers(t(np.ones(64)), 1e-2, 0.1, 2, 1e-8, 3)
