@@ -287,10 +287,10 @@ def main():
     out_h = torch.empty(out.shape, dtype=torch.float64).pin_memory()
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
 
-    def step():
+    def step(records=False):
         if linear:
-            return ctx.solve_linear(u0, src, p.T, p.P, p.tol, out=out)[1]
-        return ctx.solve_burgers(u0, p.nu, p.T, p.P, p.tol, p.max_wr_iters, out=out)[1]
+            return ctx.solve_linear(u0, src, p.T, p.P, p.tol, out=out, records=records)[1]
+        return ctx.solve_burgers(u0, p.nu, p.T, p.P, p.tol, p.max_wr_iters, out=out, records=records)[1]
 
     st = None
     for _ in range(args.warmup):
@@ -322,12 +322,19 @@ def main():
     pexp.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    step()
+    stp = step(records=True)
     e1.record()
     e1.synchronize()
     prof_step_ms = e0.elapsed_time(e1)
     prof = pexp.profile_read()
     pexp.profile_enable(False)
+    if not linear and prof["hom_scan"]["ms"]:
+        # the persistent scan kernel: algorithmic bytes of its single-vector SaI Arnoldi per subinterval by
+        # SURVEY §8(d).4's figure for homogeneous legs, 8n(2K^2 + 10K) (CGS2 reads the basis four times per
+        # step, solve read/write), K = the converged dimension recorded per subinterval (pexp_stats.kscan_j)
+        ks = np.array([k for it in stp["kscan_j"] for k in it if k > 0], dtype=np.float64)
+        prof["hom_scan"]["bytes"] = float(8.0 * p.n * np.sum(2.0 * ks * ks + 10.0 * ks))
+        prof["hom_scan"]["flops"] = float(np.sum(8.0 * p.n * ks * ks))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -378,9 +385,27 @@ def main():
         if tj and tj.get("workload") == args.config:
             roof["traffic"] = tj["dram_bytes_per_launch"]
             roof["traffic_source"] = tj["source"]
+    if dom == "hom_scan":
+        roof["note"] = ("sequential chain (255 subintervals x ~37 dependent Arnoldi steps per WR iteration): latency-bound; "
+                        "its basis rows live in shared memory, so DRAM traffic is far below the algorithmic bytes")
     roof["share_of_step"] = d["ms"] / max(1e-9, prof_step_ms)
     roof["launches_per_step"] = d["launches"]
     roof["ms_per_step"] = d["ms"]
+    def hbm_roof(name):
+        v = prof[name]
+        if not v["ms"]:
+            return None
+        a = v["bytes"] / (v["ms"] / 1e3) / 1e9
+        r = {"kernel": name, "bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s", "frac": a / hbm_peak,
+             "TFLOP_per_s": v["flops"] / (v["ms"] / 1e3) / 1e12, "fp64_tensor_frac": v["flops"] / (v["ms"] / 1e3) / 1e12 / fp64["tflops"],
+             "share_of_step": v["ms"] / max(1e-9, prof_step_ms), "launches_per_step": v["launches"]}
+        if os.path.exists(tf):
+            tj = json.load(open(tf)).get(name)
+            if tj and tj.get("workload") == args.config:
+                r["traffic"] = tj["dram_bytes_per_launch"]
+                r["traffic_source"] = tj["source"]
+        return r
+    roof_stream = [r for r in (hbm_roof("stream_proj"), hbm_roof("stream_update")) if r]
     classes = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"],
                    "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None,
                    "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None}
@@ -397,7 +422,7 @@ def main():
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "flushed (256 MiB write) before every timed step",
                        "max_m": st["max_m"], "max_k": st["max_k"], "wr_iters": st["wr_iters"]},
-            "roofline": roof, "kernel_classes": classes,
+            "roofline": roof, "roofline_ebk_streaming": roof_stream, "kernel_classes": classes,
             "gpu_launches": int(launches / args.steps),
             "host_syncs_per_step": syncs / args.steps,
             "profiled_step_ms": prof_step_ms,

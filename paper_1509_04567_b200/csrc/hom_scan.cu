@@ -45,6 +45,7 @@ constexpr int XG_DOUBLES = 148 * 8;  // gathered rows of exchange 1
 constexpr int SCAN_SMEM_DOUBLES = 26400;  // 206 KB dynamic (+ ~19 KB static of the dense helpers) of the 227 KB per CTA
 constexpr int VS_DOUBLES = SCAN_SMEM_DOUBLES - 2 * (KSMALL_MAX + 8) - NT * RPT_MAX - XG_DOUBLES;
 static_assert(XG_DOUBLES + VS_DOUBLES >= HS_PSM, "checker scratch must fit");
+static_assert(SCAN_SMEM_DOUBLES >= 6 * 64 * 64 + 4 * 64, "small-matrix checker buffers must fit");
 
 enum { F_STEPS = 0, F_RESULT = 1, F_DECISION = 2, F_KMAX = 3, F_ERR = 4, F_BREAK = 5,
        F_NSTEPS = 8, F_NCHECK = 9, F_CHKCYC = 10,  // diagnostics: Arnoldi steps, checks, checker kilo-cycles
@@ -315,6 +316,223 @@ struct ScanArgs {
   int* flags;                   // [F_NFLAGS]
 };
 
+// ---------------------------------------------------------------- small dense kit (checker CTA)
+// K <= 64 (the usual scan space): the whole projected check runs out of shared memory -- six 64 x 64
+// column-major buffers (ld SLD), zero-padded so the products need no bounds checks.
+constexpr int SLD = 64;
+constexpr int SMAT = SLD * SLD;
+
+// C = A * B on the zero-padded 64 x 64 buffers, contraction over the first Np indices (Np = N rounded up
+// to 4; C must not alias A or B).  Thread t owns rows (t % 16) + 16 ii and columns (t / 16) + 16 jj
+// (conflict-free shared-memory reads: 16 consecutive doubles of A, broadcast of B).
+__device__ inline void sm_gemm(int Np, const double* A, const double* B, double* C) {
+  const int ti = threadIdx.x & 15, tj = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+  for (int k = 0; k < Np; ++k) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) av[ii] = A[ti + 16 * ii + k * SLD];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) bv[jj] = B[k + (tj + 16 * jj) * SLD];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(av[ii], bv[jj], acc[ii][jj]);
+  }
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) C[ti + 16 * ii + (tj + 16 * jj) * SLD] = acc[ii][jj];
+  __syncthreads();
+}
+
+// Gauss-Jordan with partial (row) pivoting: M X = B solved in place (M destroyed, B <- X), N x N with
+// nb right-hand columns.  col: N doubles of scratch.  Returns false on a zero pivot.
+__device__ inline bool sm_gauss_jordan(int N, double* M, double* B, int nb, double* col, int* s_p) {
+  for (int k = 0; k < N; ++k) {
+    if (threadIdx.x < 32) {  // pivot row: largest |M[i][k]|, i >= k (first on ties)
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + threadIdx.x; i < N; i += 32) {
+        const double v = fabs(M[i + k * SLD]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (threadIdx.x == 0) *s_p = best > 0.0 ? bi : -1;
+    }
+    __syncthreads();
+    const int pr = *s_p;
+    if (pr < 0) return false;
+    // swap rows k <-> pr, scale row k by 1 / pivot (columns j >= k of M, all of B)
+    const double pinv = 1.0 / M[pr + k * SLD];
+    __syncthreads();
+    for (int j = threadIdx.x; j < N + nb; j += NT) {
+      double* X = j < N ? M + j * SLD : B + (j - N) * SLD;
+      if (j < N && j < k) continue;
+      const double a = X[pr], b = X[k];
+      X[pr] = b;
+      X[k] = a * pinv;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += NT) col[i] = i == k ? 0.0 : M[i + k * SLD];
+    __syncthreads();
+    // eliminate column k from every other row
+    for (int idx = threadIdx.x; idx < N * (N - k + nb); idx += NT) {
+      const int i = idx % N, jj = idx / N;
+      const int j = k + jj;  // k..N-1: M columns; beyond: B columns
+      double* X = j < N ? M + j * SLD : B + (j - N) * SLD;
+      if (i != k) X[i] = fma(-col[i], X[k], X[i]);
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// The projected check for K <= 64 entirely in shared memory (buf: 6 * SMAT + 4 * SLD doubles):
+// H^{-1}, A_hat = (I - H^{-1}) / gamma, F = exp(h A_hat) by Pade-13 scaling and squaring (Higham 2005),
+// the chain z_q = F z_{q-1} in one warp, the residuals at every node.  Same outputs as hom_check.
+__device__ static double hom_check_small(const ScanArgs& a, double* Zc, int K, double gam, double beta, double* buf,
+                                         double* red, int* s_p) {
+  const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                        1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                        670442572800.0,      33522128640.0,       1323241920.0,
+                        40840800.0,          960960.0,            16380.0,
+                        182.0,               1.0};
+  const double theta13 = 5.371920351148152;
+  const int ldh = a.kcap + 1;
+  const int Np = (K + 3) & ~3;
+  double *A1 = buf, *A2 = buf + SMAT, *A4 = buf + 2 * SMAT, *A6 = buf + 3 * SMAT, *T1 = buf + 4 * SMAT,
+         *T2 = buf + 5 * SMAT;
+  double* col = buf + 6 * SMAT;   // [SLD]
+  double* hrow = col + SLD;       // last row of H^{-1}
+  double* nrmc = hrow + SLD;      // column sums
+  for (int t = threadIdx.x; t < 6 * SMAT; t += NT) buf[t] = 0.0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int i = t % K, j = t / K;
+    T1[i + j * SLD] = __ldcg(a.H + i + size_t(j) * ldh);
+    if (i == j) T2[i + j * SLD] = 1.0;
+  }
+  __syncthreads();
+  const double htail = __ldcg(a.H + K + size_t(K - 1) * ldh);
+  if (!sm_gauss_jordan(K, T1, T2, K, col, s_p)) return INFINITY;  // T2 = H^{-1}
+  for (int t = threadIdx.x; t < K; t += NT) hrow[t] = T2[(K - 1) + t * SLD];
+  // A1 = h (I - H^{-1}) / gamma, its 1-norm, scaling
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int i = t % K, j = t / K;
+    A1[i + j * SLD] = a.h * ((i == j ? 1.0 : 0.0) - T2[i + j * SLD]) / gam;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < K; j += NT) {
+    double sum = 0.0;
+    for (int i = 0; i < K; ++i) sum += fabs(A1[i + j * SLD]);
+    nrmc[j] = sum;
+  }
+  __syncthreads();
+  double nrm = 0.0;
+  for (int j = 0; j < K; ++j) nrm = fmax(nrm, nrmc[j]);
+  if (!isfinite(nrm)) return INFINITY;
+  int sq = 0;
+  if (nrm > theta13) sq = max(0, (int)ceil(log2(nrm / theta13)));
+  if (sq > 0) {
+    const double sc = ldexp(1.0, -sq);
+    for (int t = threadIdx.x; t < K * K; t += NT) A1[(t % K) + (t / K) * SLD] *= sc;
+    __syncthreads();
+  }
+  sm_gemm(Np, A1, A1, A2);
+  sm_gemm(Np, A2, A2, A4);
+  sm_gemm(Np, A4, A2, A6);
+  // U = A1 [A6 (b13 A6 + b11 A4 + b9 A2) + b7 A6 + b5 A4 + b3 A2 + b1 I]
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int o = (t % K) + (t / K) * SLD;
+    T1[o] = b[13] * A6[o] + b[11] * A4[o] + b[9] * A2[o];
+  }
+  __syncthreads();
+  sm_gemm(Np, A6, T1, T2);
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int i = t % K, j = t / K, o = i + j * SLD;
+    T2[o] += b[7] * A6[o] + b[5] * A4[o] + b[3] * A2[o] + (i == j ? b[1] : 0.0);
+  }
+  __syncthreads();
+  sm_gemm(Np, A1, T2, T1);  // T1 = U
+  // V = A6 (b12 A6 + b10 A4 + b8 A2) + b6 A6 + b4 A4 + b2 A2 + b0 I   (into A1: no longer needed)
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int o = (t % K) + (t / K) * SLD;
+    T2[o] = b[12] * A6[o] + b[10] * A4[o] + b[8] * A2[o];
+  }
+  __syncthreads();
+  sm_gemm(Np, A6, T2, A1);
+  for (int t = threadIdx.x; t < K * K; t += NT) {
+    const int i = t % K, j = t / K, o = i + j * SLD;
+    const double v = A1[o] + b[6] * A6[o] + b[4] * A4[o] + b[2] * A2[o] + (i == j ? b[0] : 0.0);
+    const double u = T1[o];
+    T2[o] = v - u;   // (V - U) R = (V + U)
+    T1[o] = v + u;
+  }
+  __syncthreads();
+  if (!sm_gauss_jordan(K, T2, T1, K, col, s_p)) return INFINITY;  // T1 = R
+  double *cur = T1, *nxt = T2;
+  for (int t = threadIdx.x; t < SMAT; t += NT) nxt[t] = 0.0;  // T2 held the eliminated system
+  __syncthreads();
+  for (int q = 0; q < sq; ++q) {
+    sm_gemm(Np, cur, cur, nxt);
+    double* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  // chain z_q = F z_{q-1} in ONE warp (lane l owns rows l and l + 32; z through shuffles)
+  const double* F = cur;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int r0 = lane, r1 = lane + 32;
+    double z0 = lane == 0 ? beta : 0.0, z1 = 0.0;
+    if (r0 < K) Zc[r0] = z0;
+    if (r1 < K) Zc[r1] = 0.0;
+    for (int q = 1; q < a.s; ++q) {
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+      int j = 0;
+      for (; j + 1 < K; j += 2) {
+        const double zj = __shfl_sync(0xffffffffu, j < 32 ? z0 : z1, j & 31);
+        const double zk = __shfl_sync(0xffffffffu, j + 1 < 32 ? z0 : z1, (j + 1) & 31);
+        a0 = fma(F[r0 + j * SLD], zj, a0);
+        a1 = fma(F[r1 + j * SLD], zj, a1);
+        b0 = fma(F[r0 + (j + 1) * SLD], zk, b0);
+        b1 = fma(F[r1 + (j + 1) * SLD], zk, b1);
+      }
+      if (j < K) {
+        const double zj = __shfl_sync(0xffffffffu, j < 32 ? z0 : z1, j & 31);
+        a0 = fma(F[r0 + j * SLD], zj, a0);
+        a1 = fma(F[r1 + j * SLD], zj, a1);
+      }
+      z0 = r0 < K ? a0 + b0 : 0.0;
+      z1 = r1 < K ? a1 + b1 : 0.0;
+      if (r0 < K) Zc[size_t(q) * a.kcap + r0] = z0;
+      if (r1 < K) Zc[size_t(q) * a.kcap + r1] = z1;
+    }
+  }
+  __threadfence_block();
+  __syncthreads();
+  // residuals |h_{K+1,K} (H^{-1} z_q)_K| / gamma at every node (one warp per node)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double maxres = 0.0;
+  for (int q = 1 + w; q < a.s; q += NT / 32) {
+    double xp = 0.0;
+    for (int r = lane; r < K; r += 32) xp = fma(hrow[r], Zc[size_t(q) * a.kcap + r], xp);
+    xp = warp_sum(xp);
+    maxres = fmax(maxres, fabs(htail * xp) / gam);
+  }
+  maxres = block_max(maxres, red);
+  __syncthreads();
+  return maxres;
+}
+
 // Projected check on the checker CTA: returns max_r residual; writes Zc[r][0..K).
 __device__ static double hom_check(const ScanArgs& a, double* Zc, int K, double gam, double beta, double* z,
                                    double* zn, double* red, double* psm) {
@@ -352,6 +570,40 @@ __device__ static double hom_check(const ScanArgs& a, double* Zc, int K, double 
   for (int r = threadIdx.x; r < K; r += NT) Zc[r] = z[r];
   const int ng = max(1, min(8, NT / max(K, 1)));  // thread groups per row
   const int jper = (K + ng - 1) / ng;
+  if (fs && K <= 64) {
+    // small spaces (the usual case): the whole chain in ONE warp, no block barriers -- lane l owns rows
+    // l and l + 32 of the state, the products read F from shared memory and z through shuffles
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int r0 = lane, r1 = lane + 32;
+      double z0 = lane == 0 ? beta : 0.0, z1 = 0.0;
+      const double* F0 = F + (r0 < K ? r0 : 0);
+      const double* F1 = F + (r1 < K ? r1 : 0);
+      for (int q = 1; q < a.s; ++q) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        int j = 0;
+        for (; j + 1 < K; j += 2) {
+          const double zj = __shfl_sync(0xffffffffu, j < 32 ? z0 : z1, j & 31);
+          const double zk = __shfl_sync(0xffffffffu, j + 1 < 32 ? z0 : z1, (j + 1) & 31);
+          a0 = fma(F0[size_t(j) * K], zj, a0);
+          a1 = fma(F1[size_t(j) * K], zj, a1);
+          b0 = fma(F0[size_t(j + 1) * K], zk, b0);
+          b1 = fma(F1[size_t(j + 1) * K], zk, b1);
+        }
+        if (j < K) {
+          const double zj = __shfl_sync(0xffffffffu, j < 32 ? z0 : z1, j & 31);
+          a0 = fma(F0[size_t(j) * K], zj, a0);
+          a1 = fma(F1[size_t(j) * K], zj, a1);
+        }
+        z0 = r0 < K ? a0 + b0 : 0.0;
+        z1 = r1 < K ? a1 + b1 : 0.0;
+        if (r0 < K) Zc[size_t(q) * a.kcap + r0] = z0;
+        if (r1 < K) Zc[size_t(q) * a.kcap + r1] = z1;
+      }
+    }
+    __threadfence_block();
+    __syncthreads();
+  } else
   for (int q = 1; q < a.s; ++q) {
     const int r = threadIdx.x % K, gq = threadIdx.x / K;
     if (threadIdx.x < ng * K) {
@@ -391,7 +643,7 @@ __device__ static double hom_check(const ScanArgs& a, double* Zc, int K, double 
 __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
   __shared__ double red[32];
   __shared__ Aff wsm[NT / 32 + 1];
-  __shared__ int s_dec;
+  __shared__ int s_dec, s_dec2;
   extern __shared__ double dyn[];  // hv, hv2: KSMALL_MAX + 8 each; xs: NT * RPT_MAX; LU scratch HS_PSM
   double* hv = dyn;
   double* hv2 = dyn + KSMALL_MAX + 8;
@@ -454,7 +706,7 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
         double* zn = hv2;
         // first check just below the previous subinterval's converged dimension (the operators of
         // neighbouring subintervals are close), then extrapolate the residual decay
-        int target = min(max(4, kconv_prev - 3), a.kcap - 1), Kprev = -1;
+        int target = min(max(4, kconv_prev - 2), a.kcap - 1), Kprev = -1;
         double qprev = -1.0;
         while (true) {
           if (threadIdx.x == 0) {
@@ -473,7 +725,8 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
           const int K = s_dec;
           const bool brk = vload(fl + F_BREAK) == K;
           const long long tc0 = clock64();
-          const double res = hom_check(a, Zi, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
+          const double res = K <= SLD ? hom_check_small(a, Zi, K, gam, beta, dyn, red, &s_dec2)
+                                      : hom_check(a, Zi, K, gam, beta, z, zn, red, xs + NT * RPT_MAX);
           if (threadIdx.x == 0) {
             fl[F_NCHECK] += 1;
             fl[F_CHKCYC] += int((clock64() - tc0) >> 10);
@@ -519,8 +772,8 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
         f_w[q] = ok && a.periodic ? a.fw[fo + g] : 0.0;
         vr[q] = uh[q] * inv;
         if (ok) {
-          Vi[g] = vr[q];
           if (0 < a.vcap) Vs[threadIdx.x * rpt + q] = vr[q];
+          else Vi[g] = vr[q];
         }
       }
       __syncthreads();
@@ -704,8 +957,10 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
               if (j < ks) v0 = fma(-hv2[j], Vs[size_t(j) * a.segp + l], v0);
               for (j = ks; j < kk; ++j) v0 = fma(-hv2[j], Vi[size_t(j) * n + g], v0);
               vr[q] = (v0 + v1) * sc;
-              Vi[size_t(kk) * n + g] = vr[q];
+              // columns resident in shared memory reach the global archive once, after the loop (no
+              // global stores in flight when the exchange's fence runs)
               if (kk < a.vcap) Vs[size_t(kk) * a.segp + l] = vr[q];
+              else Vi[size_t(kk) * n + g] = vr[q];
             }
           }
           if (c == 0) {
@@ -725,6 +980,18 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
       if (Kc < 0) {
         if (c == 0 && threadIdx.x == 0) atomicExch(fl + F_ERR, 1);
         Kc = 0;
+      }
+      // the shared-memory columns of this subinterval's basis -> global (archive for k_scan_output /
+      // the in-scan waveform update below); every thread stores the rows it reads back later
+      {
+        const int nc = min(max(Kc, 0), a.vcap);
+        _Pragma("unroll") for (int q = 0; q < RPT_MAX; ++q) if (q < rpt) {
+          const int g = row0 + threadIdx.x * rpt + q;
+          if (g < rend) {
+            const int l = threadIdx.x * rpt + q;
+            for (int j = 0; j < nc; ++j) Vi[size_t(j) * n + g] = Vs[size_t(j) * a.segp + l];
+          }
+        }
       }
       // archived: only the end value u_hat(T_i) = Y(T_i) + V z(T_i) here (the waveform at all nodes is
       // written by k_scan_output after the scan); otherwise the full waveform update in place

@@ -394,8 +394,12 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
       launch_small_problem(st, a, B.nslots, Koff);
     PEXP_CUDA_TRY(cudaMemsetAsync(B.count, 0, sizeof(int), st));
     launch_update_active(st, E, B.conv, B.active, B.count, B.krec, Koff + K);
+    // one synchronisation per check: the active count and the residual ratios that place the next check
     int h_count = 0;
     PEXP_CUDA_TRY(cudaMemcpyAsync(&h_count, B.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaMemcpyAsync(hres.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaMemcpyAsync(hcrit.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PEXP_CUDA_TRY(cudaMemcpyAsync(hact.data(), B.active, E * sizeof(int), cudaMemcpyDeviceToHost, st));
     host_sync(st);
     remaining = h_count;
     g_cfg.active_hint = remaining;
@@ -407,10 +411,6 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
     // q = res/crit decays roughly geometrically in K; extrapolate from the last two checks
     predicted_next = -1;
     if (remaining > 0) {
-      PEXP_CUDA_TRY(cudaMemcpyAsync(hres.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
-      PEXP_CUDA_TRY(cudaMemcpyAsync(hcrit.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
-      PEXP_CUDA_TRY(cudaMemcpyAsync(hact.data(), B.active, E * sizeof(int), cudaMemcpyDeviceToHost, st));
-      host_sync(st);
       std::vector<double> preds;
       for (int e = 0; e < E; ++e) {
         if (!hact[e] || !(kind == 2 || hcrit[e] > 0)) continue;
@@ -542,15 +542,11 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   }
   info.unconverged = remaining;
   g_cfg.active_hint = -1;
-  {  // worst residual / target over the evaluations at their last check (diagnostic)
-    std::vector<double> r(E), c(E);
-    PEXP_CUDA_TRY(cudaMemcpyAsync(r.data(), B.res, E * sizeof(double), cudaMemcpyDeviceToHost, st));
-    PEXP_CUDA_TRY(cudaMemcpyAsync(c.data(), B.crit, E * sizeof(double), cudaMemcpyDeviceToHost, st));
-    host_sync(st);
-    for (int e = 0; e < E; ++e)
-      if (last_check >= 0 && (kind == 2 || c[e] > 0))
-        info.worst_res_ratio = std::max(info.worst_res_ratio, kind == 2 ? r[e] : r[e] / c[e]);
-  }
+  // worst residual / target over the evaluations at their last check (diagnostic; the host copies of
+  // the last check)
+  for (int e = 0; e < E; ++e)
+    if (last_check >= 0 && (kind == 2 || hcrit[e] > 0))
+      info.worst_res_ratio = std::max(info.worst_res_ratio, kind == 2 ? hres[e] : hres[e] / hcrit[e]);
   return info;
 }
 
@@ -558,6 +554,7 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
 struct SvdBufs {
   double *U, *R, *Gs, *lam, *Msel, *sigma1, *Cb, *Qs, *Cs, *sig, *Cfin, *Rinv, *Kinv, *Dmat;
   int *off, *me, *fill;
+  bool pt_ready = false;  // the p(t) matrix (Kinv / Dmat) is on the device for this solve
 };
 
 static void alloc_svd(Arena& ar, SvdBufs& S, int E, int n, int s) {
@@ -732,14 +729,13 @@ static int svd_stage(cudaStream_t st, SvdBufs& S, EbkBufs* B, int E, int n, int 
     }
   }
   if (g_cfg.node_rule == 1) {
-    std::vector<double> Dm = cheb_taylor_matrix(s, g_cfg.nq, h * (s - 1));
-    h2d(st, S.Dmat, Dm);
+    if (!S.pt_ready) h2d(st, S.Dmat, cheb_taylor_matrix(s, g_cfg.nq, h * (s - 1)));
     launch_poly_coef(st, E, s, mb, g_cfg.nq, S.Dmat, S.Cfin, eta, B->coef, B->crit);
   } else {
-    std::vector<double> Ki = notaknot_inverse(s);
-    h2d(st, S.Kinv, Ki);
+    if (!S.pt_ready) h2d(st, S.Kinv, notaknot_inverse(s));  // once per solve (depends on s only)
     launch_spline(st, E, s, mb, S.Kinv, S.Cfin, h, eta, B->coef, B->crit);
   }
+  S.pt_ready = true;
   k_active_from_m<<<cdiv(E, 256), 256, 0, st>>>(E, S.me, B->active);
   count_launch();
   PEXP_LAUNCH_CHECK();
