@@ -1064,34 +1064,45 @@ __global__ void __launch_bounds__(NT, 1) k_hom_scan(ScanArgs a) {
 //   u_{k+1}(t_{i,r}) = u0 + Y_i(t_r) + V_i z_i(t_r),  delta = max |u_{k+1} - u_k|    (Eq.(updateSolution))
 // One thread per row; the node coefficients z_i(t_r) staged in shared memory 32 columns at a time.
 constexpr int OUT_SMAX = 64;
-__global__ void __launch_bounds__(NT) k_scan_output(int s, int n, int kcap, const double* u0, const double* Y,
-                                                    const double* Uold, double* Unew, const double* Vpool,
-                                                    const int* koff, const int* kc, const double* Zc, double* delta) {
+constexpr int OUT_SG = 32;  // nodes per CTA (blockIdx.z selects the node group: 64 registers of accumulators)
+__global__ void __launch_bounds__(NT, 2) k_scan_output(int s, int n, int kcap, const double* u0, const double* Y,
+                                                       const double* Uold, double* Unew, const double* Vpool,
+                                                       const int* koff, const int* kc, const double* Zc,
+                                                       double* delta) {
   const int i = blockIdx.y;
   const int K = kc[i];
   if (K < 0) return;  // this subinterval's waveform was written inside the scan
-  __shared__ double Zs[OUT_SMAX][33];
+  const int rb = blockIdx.z * OUT_SG;       // first node of this CTA's group
+  const int ns = min(OUT_SG, s - rb);
+  if (ns <= 0) return;
+  __shared__ double Zs[OUT_SG][33];
   __shared__ double red[32];
   const int g = blockIdx.x * NT + threadIdx.x;
-  double acc[OUT_SMAX];
+  double acc[OUT_SG];
 #pragma unroll
-  for (int r = 0; r < OUT_SMAX; ++r) acc[r] = 0.0;
+  for (int r = 0; r < OUT_SG; ++r) acc[r] = 0.0;
   const double* V = Vpool + size_t(koff[i]) * n;
   const double* Z = Zc + size_t(i) * s * kcap;
   for (int j0 = 0; j0 < K; j0 += 32) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < s * 32; idx += NT) {
+    for (int idx = threadIdx.x; idx < OUT_SG * 32; idx += NT) {
       const int r = idx / 32, jj = idx % 32;
-      Zs[r][jj] = j0 + jj < K ? __ldcg(Z + size_t(r) * kcap + j0 + jj) : 0.0;
+      Zs[r][jj] = (r < ns && j0 + jj < K) ? __ldcg(Z + size_t(rb + r) * kcap + j0 + jj) : 0.0;
     }
     __syncthreads();
     if (g < n) {
       const int jn = min(32, K - j0);
-      for (int jj = 0; jj < jn; ++jj) {
-        const double v = V[size_t(j0 + jj) * n + g];
+      for (int jj = 0; jj < jn; jj += 4) {  // four basis columns per round: independent loads in flight
+        double v[4];
 #pragma unroll
-        for (int r = 0; r < OUT_SMAX; ++r)
-          if (r < s) acc[r] = fma(v, Zs[r][jj], acc[r]);
+        for (int u = 0; u < 4; ++u) v[u] = jj + u < jn ? V[size_t(j0 + jj + u) * n + g] : 0.0;
+#pragma unroll
+        for (int r = 0; r < OUT_SG; ++r) {
+          double a = acc[r];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a = fma(v[u], Zs[r][jj + u], a);   // Zs is zero beyond K
+          acc[r] = a;
+        }
       }
     }
   }
@@ -1099,14 +1110,24 @@ __global__ void __launch_bounds__(NT) k_scan_output(int s, int n, int kcap, cons
   if (g < n) {
     const double ug = u0[g];
 #pragma unroll
-    for (int r = 0; r < OUT_SMAX; ++r)
-      if (r < s) {
-        const size_t k = (size_t(i) * s + r) * n + g;
-        const double un = ug + Y[k] + acc[r];
-        mx = fmax(mx, fabs(un - Uold[k]));
-        if (!isfinite(un)) mx = INFINITY;
-        Unew[k] = un;
+    for (int r0 = 0; r0 < OUT_SG; r0 += 8) {  // eight nodes per round: 16 independent loads in flight
+      double yv[8], uo[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const size_t k = (size_t(i) * s + rb + r0 + u) * n + g;
+        yv[u] = r0 + u < ns ? Y[k] : 0.0;
+        uo[u] = r0 + u < ns ? Uold[k] : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (r0 + u < ns) {
+          const size_t k = (size_t(i) * s + rb + r0 + u) * n + g;
+          const double un = ug + yv[u] + acc[r0 + u];
+          mx = fmax(mx, fabs(un - uo[u]));
+          if (!isfinite(un)) mx = INFINITY;
+          Unew[k] = un;
+        }
+    }
   }
   mx = block_max(mx, red);
   if (threadIdx.x == 0) atomic_max_nonneg(delta, mx);
@@ -1179,7 +1200,7 @@ int launch_hom_scan(cudaStream_t st, const Factors& F, const double* gam, int P,
   {
     // algorithmic: Y, u_k read, u_{k+1} written at every node; the archived bases read once (~32 columns)
     ProfScope ps(PC_SCANOUT, st, double(P) * s * n * 24.0 + double(P) * 32.0 * n * 8.0, 2.0 * double(P) * s * n * 32.0);
-    k_scan_output<<<dim3(cdiv(n, NT), P), NT, 0, st>>>(s, n, kcap, u0, Y, Uold, Unew, a.Vpool, a.koff, a.kc, a.Zc,
+    k_scan_output<<<dim3(cdiv(n, NT), P, cdiv(s, OUT_SG)), NT, 0, st>>>(s, n, kcap, u0, Y, Uold, Unew, a.Vpool, a.koff, a.kc, a.Zc,
                                                        delta);
   }
   count_launch();

@@ -22,7 +22,8 @@ namespace pexp {
 constexpr int MAXS = 64;
 namespace cg = cooperative_groups;
 // k_small_problem dynamic shared memory: replicated state 2*KSMALL_MAX, row partials CH_PSUM,
-// own rows KSMALL_MAX, residual ring 2*MAXS, then the CTA's slice of F (FS_CAP doubles)
+// own rows KSMALL_MAX, residual partials of every piece RING_N*MAXS, then the CTA's slice of F
+// (FS_CAP doubles)
 constexpr int CH_PSUM = KSMALL_MAX + 32;
 #if PEXP_GEMM_TM >= 128
 constexpr size_t SP_DYN = 180 * 1024;

@@ -169,7 +169,8 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
         int gram, double* part, const int* active) {
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;
-  double* red = ring + SNST * SSTAGE;  // [SNW][8 * MB] warp tiles
+  double* red = ring + SNST * SSTAGE;  // [2][SNW][8 * MB] warp tiles (double-buffered over the stages)
+  int rbuf = 0;
   __shared__ __align__(8) unsigned long long full[SNST], empty[SNST];
   ring_setup(ring, full, empty);
   const int nitems = E * nch;
@@ -223,8 +224,12 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[rp.slot]);
       rp.advance();
-      // warp tiles -> shared (D[i = lane>>2][jcol = 8j + 2(lane&3) + h]); sum in warp order
-      double* rw = red + warp * (8 * MB);
+      // warp tiles -> shared (D[i = lane>>2][jcol = 8j + 2(lane&3) + h]); sum in warp order.  The tile
+      // buffer is double-buffered over the stages, so ONE consumer barrier per stage suffices (the
+      // barrier of stage g+1 orders the reads of buffer b before the writes of stage g+2 into it)
+      double* rb = red + rbuf * (SNW * 8 * MB);
+      rbuf ^= 1;
+      double* rw = rb + warp * (8 * MB);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3)] = acc[j][0];
@@ -236,11 +241,11 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
         const int i = idx % nc, b = idx / nc;
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < SNW; ++q) s += red[q * (8 * MB) + i * MB + b];
+        for (int q = 0; q < SNW; ++q) s += rb[q * (8 * MB) + i * MB + b];
         P[(g + i) + size_t(b) * pw] = s;
       }
-      consumer_sync();
     }
+    consumer_sync();  // the Gram tiles below reuse buffer 0
     if (gram) {  // G = Y^T Y over the chunk: A fragment of tile i = bf[q][i] (same layout)
 #pragma unroll
       for (int i = 0; i < NJ; ++i) {
@@ -416,7 +421,7 @@ bool stream_ok(int n, int ny) { return (n % 2) == 0 && ny >= 1 && ny <= 32 && n 
 
 static int stream_grid(int items) { return std::max(1, std::min(items, 148)); }
 
-static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + size_t(SNW) * 8 * MB); }
+static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + 2 * size_t(SNW) * 8 * MB); }
 static size_t supdate_smem() { return sizeof(double) * size_t(SNST) * SSTAGE; }
 
 // partial doubles of E evaluations when pw rows (nx, plus ny if the Gram is fused) x ny are reduced
