@@ -169,7 +169,7 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
         int gram, double* part, const int* active) {
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;
-  double* red = ring + SNST * SSTAGE;  // [2][SNW][8 * MB] warp tiles (double-buffered over the stages)
+  double* red = ring + SNST * SSTAGE;  // [2][SNW][8][MB + 8] warp tiles (double-buffered over the stages)
   int rbuf = 0;
   __shared__ __align__(8) unsigned long long full[SNST], empty[SNST];
   ring_setup(ring, full, empty);
@@ -180,6 +180,7 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
     return;
   }
   constexpr int NJ = MB / 8;
+  constexpr int MBP = MB + 8;  // tile row stride: consecutive rows 64 B apart modulo 128 B (conflict-free)
   const int njt = (ny + 7) >> 3;
   const int pw = nx + (gram ? ny : 0);
   RingPos rp;
@@ -227,21 +228,21 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
       // warp tiles -> shared (D[i = lane>>2][jcol = 8j + 2(lane&3) + h]); sum in warp order.  The tile
       // buffer is double-buffered over the stages, so ONE consumer barrier per stage suffices (the
       // barrier of stage g+1 orders the reads of buffer b before the writes of stage g+2 into it)
-      double* rb = red + rbuf * (SNW * 8 * MB);
+      double* rb = red + rbuf * (SNW * 8 * MBP);
       rbuf ^= 1;
-      double* rw = rb + warp * (8 * MB);
+      double* rw = rb + warp * (8 * MBP);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
-        rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3)] = acc[j][0];
-        rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3) + 1] = acc[j][1];
+        rw[(lane >> 2) * MBP + 8 * j + 2 * (lane & 3)] = acc[j][0];
+        rw[(lane >> 2) * MBP + 8 * j + 2 * (lane & 3) + 1] = acc[j][1];
       }
       consumer_sync();
       const int nc = min(SCOLS, nx - g);
       for (int idx = threadIdx.x; idx < nc * ny; idx += SNW * 32) {
-        const int i = idx % nc, b = idx / nc;
+        const int b = idx % ny, i = idx / ny;   // consecutive threads -> consecutive tile columns
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < SNW; ++q) s += rb[q * (8 * MB) + i * MB + b];
+        for (int q = 0; q < SNW; ++q) s += rb[q * (8 * MBP) + i * MBP + b];
         P[(g + i) + size_t(b) * pw] = s;
       }
     }
@@ -258,19 +259,19 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
 #pragma unroll
           for (int j = 0; j < NJ; ++j)
             if (j < njt) dmma(acc[j][0], acc[j][1], bf[q][i], bf[q][j]);
-        double* rw = red + warp * (8 * MB);
+        double* rw = red + warp * (8 * MBP);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-          rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3)] = acc[j][0];
-          rw[(lane >> 2) * MB + 8 * j + 2 * (lane & 3) + 1] = acc[j][1];
+          rw[(lane >> 2) * MBP + 8 * j + 2 * (lane & 3)] = acc[j][0];
+          rw[(lane >> 2) * MBP + 8 * j + 2 * (lane & 3) + 1] = acc[j][1];
         }
         consumer_sync();
         const int nc = min(8, ny - 8 * i);
         for (int idx = threadIdx.x; idx < nc * ny; idx += SNW * 32) {
-          const int ii = idx % nc, b = idx / nc;
+          const int b = idx % ny, ii = idx / ny;
           double s = 0.0;
 #pragma unroll
-          for (int q = 0; q < SNW; ++q) s += red[q * (8 * MB) + ii * MB + b];
+          for (int q = 0; q < SNW; ++q) s += red[q * (8 * MBP) + ii * MBP + b];
           P[nx + 8 * i + ii + size_t(b) * pw] = s;
         }
         consumer_sync();
@@ -421,7 +422,7 @@ bool stream_ok(int n, int ny) { return (n % 2) == 0 && ny >= 1 && ny <= 32 && n 
 
 static int stream_grid(int items) { return std::max(1, std::min(items, 148)); }
 
-static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + 2 * size_t(SNW) * 8 * MB); }
+static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + 2 * size_t(SNW) * 8 * (MB + 8)); }
 static size_t supdate_smem() { return sizeof(double) * size_t(SNST) * SSTAGE; }
 
 // partial doubles of E evaluations when pw rows (nx, plus ny if the Gram is fused) x ny are reduced
