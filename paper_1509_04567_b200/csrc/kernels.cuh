@@ -18,6 +18,7 @@ struct CallCfg {
   int syncs = 0;           // host synchronisations performed by the current call
   int nq = 4;              // Taylor terms per polynomial piece of p(t): 4 (cubic spline) or 12 (node_rule 1)
   int node_rule = 0;       // pexp_options.node_rule
+  const int* kprev = nullptr;  // host: Krylov dimension every evaluation needed in the previous WR iteration
   int active_hint = -1;    // evaluations still active in the running EBK loop (-1: unknown);
                            // the profiler's algorithmic byte/flop counts use it
 };

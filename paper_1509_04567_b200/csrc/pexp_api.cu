@@ -327,7 +327,7 @@ struct Accum {
 // forced: coef and crit set; homogeneous: beta, crit, npieces set.
 static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops& O, bool periodic, int m,
                        int kind, double h, int npieces_const, int out_stride, int nout, int stop_rule,
-                       Accum acc = Accum{}, int restart_blocks = 0) {
+                       Accum acc = Accum{}, int restart_blocks = 0, int first_hint = 0) {
   RunInfo info;
   const int E = B.E, n = B.n, kcap = B.kcap;
   if (E == 0) return info;
@@ -343,6 +343,9 @@ static RunInfo ebk_run(cudaStream_t st, EbkBufs& B, const Factors& F, const Ops&
   // fused cluster step (arnoldi.cu) whenever the step's panels fit shared memory
   int steps = 0, last_check = -1;
   int next_check = std::max(4, 2 * m);
+  // WR iterations after the first: no evaluation of this run converged below first_hint columns last
+  // time, so the checks before ~0.8 first_hint are skipped (the operators change little between iterations)
+  if (first_hint > 0) next_check = std::max(next_check, std::min(int(0.8 * first_hint) / m * m, kcap - 2 * m));
   // deflation: a new column is dropped when BCGS leaves < defl (default 1e-10) of
   // ||(I - gamma A)^{-1} v|| (well above the shift-and-invert solve rounding (~1e-13..1e-12),
   // below the 1e-8 parity bar); pexp_options.defl_tol
@@ -953,6 +956,18 @@ static void init_once() {
   }
 }
 
+// Smallest Krylov dimension the evaluations idx[0..cnt) (or first..first+cnt) needed in the previous WR
+// iteration (g_cfg.kprev), 0 if unknown.
+static int kprev_min(const int* idx, int first, int cnt) {
+  if (!g_cfg.kprev) return 0;
+  int mn = 1 << 30;
+  for (int i = 0; i < cnt; ++i) {
+    const int k = g_cfg.kprev[idx ? idx[i] : first + i];
+    if (k > 0) mn = std::min(mn, k);
+  }
+  return mn == (1 << 30) ? 0 : mn;
+}
+
 // The forced EBK over E evaluations in chunks of B.E (eval_chunk): each chunk copies its
 // U_j from the SVD stage into basis block 0, runs the block Arnoldi, and writes its outputs
 // Y[e] (+)= V_e z_e at output o0 (restart accumulation, then the final cycle).
@@ -970,7 +985,7 @@ static RunInfo ebk_forced_chunked(cudaStream_t st, EbkBufs& B, const SvdBufs& S,
                                     cudaMemcpyDeviceToDevice, st));
     double* Yc = Y + size_t(c0) * ys_e;
     RunInfo r = ebk_run(st, Bc, F, O, periodic, mmax, 0, h, s - 1, out_stride, nout, stop_rule,
-                        Accum{Yc, ys_e, o0, no}, restart_blocks);
+                        Accum{Yc, ys_e, o0, no}, restart_blocks, kprev_min(nullptr, c0, ec));
     launch_combine(st, ec, n, Bc.V, Bc.vs_e, 0, std::max(r.max_k, 1), Bc.Z + size_t(o0) * Bc.kcap, Bc.zs_e, Bc.kcap,
                    Yc, ys_e, 0, no, 1.0, r.restarts ? 1.0 : 0.0, nullptr, Bc.kfin);
     tot.max_k = std::max(tot.max_k, r.max_k);
@@ -1046,7 +1061,7 @@ static RunInfo ebk_forced_bucketed(cudaStream_t st, EbkBufs& B, const SvdBufs& S
       // restart cycles keep the column count of the unbucketed run: restart_blocks steps of max m_j
       const int rb = restart_blocks > 0 ? cdiv(long(restart_blocks) * std::max(mmax, 1), wb) : restart_blocks;
       RunInfo r = ebk_run(st, Bc, F, O, periodic, wb, 0, h, s - 1, out_stride, nout, stop_rule,
-                          Accum{B.Ytmp, yts, o0, no}, rb);
+                          Accum{B.Ytmp, yts, o0, no}, rb, kprev_min(perm.data() + p0, 0, ec));
       launch_combine(st, ec, n, Bc.V, Bc.vs_e, 0, std::max(r.max_k, 1), Bc.Z + size_t(o0) * Bc.kcap, Bc.zs_e, Bc.kcap,
                      B.Ytmp, yts, 0, no, 1.0, r.restarts ? 1.0 : 0.0, nullptr, Bc.kfin);
       launch_bucket_scatter(st, ec, B.perm + p0, size_t(no) * n, B.Ytmp, yts, Y, ys_e, B.krec_c, B.krec);
@@ -1349,6 +1364,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
     int32_t* rec_ks = st_out ? st_out->kscan_j : nullptr;
     std::vector<double> dhist;
     double scan_diag[3] = {0.0, 0.0, 0.0};
+    std::vector<int> kprev(P, 0), kcur(P, 0);
     std::vector<std::unique_ptr<EventPair>> scan_ev;  // homogeneous scan + waveform update per iteration
     std::vector<int> iota(P);
     for (int j = 0; j < P; ++j) iota[j] = j;
@@ -1380,6 +1396,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       if (rec_g) PEXP_CUDA_TRY(cudaMemcpyAsync(rec_g + size_t(k) * P, L.B.gam, P * sizeof(double),
                                                cudaMemcpyDeviceToHost, st));
       launch_fill_i32(st, L.B.krec, E, 0);
+      g_cfg.kprev = k > 0 ? kprev.data() : nullptr;
       if (mmax > 0) {
         RunInfo ri = ebk_forced(st, L.B, L.S, L.F, L.O, true, E, mmax, me.data(), h, s, 1, s, 0, L.Y, (long long)s * n,
                                         o.stop_rule, o.restart_blocks);
@@ -1391,6 +1408,8 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       }
       if (rec_k) PEXP_CUDA_TRY(cudaMemcpyAsync(rec_k + size_t(k) * P, L.B.krec, P * sizeof(int),
                                                cudaMemcpyDeviceToHost, st));
+      // read back with the delta synchronisation below: the next iteration's check-schedule hint
+      PEXP_CUDA_TRY(cudaMemcpyAsync(kcur.data(), L.B.krec, P * sizeof(int), cudaMemcpyDeviceToHost, st));
       PEXP_CUDA_TRY(cudaMemsetAsync(L.delta, 0, sizeof(double), st));
       scan_ev.emplace_back(new EventPair);
       PEXP_CUDA_TRY(cudaEventRecord(scan_ev.back()->a, st));
@@ -1426,6 +1445,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       PEXP_CUDA_TRY(cudaMemcpyAsync(&delta, L.delta, sizeof(double), cudaMemcpyDeviceToHost, st));
       host_sync(st);
       std::swap(L.Uk, L.Un);
+      kprev = kcur;
       dhist.push_back(delta);
       ++iters;
       if (delta0 < 0) delta0 = delta;

@@ -280,6 +280,147 @@ k_sproj(int E, int n, int nch, const double* X, long long xs_e, int nx, const do
   }
 }
 
+// ---------------------------------------------------------------- wide blocks (ny > 8): k_sproj2
+// Same product and partial layout as k_sproj, with the work split so that the fp64 tensor pipe never
+// waits for a CTA-wide reduction: 4 NJ consumer warps, warp (tj, q) = (w / 4, w % 4) owns the 8-column
+// tile tj of Y and the row quarter q (128 rows) of the chunk (the four quarters of a tile sit on the four
+// SM sub-partitions, every sub-partition hosts one warp per tile).  Its Y rows are DMMA B fragments in 64
+// registers; per X stage it issues 32 DMMAs and the four quarter tiles are summed through shared memory
+// behind a 128-thread NAMED barrier of that tile group only -- the other tile groups keep the tensor
+// pipe busy meanwhile.  G = Y^T Y uses the Y stages themselves as A operands (they stay in the ring
+// until every tile pair is done), so a warp never needs another tile's fragments.
+constexpr int SNST2 = 6;  // ring stages (the Y stages of an item, up to 4, stay resident during the Gram)
+template <int NJ>
+__global__ void __launch_bounds__((4 * NJ + 1) * 32, 1)
+k_sproj2(int E, int n, int nch, const double* X, long long xs_e, int nx, const double* Y, long long ys_e, int ny,
+         int gram, double* part, const int* active) {
+  constexpr int NCW = 4 * NJ;
+  extern __shared__ __align__(16) double sm[];
+  double* ring = sm;
+  double* red = ring + SNST2 * SSTAGE;  // [2][NJ][4][64] quarter tiles (double-buffered over the stages)
+  __shared__ __align__(8) unsigned long long full[SNST2], empty[SNST2];
+  for (int i = threadIdx.x; i < SNST2 * SSTAGE; i += blockDim.x) ring[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SNST2; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NCW);
+    }
+  }
+  fence_proxy_async();
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  const int nitems = E * nch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int njt = (ny + 7) >> 3;
+  if (warp == NCW) {  // producer: the Y stages, then the X stages of every item
+    if (lane != 0) return;
+    int slot = 0;
+    unsigned ph = 0;
+    Item w;
+    for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
+      const int r0 = w.c * SR, rows = min(SR, n - r0);
+      const unsigned bytes = unsigned(rows) * 8u;
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const double* Pe = q == 0 ? Y + w.e * ys_e + r0 : X + w.e * xs_e + r0;
+        const int ncol = q == 0 ? ny : nx;
+        for (int g = 0; g < ncol; g += SCOLS) {
+          const int nc = min(SCOLS, ncol - g);
+          mbar_wait(&empty[slot], ph ^ 1u);
+          mbar_expect_tx(&full[slot], bytes * nc);
+          double* st = ring + size_t(slot) * SSTAGE;
+          for (int k = 0; k < nc; ++k) bulk_g2s(st + k * SCOL_STRIDE, Pe + size_t(g + k) * n, bytes, &full[slot]);
+          if (++slot == SNST2) { slot = 0; ph ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+  const int tj = warp >> 2, q4 = warp & 3;
+  const bool tile_on = tj < njt;
+  const int pw = nx + (gram ? ny : 0);
+  int slot = 0, rbuf = 0;
+  unsigned ph = 0;
+  auto advance = [&]() {
+    if (++slot == SNST2) { slot = 0; ph ^= 1u; }
+  };
+  // quarter tiles of one 8 x 8 output block -> partial rows [orow, orow + nrow) x columns of tile tj
+  auto reduce_store = [&](double a0, double a1, double* P, int orow, int nrow) {
+    double* rb = red + size_t(rbuf) * (NJ * 4 * 64) + tj * (4 * 64);
+    rbuf ^= 1;
+    rb[q4 * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = a0;
+    rb[q4 * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = a1;
+    asm volatile("bar.sync %0, 128;\n" ::"r"(1 + tj) : "memory");
+    const int t = q4 * 32 + lane;  // 0..127 within the tile group; the first 64 threads own one output each
+    if (t < 64) {
+      const int m = t & 7, nn = t >> 3;  // consecutive threads -> consecutive partial rows (coalesced)
+      const double s4 = (rb[m * 8 + nn] + rb[64 + m * 8 + nn]) + (rb[128 + m * 8 + nn] + rb[192 + m * 8 + nn]);
+      if (m < nrow && 8 * tj + nn < ny) P[(orow + m) + size_t(8 * tj + nn) * pw] = s4;
+    }
+  };
+  Item w;
+  for (int it = blockIdx.x; next_item(it, nitems, nch, active, w); it += gridDim.x) {
+    const int r0 = w.c * SR, rows = min(SR, n - r0);
+    double* P = part + size_t(w.e * nch + w.c) * pw * ny;
+    // ---- Y stages: B fragments of the warp's tile; the stages stay in the ring for the Gram
+    const int yslot0 = slot;
+    const unsigned yph0 = ph;
+    double bf[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) bf[k] = 0.0;
+    for (int j = 0; j < njt; ++j) {
+      mbar_wait(&full[slot], ph);
+      if (j == tj) {
+        const double* st = ring + size_t(slot) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 128 * q4 + (lane & 3);
+        const bool colok = 8 * j + (lane >> 2) < ny;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) bf[k] = (colok && 128 * q4 + 4 * k + (lane & 3) < rows) ? st[4 * k] : 0.0;
+      }
+      advance();
+    }
+    if (gram) {  // G[8 i + m][8 tj + nn] = sum_rows Y_i[row][m] Y_tj[row][nn]: A from the resident Y stage i
+      int gs = yslot0;
+      for (int i = 0; i < njt; ++i) {
+        double a0 = 0.0, a1 = 0.0;
+        if (tile_on) {
+          const double* st = ring + size_t(gs) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 128 * q4 + (lane & 3);
+          const bool colok = 8 * i + (lane >> 2) < ny;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const double a = (colok && 128 * q4 + 4 * k + (lane & 3) < rows) ? st[4 * k] : 0.0;
+            dmma(a0, a1, a, bf[k]);
+          }
+          reduce_store(a0, a1, P, nx + 8 * i, min(8, ny - 8 * i));
+        }
+        if (++gs == SNST2) gs = 0;
+      }
+    }
+    {  // release the Y stages
+      int rs = yslot0;
+      __syncwarp();
+      for (int j = 0; j < njt; ++j) {
+        if (lane == 0) mbar_arrive(&empty[rs]);
+        if (++rs == SNST2) rs = 0;
+      }
+      (void)yph0;
+    }
+    // ---- X stages
+    for (int g = 0; g < nx; g += SCOLS) {
+      double a0 = 0.0, a1 = 0.0;
+      mbar_wait(&full[slot], ph);
+      if (tile_on && 128 * q4 < rows) {
+        const double* st = ring + size_t(slot) * SSTAGE + (lane >> 2) * SCOL_STRIDE + 128 * q4 + (lane & 3);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) dmma(a0, a1, st[4 * k], bf[k]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      advance();
+      if (tile_on) reduce_store(a0, a1, P, g, min(SCOLS, nx - g));
+    }
+  }
+}
+
 // Output descriptor of a reduced block: element (a, b) -> p[e * s_e + (row0 + a) + (col0 + b) * ld].
 struct OutDesc {
   double* p;
@@ -424,6 +565,7 @@ static int stream_grid(int items) { return std::max(1, std::min(items, 148)); }
 
 static size_t sproj_smem(int MB) { return sizeof(double) * (size_t(SNST) * SSTAGE + 2 * size_t(SNW) * 8 * (MB + 8)); }
 static size_t supdate_smem() { return sizeof(double) * size_t(SNST) * SSTAGE; }
+static size_t sproj2_smem(int NJ) { return sizeof(double) * (size_t(SNST2) * SSTAGE + 2 * size_t(NJ) * 4 * 64); }
 
 // partial doubles of E evaluations when pw rows (nx, plus ny if the Gram is fused) x ny are reduced
 size_t stream_part_doubles(int E, int n, int pw, int ny) { return size_t(E) * cdiv(n, SR) * size_t(pw) * ny; }
@@ -446,10 +588,12 @@ void launch_sproj(cudaStream_t st, int E, int n, const double* X, long long xs_e
     const int gram = G ? 1 : 0;
     if (MB == 8)
       k_sproj<8><<<gx, STHREADS, sproj_smem(8), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
-    else if (MB == 16)
-      k_sproj<16><<<gx, STHREADS, sproj_smem(16), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
+    else if (ny <= 16)
+      k_sproj2<2><<<gx, 9 * 32, sproj2_smem(2), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
+    else if (ny <= 24)
+      k_sproj2<3><<<gx, 13 * 32, sproj2_smem(3), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
     else
-      k_sproj<32><<<gx, STHREADS, sproj_smem(32), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
+      k_sproj2<4><<<gx, 17 * 32, sproj2_smem(4), st>>>(E, n, nch, X, xs_e, nx, Y, ys_e, ny, gram, part, active);
     count_launch();
     PEXP_LAUNCH_CHECK();
     dim3 g2(std::min(cdiv(pw * ny, 256), 16), E);
@@ -488,6 +632,9 @@ void stream_init() {
   PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj_smem(8)));
   PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj_smem(16)));
   PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj_smem(32)));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj2_smem(2)));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj2_smem(3)));
+  PEXP_CUDA_TRY(cudaFuncSetAttribute(k_sproj2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sproj2_smem(4)));
   PEXP_CUDA_TRY(cudaFuncSetAttribute(k_supdate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)supdate_smem()));
   PEXP_CUDA_TRY(cudaFuncSetAttribute(k_supdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)supdate_smem()));
   PEXP_CUDA_TRY(cudaFuncSetAttribute(k_supdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)supdate_smem()));
