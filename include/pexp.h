@@ -101,6 +101,9 @@ typedef struct {
   int32_t width_buckets;  /* 0 = default (on): evaluations grouped by retained rank m_j run
                              with their own block width; -1 = off (every evaluation padded
                              to max_j m_j).                                 */
+  double scan_gamma_factor; /* Burgers homogeneous scan: its shift-and-invert parameter is
+                             scan_gamma_factor * gamma_j (own factorisation when != 1); 0 = default 1.
+                             Route only (reading #4)                                        */
 } pexp_options;
 
 /* Per-solve statistics (host memory, caller-owned). */

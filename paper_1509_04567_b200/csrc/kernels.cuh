@@ -231,6 +231,7 @@ void launch_hom_setup_block(cudaStream_t st, int Eh, int mh, int groups, int P, 
                             const double* beta, double* critc, int* horc, int* active);
 void launch_copy_end(cudaStream_t st, int P, int s, int n, const double* U, double* out);
 void launch_norms(cudaStream_t st, int E, int n, const double* X, long long xs_e, double* nrm);
+void launch_scale_f64(cudaStream_t st, double* y, const double* x, int n, double f);  // y = f x
 void launch_scale_cols(cudaStream_t st, int E, int n, const double* X, long long xs_e, const double* nrm,
                        double* Y, long long ys_e);
 void launch_add_block(cudaStream_t st, int E, int rows, int cols, const double* S, long long ss_e, int lds,

@@ -885,7 +885,8 @@ static void plan_linear(Arena& ar, LinPlan& L, const pexp_ctx* c, int P) {
 
 struct BurPlan {
   Ops O;
-  Factors F;
+  Factors F, Fs;            // Fs: factorisations with the scan's own shift (scan_gamma_factor != 1)
+  double* gam_s = nullptr;  // [P] scan shifts
   double *Uk, *Un, *ubar, *G, *Y, *Wh, *uhat, *delta;
   int *iota, *err;
   char* scan_ws = nullptr;
@@ -907,6 +908,15 @@ static void plan_burgers(Arena& ar, BurPlan& L, const pexp_ctx* c, int P) {
   L.F.sup = ar.take<double>(size_t(P) * n);
   L.F.z = ar.take<double>(size_t(P) * n);
   L.F.w = ar.take<double>(size_t(P) * n);
+  if (c->opt.scan_gamma_factor > 0 && c->opt.scan_gamma_factor != 1.0) {  // the scan's own shift
+    L.Fs = L.F;
+    L.Fs.l = ar.take<double>(size_t(P) * n);
+    L.Fs.dinv = ar.take<double>(size_t(P) * n);
+    L.Fs.sup = ar.take<double>(size_t(P) * n);
+    L.Fs.z = ar.take<double>(size_t(P) * n);
+    L.Fs.w = ar.take<double>(size_t(P) * n);
+    L.gam_s = ar.take<double>(P);
+  }
   L.Uk = ar.take<double>(size_t(P) * s * n);
   L.Un = ar.take<double>(size_t(P) * s * n);
   L.ubar = ar.take<double>(size_t(P) * n);
@@ -1117,6 +1127,7 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
   if (o.route < 0 || o.route > 2 || o.defl_tol < 0 || o.piv_tol < 0 || o.hom_group < 0 || o.hom_group > 16)
     return PEXP_EINVAL;
   if (o.width_buckets < -1 || o.width_buckets > 1) return PEXP_EINVAL;
+  if (!(o.scan_gamma_factor >= 0.0) || o.scan_gamma_factor > 16.0) return PEXP_EINVAL;
   pexp_ctx* c = new pexp_ctx;
   c->n = n;
   c->bc = bc;
@@ -1383,6 +1394,10 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
       SideFactor sf(ctx, st);
       launch_factor(sf.stream(), L.F, P, L.iota, L.B.gam, L.O, L.err);
+      if (L.gam_s) {
+        launch_scale_f64(sf.stream(), L.gam_s, L.B.gam, P, ctx->opt.scan_gamma_factor);
+        launch_factor(sf.stream(), L.Fs, P, L.iota, L.gam_s, L.O, L.err);
+      }
       launch_burgers_source(st, P, s, n, nu, u0, L.Uk, L.ubar, f, L.G);
       std::vector<int> me(E);
       int mmax = svd_stage(st, L.S, &L.B, E, n, s, L.G, tau, eta, h, me.data());
@@ -1416,7 +1431,8 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
       if (L.scan_ws) {  // persistent cooperative scan; host-driven fallback beyond its row capacity
         const int k1 = std::min(o.kcap, 512);
         const double defl_s = g_cfg.defl;
-        max_k = std::max(max_k, launch_hom_scan(st, L.F, L.B.gam, P, s, n, k1, h, eta, defl_s, u0, L.Y, L.Uk, L.Un,
+        max_k = std::max(max_k, launch_hom_scan(st, L.gam_s ? L.Fs : L.F, L.gam_s ? L.gam_s : L.B.gam, P, s, n, k1, h,
+                                                eta, defl_s, u0, L.Y, L.Uk, L.Un,
                                                 L.delta, L.scan_ws, L.scan_bytes,
                                                 rec_ks ? rec_ks + size_t(k) * P : nullptr, scan_diag));
       } else

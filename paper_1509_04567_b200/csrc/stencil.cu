@@ -263,6 +263,15 @@ __global__ void k_fill_f64(double* p, size_t count, double v) {
     p[i] = v;
 }
 
+__global__ void k_scale_f64(double* y, const double* x, int n, double f) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = f * x[i];
+}
+void launch_scale_f64(cudaStream_t st, double* y, const double* x, int n, double f) {
+  k_scale_f64<<<cdiv(n, 256), 256, 0, st>>>(y, x, n, f);
+  count_launch();
+  PEXP_LAUNCH_CHECK();
+}
+
 // ---------------------------------------------------------------- width buckets (pexp_api.cu)
 // Gather evaluations perm[0..ec) into the slots of one EBK chunk of block width wb: per-eval
 // scalars, the first wb columns of the orthonormal source basis (basis block 0) and the first wb

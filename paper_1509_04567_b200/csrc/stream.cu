@@ -11,11 +11,13 @@
 // (DMMA m8n8k4).  A stage holds 8 columns of X for R = 512 rows (each column one 4 KB bulk copy,
 // column stride padded by 32 B so a fragment load is exactly two shared-memory wavefronts).
 //
-// k_sproj: consumer warp w owns rows [64w, 64w + 64) of the chunk and keeps its Y rows as DMMA B
+// k_sproj (ny <= 8): consumer warp w owns rows [64w, 64w + 64) of the chunk and keeps its Y rows as DMMA B
 // fragments in registers for the whole item; per stage it accumulates the 8 x ny tile of X^T Y over
 // its rows, the 8 warps' tiles are summed through shared memory in warp order and written as the
-// chunk's partial; G = Y^T Y uses the same registers as A and B operands.  Partials are summed in
-// chunk order by k_sred (deterministic, parallel over outputs).
+// chunk's partial; G = Y^T Y uses the same registers as A and B operands.  k_sproj2 (ny > 8, see there):
+// warps own (column tile, row quarter) pairs and reduce behind per-tile named barriers, which keeps the
+// DMMA pipe busy at the wide blocks where it is the limiter.  Partials are summed in chunk order by
+// k_sred (deterministic, parallel over outputs).
 // k_supdate: consumer warp w owns the same 64 rows; its D fragments (64 rows x ny) stay in
 // registers across all stages (the sum over X's columns is the DMMA k-dimension), B fragments are
 // the matching 8 rows of M per stage (L1/L2 resident), the epilogue writes beta Y + alpha acc.
@@ -496,7 +498,7 @@ k_supdate(int E, int n, int nch, const double* X, long long xs_e, int nx0, const
         }
       }
     };
-    constexpr bool PREF = NJ <= 2;  // register budget: prefetch M one stage ahead below MB = 32
+    constexpr bool PREF = NJ <= 2;  // prefetching M one stage ahead pays only below MB = 32 (measured: 2.58 vs 2.70 s on C5)
     if (PREF) load_bm(0, bm);
     for (int g = 0; g < nx; g += SCOLS) {
       if (PREF)
