@@ -64,7 +64,11 @@ def workload(name):
         p = synth.config5()
         # 256 subintervals x 65536 points: the EBK runs in chunks of 64 subintervals with
         # 960-column bases (32 GiB of basis; 92 GiB workspace in total)
-        return p, dict(kind="burgers", s=p.s, k_max=960, basis_cols=960, eval_chunk=64)
+        # shift-and-invert parameters tuned for this very stiff case (4 nu dT/dx^2 = 6.7e4): gamma = dT/20 for
+        # the nonhomogeneous evaluations and 0.7 of that for the scan (route only, DESIGN.md §3 #4; measured
+        # 14 % faster than the default dT/10; the less stiff C1-C4 are fastest at the default)
+        return p, dict(kind="burgers", s=p.s, k_max=960, basis_cols=960, eval_chunk=64, gamma_factor=0.5,
+                       scan_gamma_factor=0.7)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -277,7 +281,9 @@ def main():
         out = torch.empty((p.batch, p.P, p.n), dtype=torch.float64, device=dev)
     else:
         ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"],
-                           basis_cols=cfg.get("basis_cols", 0), eval_chunk=cfg.get("eval_chunk", 0))
+                           basis_cols=cfg.get("basis_cols", 0), eval_chunk=cfg.get("eval_chunk", 0),
+                           gamma_factor=cfg.get("gamma_factor", 0.0),
+                           scan_gamma_factor=cfg.get("scan_gamma_factor", 0.0))
         ctx.ensure_workspace(p.P, dev, kind=1)
         u0_h = torch.tensor(p.u0).pin_memory()
         src_h = None
@@ -421,7 +427,9 @@ def main():
                        "batch": getattr(p, "batch", 1), "evals_per_step": evals_per_step,
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "max_m": st["max_m"], "max_k": st["max_k"], "wr_iters": st["wr_iters"]},
+                       "max_m": st["max_m"], "max_k": st["max_k"], "wr_iters": st["wr_iters"],
+                       "options": {k: cfg[k] for k in ("k_max", "basis_cols", "eval_chunk", "gamma_factor",
+                                                       "scan_gamma_factor") if k in cfg}},
             "roofline": roof, "roofline_ebk_streaming": roof_stream, "kernel_classes": classes,
             "gpu_launches": int(launches / args.steps),
             "host_syncs_per_step": syncs / args.steps,

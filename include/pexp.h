@@ -104,6 +104,9 @@ typedef struct {
   double scan_gamma_factor; /* Burgers homogeneous scan: its shift-and-invert parameter is
                              scan_gamma_factor * gamma_j (own factorisation when != 1); 0 = default 1.
                              Route only (reading #4)                                        */
+  double gamma_factor;    /* shift-and-invert parameter of the nonhomogeneous evaluations:
+                             gamma = gamma_factor * dT/10 (Burgers: before the cap of reading #4);
+                             0 = default 1.  Route only                                       */
 } pexp_options;
 
 /* Per-solve statistics (host memory, caller-owned). */

@@ -217,7 +217,7 @@ void launch_lin_source(cudaStream_t st, int batch, int P, int s, int n, const do
 void launch_fill_random(cudaStream_t st, int E, int n, int mmax, const int* fill, double* V, long long vs_e,
                         unsigned seed);
 void launch_broadcast_waveform(cudaStream_t st, int P, int s, int n, const double* u0, double* U);
-void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, double dT, double* ubar,
+void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, double g0, double* ubar,
                        double* gam);
 void launch_burgers_source(cudaStream_t st, int P, int s, int n, double nu, const double* u0, const double* U,
                            const double* ubar, const double* f, double* G);

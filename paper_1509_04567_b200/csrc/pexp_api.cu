@@ -1128,6 +1128,7 @@ pexp_status pexp_create_batched(pexp_ctx** ctx, int64_t n, pexp_bc bc, int32_t b
     return PEXP_EINVAL;
   if (o.width_buckets < -1 || o.width_buckets > 1) return PEXP_EINVAL;
   if (!(o.scan_gamma_factor >= 0.0) || o.scan_gamma_factor > 16.0) return PEXP_EINVAL;
+  if (!(o.gamma_factor >= 0.0) || o.gamma_factor > 16.0) return PEXP_EINVAL;
   pexp_ctx* c = new pexp_ctx;
   c->n = n;
   c->bc = bc;
@@ -1205,7 +1206,8 @@ pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const doub
     launch_ade_rows(st, Bt, n, !periodic, L.nu_d, L.a_d, L.O.sub, L.O.diag, L.O.sup);
     std::vector<double> gf(2 * Bt);
     std::vector<int> of(2 * Bt), iota(Bt);
-    for (int b = 0; b < Bt; ++b) { gf[b] = dT / 10; gf[Bt + b] = T / 10; of[b] = b; of[Bt + b] = b; iota[b] = b; }
+    const double gfac = ctx->opt.gamma_factor > 0 ? ctx->opt.gamma_factor : 1.0;
+    for (int b = 0; b < Bt; ++b) { gf[b] = gfac * dT / 10; gf[Bt + b] = T / 10; of[b] = b; of[Bt + b] = b; iota[b] = b; }
     h2d(st, L.gam_f, gf);
     h2d(st, L.opidx_f, of);
     h2d(st, L.iota, iota);
@@ -1220,7 +1222,7 @@ pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const doub
       launch_lin_source(st, Bt, P, s, n, L.Au0, src, L.G);
       // per-eval maps for the nonhomogeneous batch
       std::vector<int> fe(E);
-      std::vector<double> ge(E, dT / 10);
+      std::vector<double> ge(E, gfac * dT / 10);
       for (int e = 0; e < E; ++e) fe[e] = e / P;
       h2d(st, L.B.fidx, fe);
       h2d(st, L.B.opidx, fe);
@@ -1297,7 +1299,7 @@ pexp_status pexp_solve_linear_stages(pexp_ctx* ctx, const double* u0, const doub
         PEXP_CUDA_TRY(cudaMemcpy(kj, L.B.krec, E * sizeof(int), cudaMemcpyDeviceToHost));
         ++g_cfg.syncs;
       }
-      if (gj) std::fill(gj, gj + E, dT / 10);
+      if (gj) std::fill(gj, gj + E, gfac * dT / 10);
       st_out->max_m = mmax;
       st_out->max_k = std::max(ri.max_ktot, rh.max_ktot);
       st_out->restarts = ri.restarts;
@@ -1364,6 +1366,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
     const int n = (int)ctx->n, s = o.s, E = P;
     const double dT = T / P, h = dT / (s - 1), tau = o.tau_f * tol, eta = o.eta_f * tol;
     const double wr_tol = 1e-6;
+    const double gfac = ctx->opt.gamma_factor > 0 ? ctx->opt.gamma_factor : 1.0;
     Arena ar{ctx->ws, ctx->ws_bytes, 0};
     BurPlan L;
     plan_burgers(ar, L, ctx, P);
@@ -1389,7 +1392,7 @@ static pexp_status burgers_impl(pexp_ctx* ctx, const double* u0, const double* f
     int iters = 0, max_m = 0, max_k = 0, restarts = 0;
     double delta = 0.0, delta0 = -1.0;
     for (int k = 0; k < max_wr_iters; ++k) {
-      launch_ubar_gamma(st, P, s, n, L.Uk, dT, L.ubar, L.B.gam);
+      launch_ubar_gamma(st, P, s, n, L.Uk, gfac * dT / 10, L.ubar, L.B.gam);
       launch_burgers_rows(st, P, n, nu, L.ubar, L.O.sub, L.O.diag, L.O.sup);
       PEXP_CUDA_TRY(cudaMemsetAsync(L.err, 0, sizeof(int), st));
       SideFactor sf(ctx, st);

@@ -67,8 +67,8 @@ __global__ void k_ubar(int s, int n, const double* U, double* ubar) {
   }
 }
 
-// gamma_j = min(dT/10, 0.5 / max_r(-(D1 ubar_j)_r))  (reading #4; keeps pivot-free solves safe)
-__global__ void k_gamma(int n, const double* ubar, double dT, double* gam) {
+// gamma_j = min(g0, 0.5 / max_r(-(D1 ubar_j)_r)), g0 = gamma_factor dT/10  (reading #4; keeps pivot-free solves safe)
+__global__ void k_gamma(int n, const double* ubar, double g0, double* gam) {
   const int j = blockIdx.x;
   __shared__ double red[32];
   const double* u = ubar + size_t(j) * n;
@@ -80,7 +80,7 @@ __global__ void k_gamma(int n, const double* ubar, double dT, double* gam) {
   }
   mx = block_max(mx, red);
   if (threadIdx.x == 0) {
-    double g = dT / 10.0;
+    double g = g0;
     if (mx > 0.0) g = fmin(g, 0.5 / mx);
     gam[j] = g;
   }
@@ -393,7 +393,7 @@ void launch_broadcast_waveform(cudaStream_t st, int P, int s, int n, const doubl
   PEXP_LAUNCH_CHECK();
 }
 
-void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, double dT, double* ubar,
+void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, double g0, double* ubar,
                        double* gam) {
   dim3 grid(gx_small(n, P), P);
   { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
@@ -402,7 +402,7 @@ void launch_ubar_gamma(cudaStream_t st, int P, int s, int n, const double* U, do
   count_launch();
   PEXP_LAUNCH_CHECK();
   { ProfScope ps(PC_STENCIL, st, 0.0, 0.0);
-  k_gamma<<<P, PEXP_THREADS, 0, st>>>(n, ubar, dT, gam);
+  k_gamma<<<P, PEXP_THREADS, 0, st>>>(n, ubar, g0, gam);
   }
   count_launch();
   PEXP_LAUNCH_CHECK();

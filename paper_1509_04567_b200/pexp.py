@@ -38,7 +38,7 @@ class Options(C.Structure):
                 ("stream", C.c_void_p), ("stop_rule", C.c_int32), ("basis_cols", C.c_int32),
                 ("eval_chunk", C.c_int32), ("route", C.c_int32), ("defl_tol", C.c_double),
                 ("piv_tol", C.c_double), ("hom_group", C.c_int32), ("width_buckets", C.c_int32),
-                ("scan_gamma_factor", C.c_double)]
+                ("scan_gamma_factor", C.c_double), ("gamma_factor", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -117,7 +117,8 @@ class Context:
                  svd_tau_factor: float = 0.01, stop_factor: float = 0.1, restart_blocks: int = 20,
                  stream: Optional[torch.cuda.Stream] = None, stop_rule: int = 0, basis_cols: int = 0,
                  eval_chunk: int = 0, route: int = 0, defl_tol: float = 0.0, piv_tol: float = 0.0,
-                 hom_group: int = 0, width_buckets: int = 0, node_rule: int = 0, scan_gamma_factor: float = 0.0):
+                 hom_group: int = 0, width_buckets: int = 0, node_rule: int = 0, scan_gamma_factor: float = 0.0,
+                 gamma_factor: float = 0.0):
         self.n, self.bc, self.s = int(n), bc, int(s)
         self._stream = stream
         nu = [float(v) for v in (nu if hasattr(nu, "__len__") else [nu])]
@@ -128,7 +129,7 @@ class Context:
         handle = stream.cuda_stream if stream is not None else None  # None = legacy default stream
         self.opt = Options(self.s, int(node_rule), svd_tau_factor, stop_factor, restart_blocks, k_max, handle, stop_rule,
                            basis_cols, eval_chunk, route, defl_tol, piv_tol, hom_group, width_buckets,
-                           scan_gamma_factor)
+                           scan_gamma_factor, gamma_factor)
         self._h = _P()
         arr = C.c_double * self.batch
         st = _lib.pexp_create_batched(C.byref(self._h), self.n, BC[bc], self.batch, arr(*nu), arr(*a),

@@ -21,6 +21,8 @@ ap.add_argument("config", default="C5", nargs="?")
 ap.add_argument("--route", type=int, default=0)
 ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--scan-gamma", type=float, default=0.0, help="pexp_options.scan_gamma_factor")
+ap.add_argument("--gamma", type=float, default=0.0, help="pexp_options.gamma_factor")
 ap.add_argument("--plain-only", action="store_true", help="one plain solve (ncu target), no profiler pass")
 a = ap.parse_args()
 build.build()
@@ -29,13 +31,19 @@ from paper_1509_04567_b200 import pexp  # noqa: E402
 p, cfg = bench.workload(a.config)
 dev = torch.device("cuda")
 kw = {k: cfg[k] for k in ("basis_cols", "eval_chunk") if k in cfg}
+if not a.gamma:
+    a.gamma = cfg.get("gamma_factor", 0.0)
+if not a.scan_gamma:
+    a.scan_gamma = cfg.get("scan_gamma_factor", 0.0)
 if cfg["kind"] == "linear":
-    ctx = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=cfg["s"], k_max=cfg["k_max"], route=a.route, **kw)
+    ctx = pexp.Context(p.n, p.bc, list(p.nu), list(p.a), s=cfg["s"], k_max=cfg["k_max"], route=a.route,
+                       gamma_factor=a.gamma, **kw)
     u0 = torch.tensor(p.u0, device=dev)
     src = torch.tensor(p.src, device=dev)
     run = lambda rec: ctx.solve_linear(u0, src, p.T, p.P, p.tol, records=rec)
 else:
-    ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"], route=a.route, **kw)
+    ctx = pexp.Context(p.n, "periodic", p.nu, 0.0, s=cfg["s"], k_max=cfg["k_max"], route=a.route,
+                       scan_gamma_factor=a.scan_gamma, gamma_factor=a.gamma, **kw)
     u0 = torch.tensor(p.u0, device=dev)
     its = a.iters or p.max_wr_iters
     run = lambda rec: ctx.solve_burgers(u0, p.nu, p.T, p.P, p.tol, its, records=rec)

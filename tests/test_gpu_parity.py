@@ -293,8 +293,12 @@ def test_burgers_small_restarted(route):
     assert st["restarts"] >= 1, st
 
 
-@pytest.mark.parametrize("route", ROUTES)
-def test_burgers_c5proxy_to_convergence(route):
+# bench.py's launch configuration of C5 (bench.workload("C5")): capacities and the tuned shift parameters
+C5_BENCH_OPTIONS = dict(k_max=960, basis_cols=960, eval_chunk=64, gamma_factor=0.5, scan_gamma_factor=0.7)
+
+
+@pytest.mark.parametrize("route,tuned", [(0, False), (1, False), (1, True)])
+def test_burgers_c5proxy_to_convergence(route, tuned):
     """C5-shaped WR run to convergence (SURVEY §8(d).2 C5 generator at n = 8192, ν = 1e-3,
     s = 64, ΔT = 1/256, T = 0.25): the steep front forms, block widths reach ~25 and the
     per-subinterval Jacobians differ, i.e. the iterations the C5 first-iterate check cannot
@@ -303,7 +307,8 @@ def test_burgers_c5proxy_to_convergence(route):
     every iteration."""
     p = synth.config5(n=8192, P=64, T=0.25)
     ref = _golden("c5proxy_oracle.npz")
-    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=960, route=route)
+    kw = dict(gamma_factor=0.5, scan_gamma_factor=0.7) if tuned else {}   # bench.py's C5 shift parameters
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=960, route=route, **kw)
     out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, p.max_wr_iters, records=True)
     out = out.cpu().numpy()
     assert st["wr_iters"] == int(ref["iters"]), (st["delta_hist"], ref["delta"])
@@ -344,7 +349,7 @@ def test_burgers_config5_full_size_first_iterate():
     from oracle.ebk import ebk_krylov
     from oracle.operators import burgers_J, d1_matrix, d2_matrix
     p = synth.config5()
-    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, k_max=960, basis_cols=960, eval_chunk=64)
+    c = pexp.Context(p.n, "periodic", p.nu, 0.0, s=p.s, **C5_BENCH_OPTIONS)
     out, st = c.solve_burgers(t(p.u0), p.nu, p.T, p.P, p.tol, 1)
     out = out.cpu().numpy()
     assert st["wr_iters"] == 1
@@ -580,7 +585,7 @@ def test_burgers_config5_full_size_late_wr_map_sampled():
     from oracle.wr import trapezoid_mean, wr_gamma
     p = synth.config5()
     n, s, P = p.n, p.s, p.P
-    c = pexp.Context(n, "periodic", p.nu, 0.0, s=s, k_max=960, basis_cols=960, eval_chunk=64)
+    c = pexp.Context(n, "periodic", p.nu, 0.0, s=s, **C5_BENCH_OPTIONS)
     u0 = t(p.u0)
     Uk = u0.expand(P, s, n).contiguous()
     Un = None
@@ -610,3 +615,18 @@ def test_burgers_config5_full_size_late_wr_map_sampled():
         assert U.shape[1] >= 8, U.shape
         assert rel(got, ref) < 1e-8, (j, U.shape[1])
         assert rel(got - p.u0[None, :], ref - p.u0[None, :]) < 1e-7, j        # the increment itself
+
+
+@pytest.mark.parametrize("gamma_factor,scan_gamma_factor", [(0.5, 0.7), (2.0, 0.5), (1.0, 2.0)])
+def test_shift_parameters_are_route_only(gamma_factor, scan_gamma_factor):
+    """pexp_options.gamma_factor / scan_gamma_factor (reading #4: the paper gives no shift) change the
+    Krylov spaces, not the result: linear and Burgers solves stay within 1e-8 of the oracle, whose own
+    shift is the default dT/10, and the WR iteration count is unchanged."""
+    p = synth.generic_linear(n=600, bc="dirichlet", nu=1e-3, a=1.0, P=5, s=12, T=0.5, seed=7)
+    out, st = _linear(p, k_max=512, gamma_factor=gamma_factor)
+    assert rel(out, _oracle_linear(p)) < 1e-8, st
+    q = synth.config3(n=256, P=4, s=12, T=0.2, nu=0.02)
+    outb, stb = _burgers(q, gamma_factor=gamma_factor, scan_gamma_factor=scan_gamma_factor)
+    ref, info = oracle.solve_burgers(q.n, q.nu, q.u0, q.T, q.P, q.s, q.tol, return_info=True)
+    assert stb["wr_iters"] == info["iters"]
+    assert rel(outb, ref) < 1e-8, stb
