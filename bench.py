@@ -62,12 +62,12 @@ def workload(name):
         return p, dict(kind="burgers", s=p.s, k_max=256)
     if name == "C5":
         p = synth.config5()
-        # 256 subintervals x 65536 points: the EBK runs in chunks of 64 subintervals with
-        # 960-column bases (32 GiB of basis; 92 GiB workspace in total)
+        # 256 subintervals x 65536 points: the EBK runs in chunks of 128 subintervals with 640-column
+        # bases per restart cycle (40 GiB of basis; 134 GiB workspace in total)
         # shift-and-invert parameters tuned for this very stiff case (4 nu dT/dx^2 = 6.7e4): gamma = dT/20 for
         # the nonhomogeneous evaluations and 0.7 of that for the scan (route only, DESIGN.md §3 #4; measured
         # 14 % faster than the default dT/10; the less stiff C1-C4 are fastest at the default)
-        return p, dict(kind="burgers", s=p.s, k_max=960, basis_cols=960, eval_chunk=64, gamma_factor=0.5,
+        return p, dict(kind="burgers", s=p.s, k_max=960, basis_cols=640, eval_chunk=128, gamma_factor=0.5,
                        scan_gamma_factor=0.7)
     raise SystemExit(f"unknown config {name}")
 

@@ -23,6 +23,8 @@ ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--scan-gamma", type=float, default=0.0, help="pexp_options.scan_gamma_factor")
 ap.add_argument("--gamma", type=float, default=0.0, help="pexp_options.gamma_factor")
+ap.add_argument("--eval-chunk", type=int, default=0)
+ap.add_argument("--basis-cols", type=int, default=0)
 ap.add_argument("--plain-only", action="store_true", help="one plain solve (ncu target), no profiler pass")
 a = ap.parse_args()
 build.build()
@@ -31,6 +33,10 @@ from paper_1509_04567_b200 import pexp  # noqa: E402
 p, cfg = bench.workload(a.config)
 dev = torch.device("cuda")
 kw = {k: cfg[k] for k in ("basis_cols", "eval_chunk") if k in cfg}
+if a.eval_chunk:
+    kw["eval_chunk"] = a.eval_chunk
+if a.basis_cols:
+    kw["basis_cols"] = a.basis_cols
 if not a.gamma:
     a.gamma = cfg.get("gamma_factor", 0.0)
 if not a.scan_gamma:

@@ -294,7 +294,7 @@ def test_burgers_small_restarted(route):
 
 
 # bench.py's launch configuration of C5 (bench.workload("C5")): capacities and the tuned shift parameters
-C5_BENCH_OPTIONS = dict(k_max=960, basis_cols=960, eval_chunk=64, gamma_factor=0.5, scan_gamma_factor=0.7)
+C5_BENCH_OPTIONS = dict(k_max=960, basis_cols=640, eval_chunk=128, gamma_factor=0.5, scan_gamma_factor=0.7)
 
 
 @pytest.mark.parametrize("route,tuned", [(0, False), (1, False), (1, True)])
