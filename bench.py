@@ -34,6 +34,18 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x
 METRIC = "EBK evaluations/s (Paraexp-EBK solve; solve time = ms_per_step)"
 
 
+# CUDA kernels behind each profiler class (paper_1509_04567_b200/csrc)
+KERNELS_OF_CLASS = {
+    "sai_solve": "k_sai_solve (tridiag.cu)", "xty": "k_xty_sq / k_xty_tall / k_xty_mma + k_reduce (tsmm.cu)",
+    "combine": "k_combine (tsmm.cu)", "small_problem": "k_small_problem (small.cu)",
+    "small_dense": "k_block_chol, k_sym_eig_select, k_onesided_svd, k_spline, ... (small.cu)",
+    "stencil": "k_burgers_source, k_ubar, k_gamma, k_superpose, ... (stencil.cu)",
+    "factor": "k_factor / k_factor_par (tridiag.cu)", "arnoldi_step": "k_arnoldi_step<MB> (arnoldi.cu)",
+    "hom_scan": "k_hom_scan (hom_scan.cu)", "small_hom": "k_small_hom (small.cu)",
+    "stream_proj": "k_sproj<8>, k_sproj2<2|3|4> + k_sred (stream.cu)", "stream_update": "k_supdate<8|16|32> (stream.cu)",
+    "scan_output": "k_scan_output (hom_scan.cu)"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -394,6 +406,7 @@ def main():
     if dom == "hom_scan":
         roof["note"] = ("sequential chain (255 subintervals x ~37 dependent Arnoldi steps per WR iteration): latency-bound; "
                         "its basis rows live in shared memory, so DRAM traffic is far below the algorithmic bytes")
+    roof["cuda_kernels"] = KERNELS_OF_CLASS.get(dom, dom)
     roof["share_of_step"] = d["ms"] / max(1e-9, prof_step_ms)
     roof["launches_per_step"] = d["launches"]
     roof["ms_per_step"] = d["ms"]
