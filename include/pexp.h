@@ -162,6 +162,13 @@ PEXP_API const char* pexp_last_error(const pexp_ctx* ctx);
 /* Sample times t_{j,i} (header comment) written to t_host[j*s + i], length P*s. */
 PEXP_API pexp_status pexp_sample_times(const pexp_ctx* ctx, double T, int32_t P, double* t_host);
 
+/* node_rule = 1 only (host-only, no device work): the linear map from the s values of a coefficient row at
+ * the Chebyshev-Lobatto nodes of a subinterval of length dT to the Taylor coefficients p^(q)(sigma_i),
+ * q = 0..11, of the degree-(s-1) interpolant at the uniform piece starts sigma_i = i dT/(s-1), i = 0..s-2
+ * (DESIGN.md §3 #23):  D_host[(i*12 + q)*s + k], (s-1)*12*s doubles.  Returns the number of Taylor terms
+ * (12) or 0 for a context with node_rule = 0 / bad arguments. */
+PEXP_API int32_t pexp_chebyshev_taylor_matrix(const pexp_ctx* ctx, double dT, double* D_host);
+
 /* Bytes of device scratch needed for solves with P subintervals.
  * kind: 0 = pexp_solve_linear (and the stage entry points), 1 = pexp_solve_burgers,
  * 2 = the larger of both.  Returns 0 for invalid arguments. */

@@ -1156,6 +1156,14 @@ pexp_status pexp_sample_times(const pexp_ctx* ctx, double T, int32_t P, double* 
   return PEXP_OK;
 }
 
+int32_t pexp_chebyshev_taylor_matrix(const pexp_ctx* ctx, double dT, double* D_host) {
+  if (!ctx || !D_host || !(dT > 0) || ctx->opt.node_rule != 1) return 0;
+  Opts o = norm_opts(ctx->opt);
+  const std::vector<double> D = cheb_taylor_matrix(o.s, o.nq, dT);
+  std::copy(D.begin(), D.end(), D_host);
+  return o.nq;
+}
+
 size_t pexp_workspace_bytes(const pexp_ctx* ctx, int32_t P, int32_t kind) {
   if (!ctx || P < 1 || kind < 0 || kind > 2) return 0;
   if (kind == 0) return lin_bytes(ctx, P) + 256;

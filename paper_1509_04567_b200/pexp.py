@@ -26,6 +26,7 @@ BC = {"periodic": 0, "dirichlet": 1}
 EXPORTED = ["pexp_create", "pexp_create_batched", "pexp_destroy", "pexp_last_error", "pexp_sample_times",
             "pexp_workspace_bytes", "pexp_set_workspace", "pexp_solve_linear", "pexp_solve_burgers",
             "pexp_solve_burgers_forced", "pexp_solve_linear_stages", "pexp_wr_map",
+            "pexp_chebyshev_taylor_matrix",
             "pexp_sai_solve", "pexp_source_svd", "pexp_expm_batched", "pexp_profile_enable", "pexp_profile_read"]
 PROFILE_CLASSES = ["sai_solve", "xty", "combine", "small_problem", "small_dense", "stencil", "factor",
                    "arnoldi_step", "hom_scan", "small_hom", "stream_proj", "stream_update",
@@ -84,6 +85,8 @@ _lib.pexp_solve_burgers_forced.argtypes = [_P, _P, _P, C.c_double, C.c_double, C
 _lib.pexp_solve_linear_stages.argtypes = [_P, _P, _P, _P, C.c_double, C.c_int32, C.c_double, _P, _P, _P,
                                           C.POINTER(Stats)]
 _lib.pexp_wr_map.argtypes = [_P, _P, _P, _P, C.c_double, C.c_double, C.c_int32, C.c_double, _P, _P, C.POINTER(Stats)]
+_lib.pexp_chebyshev_taylor_matrix.argtypes = [_P, C.c_double, C.POINTER(C.c_double)]
+_lib.pexp_chebyshev_taylor_matrix.restype = C.c_int32
 _lib.pexp_sai_solve.argtypes = [_P, C.c_int32, C.c_double, _P, C.c_int32, _P]
 _lib.pexp_source_svd.argtypes = [_P, _P, C.c_int32, C.c_double, C.POINTER(C.c_int32), _P, _P]
 _lib.pexp_expm_batched.argtypes = [_P, _P, C.c_int32, C.c_int32, _P]
@@ -94,7 +97,7 @@ _lib.pexp_profile_read.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C
 _lib.pexp_profile_read.restype = C.c_int32
 for _f in EXPORTED:
     if _f not in ("pexp_destroy", "pexp_last_error", "pexp_workspace_bytes", "pexp_profile_enable",
-                  "pexp_profile_read"):
+                  "pexp_profile_read", "pexp_chebyshev_taylor_matrix"):
         getattr(_lib, _f).restype = C.c_int
 
 
@@ -164,6 +167,14 @@ class Context:
         t = torch.empty(P * self.s, dtype=torch.float64)
         self._check(_lib.pexp_sample_times(self._h, float(T), int(P), C.cast(t.data_ptr(), C.POINTER(C.c_double))))
         return t.view(P, self.s)
+
+    def chebyshev_taylor_matrix(self, dT: float) -> torch.Tensor:
+        """pexp_chebyshev_taylor_matrix (node_rule = 1, host-only): tensor [s-1][12][s]."""
+        D = torch.empty((self.s - 1) * 12 * self.s, dtype=torch.float64)
+        nq = _lib.pexp_chebyshev_taylor_matrix(self._h, float(dT), C.cast(D.data_ptr(), C.POINTER(C.c_double)))
+        if nq != 12:
+            raise PexpError(PEXP_EINVAL, "pexp_chebyshev_taylor_matrix: needs a node_rule = 1 context")
+        return D.view(self.s - 1, 12, self.s)
 
     def solve_linear(self, u0: torch.Tensor, src: torch.Tensor, T: float, P: int, tol: float,
                      out: Optional[torch.Tensor] = None, records: bool = False):

@@ -80,6 +80,33 @@ def test_sample_times_chebyshev_rule(P):
         P.Context(50, "periodic", 1e-2, 1.0, node_rule=2)
 
 
+def test_chebyshev_taylor_matrix_host_logic(P):
+    """Host logic of node_rule = 1: the library's nodal-values -> Taylor-coefficients map (long double
+    Chebyshev recurrences) against (i) exact derivatives of a polynomial of degree s-1, hand-differentiated,
+    and (ii) the oracle's numpy.polynomial route on a smooth function (low orders, where that route is
+    accurate)."""
+    from oracle.lowrank import cheb_taylor
+    s, dT = 10, 0.3
+    c = P.Context(50, "periodic", 1e-2, 1.0, s=s, node_rule=1)
+    D = c.chebyshev_taylor_matrix(dT).numpy()                      # [s-1][12][s]
+    tau = 0.5 * dT * (1 - np.cos(np.pi * np.arange(s) / (s - 1)))
+    r = np.random.default_rng(1)
+    a = r.standard_normal(s)                                       # p(tau) = sum_d a[d] (tau/dT)^d
+    y = sum(a[d] * (tau / dT) ** d for d in range(s))
+    got = D @ y                                                    # [s-1][12]
+    for i in range(s - 1):
+        sg = i * dT / (s - 1)
+        for q in range(min(12, s)):
+            ref = sum(a[d] * np.prod(np.arange(d, d - q, -1)) * (sg / dT) ** (d - q) / dT ** q for d in range(q, s))
+            assert abs(got[i, q] - ref) <= 1e-10 * max(1.0, abs(ref), (s * s / dT) ** q * 1e-6), (i, q)
+    f = np.sin(7 * tau + 0.3)
+    ref = cheb_taylor(f[None, :], dT, s - 1)[:, :4, 0]             # orders 0..3
+    np.testing.assert_allclose((D @ f)[:, :4], ref, rtol=1e-9, atol=1e-9 * 7 ** 3)
+    assert P.Context(50, "periodic", 1e-2, 1.0, s=s)._h is not None
+    with pytest.raises(P.PexpError):
+        P.Context(50, "periodic", 1e-2, 1.0, s=s).chebyshev_taylor_matrix(dT)   # node_rule = 0
+
+
 def test_workspace_query_and_solve_without_workspace(P):
     c = P.Context(128, "periodic", 1e-2, 1.0, s=8)
     assert c.workspace_bytes(4, 0) > 0
