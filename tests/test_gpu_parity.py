@@ -122,8 +122,39 @@ def _linear(p, k_max=256, records=False, **kw):
     return out.cpu().numpy(), st
 
 
+_ORACLE_MEMO = {}
+
+
+def _memo_key(tag, p, kw, arrays):
+    """Key of one oracle call: every scalar argument and a digest of every array argument."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return (tag, p.n, getattr(p, "bc", "periodic"), p.T, p.P, p.s, p.tol, tuple(sorted(kw.items())), h.hexdigest())
+
+
 def _oracle_linear(p, **kw):
-    return oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol, **kw)
+    """oracle.solve_linear, memoised per pytest process on its exact inputs: several tests compare
+    different launch configurations of the CUDA path against the SAME oracle run (C2 reduced: ~170 s
+    of CPU each), which is computed once.  Only oracle outputs are stored, keyed by oracle inputs."""
+    want_info = kw.pop("return_info", False)
+    key = _memo_key("linear", p, kw, (p.nu, p.a, p.u0, p.src))
+    if key not in _ORACLE_MEMO:
+        _ORACLE_MEMO[key] = oracle.solve_linear(p.n, p.bc, p.nu, p.a, p.u0, p.src, p.T, p.P, p.s, p.tol,
+                                                return_info=True, **kw)
+    out, info = _ORACLE_MEMO[key]
+    return (out, info) if want_info else out
+
+
+def _oracle_burgers(p):
+    """oracle.solve_burgers(..., return_info=True), memoised like _oracle_linear."""
+    key = _memo_key("burgers", p, {}, ([p.nu], p.u0))
+    if key not in _ORACLE_MEMO:
+        _ORACLE_MEMO[key] = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
+    return _ORACLE_MEMO[key]
 
 
 ROUTES = [0, 1]  # pexp_options.route: 0 auto (fused cluster step where it fits), 1 streaming route
@@ -278,7 +309,7 @@ def test_burgers_small(route):
 def test_burgers_config3_full(route):
     p = synth.config3()
     out, st = _burgers(p, route=route)
-    ref, info = oracle.solve_burgers(p.n, p.nu, p.u0, p.T, p.P, p.s, p.tol, return_info=True)
+    ref, info = _oracle_burgers(p)
     assert st["wr_iters"] == info["iters"], (st, info["delta"])
     assert rel(out, ref) < 1e-8, st
 
