@@ -64,56 +64,89 @@ __device__ inline double cta_sai_solve(int n, int periodic, const double* l, con
   const int t = threadIdx.x;
   const int nchunk = (n + CHUNK - 1) / CHUNK;
   double carry = 0.0, dot = 0.0;
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const int base = ch * CHUNK;
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      int si = (i / EPT) * SPAD + (i % EPT);
-      double bv = g < n ? b[g] : 0.0;
-      s0[si] = bv;
-      s1[si] = g < n ? -l[g] : 1.0;
-      if (periodic && g < n) dot = fma(fw[g], bv, dot);
-    }
-    __syncthreads();
-    Aff m{1.0, 0.0};
+  // Software pipeline: the operands of the next chunk are loaded into registers while this chunk is
+  // scanned, so the dependent chain of chunks never waits on a DRAM round trip (ncu before:
+  // 48 % of the stall samples on the x / fz loads of the backward pass, profiles/r02_ncu_c5_sai_solve.txt).
+  {
+    double pb[EPT], pl[EPT], pw[EPT];
+    auto load_fwd = [&](int ch) {
+      const int base = ch * CHUNK;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
-    Aff tot;
-    Aff pre = block_excl_scan<false>(m, t, wsm, tot);
-    double y = fma(pre.A, carry, pre.B);
+      for (int k = 0; k < EPT; ++k) {
+        const int g = base + t + k * PEXP_THREADS;
+        const bool ok = g < n;
+        pb[k] = ok ? b[g] : 0.0;
+        pl[k] = ok ? -l[g] : 1.0;
+        pw[k] = (periodic && ok) ? fw[g] : 0.0;
+      }
+    };
+    load_fwd(0);
+    for (int ch = 0; ch < nchunk; ++ch) {
+      const int base = ch * CHUNK;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      y = fma(s1[t * SPAD + k], y, s0[t * SPAD + k]);
-      s0[t * SPAD + k] = y;
+      for (int k = 0; k < EPT; ++k) {
+        const int i = t + k * PEXP_THREADS;
+        const int si = (i / EPT) * SPAD + (i % EPT);
+        s0[si] = pb[k];
+        s1[si] = pl[k];
+        if (periodic) dot = fma(pw[k], pb[k], dot);
+      }
+      __syncthreads();
+      if (ch + 1 < nchunk) load_fwd(ch + 1);
+      Aff m{1.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
+      Aff tot;
+      Aff pre = block_excl_scan<false>(m, t, wsm, tot);
+      double y = fma(pre.A, carry, pre.B);
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        y = fma(s1[t * SPAD + k], y, s0[t * SPAD + k]);
+        s0[t * SPAD + k] = y;
+      }
+      carry = fma(tot.A, carry, tot.B);
+      __syncthreads();
+      for (int i = t; i < CHUNK; i += PEXP_THREADS) {
+        int g = base + i;
+        if (g < n) x[g] = s0[(i / EPT) * SPAD + (i % EPT)];
+      }
+      __syncthreads();
     }
-    carry = fma(tot.A, carry, tot.B);
-    __syncthreads();
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      if (g < n) x[g] = s0[(i / EPT) * SPAD + (i % EPT)];
-    }
-    __syncthreads();
   }
   double f = 0.0;
   if (periodic) f = block_sum(dot, red);
   carry = 0.0;
   double nrm2 = 0.0;
   const int r = PEXP_THREADS - 1 - t;
+  double px[EPT], pd[EPT], pc[EPT], pz[EPT];
+  // x[g] of a chunk was written by this same thread in the forward pass (same row -> thread map)
+  auto load_bwd = [&](int ch) {
+    const int base = ch * CHUNK;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int g = base + t + k * PEXP_THREADS;
+      const bool ok = g < n;
+      pd[k] = ok ? di[g] : 0.0;
+      px[k] = ok ? x[g] : 0.0;
+      pc[k] = ok ? cs[g] : 0.0;
+      pz[k] = (periodic && ok) ? fz[g] : 0.0;
+    }
+  };
+  load_bwd(nchunk - 1);
   for (int ch = nchunk - 1; ch >= 0; --ch) {
     const int base = ch * CHUNK;
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
-      int si = (i / EPT) * SPAD + (i % EPT);
-      if (g < n) {
-        double dv = di[g];
-        s0[si] = dv * x[g];
-        s1[si] = -dv * cs[g];
-      } else {
-        s0[si] = 0.0;
-        s1[si] = 1.0;
-      }
+    double cz[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int i = t + k * PEXP_THREADS;
+      const int si = (i / EPT) * SPAD + (i % EPT);
+      const bool ok = base + i < n;
+      s0[si] = ok ? pd[k] * px[k] : 0.0;
+      s1[si] = ok ? -pd[k] * pc[k] : 1.0;
+      cz[k] = pz[k];
     }
     __syncthreads();
+    if (ch > 0) load_bwd(ch - 1);
     Aff m{1.0, 0.0};
 #pragma unroll
     for (int k = EPT - 1; k >= 0; --k) m = after(m, Aff{s1[t * SPAD + k], s0[t * SPAD + k]});
@@ -127,11 +160,13 @@ __device__ inline double cta_sai_solve(int n, int periodic, const double* l, con
     }
     carry = fma(tot.A, carry, tot.B);
     __syncthreads();
-    for (int i = t; i < CHUNK; i += PEXP_THREADS) {
-      int g = base + i;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int i = t + k * PEXP_THREADS;
+      const int g = base + i;
       if (g < n) {
         double v = s0[(i / EPT) * SPAD + (i % EPT)];
-        if (periodic) v = fma(-f, fz[g], v);
+        if (periodic) v = fma(-f, cz[k], v);
         x[g] = v;
         if (x2) x2[g] = v;
         nrm2 = fma(v, v, nrm2);

@@ -393,7 +393,7 @@ k_factor_par(int n, int periodic, const int* __restrict__ opidx, const double* _
 
 // Grid (ncols, E).  Column c of eval e: rhs at rhs + e*rs_e + (cin0+c)*n, result at
 // out + e*os_e + (cout0+c)*n (may alias rhs only if identical).  fidx[e] selects the factor.
-__global__ void __launch_bounds__(PEXP_THREADS)
+__global__ void __launch_bounds__(PEXP_THREADS, 2)
 k_sai_solve(int n, int periodic, const int* fidx, const double* fl, const double* fdinv,
             const double* fsup, const double* fz, const double* fw, const double* rhs,
             long long rs_e, int cin0, double* out, long long os_e, int cout0,
